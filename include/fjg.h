@@ -1,0 +1,184 @@
+/*
+ * fjg.h — C-ABI of the B200 Free Join executor (libfjg.so).
+ *
+ * The reference has no FFI layer; its API surface is the
+ * GHT interface of Fig 5 extended in SPEC.md:286-339, the
+ * executor operations of SPEC.md:387-431, the plan compiler of
+ * SPEC.md:195-240 and the typed exceptions of proj/include/fj/error.hpp:9-33.
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Every int-returning call returns FJG_OK (0) or one FJG_E_* category
+ *    (error.hpp:8: "Error categories map 1:1 onto CLI exit codes").
+ *    fjg_last_error() returns the thread-local message of the last failure.
+ *  - No exceptions and no C++/torch types cross this boundary.
+ *  - Handles are not thread-safe; distinct engines may run concurrently
+ *    (reentrant with disjoint contexts).
+ *  - fjg_execute is synchronous: it returns after its stream has drained.
+ *  - Values are int32 columns; they are widened to int64 exactly as
+ *    fj::Value (value.hpp:28-57) when hashed for the checksum.
+ */
+#ifndef FJG_H_
+#define FJG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error.hpp:9-33 categories */
+#define FJG_OK 0
+#define FJG_E_IO 1
+#define FJG_E_PARSE 2
+#define FJG_E_VALIDATION 3
+#define FJG_E_RESOURCE 4 /* cudaErrorMemoryAllocation, NCCL OOM, capacity */
+#define FJG_E_ENGINE 5   /* invariant violation or CUDA launch failure */
+
+/* plan modes (SPEC.md:463-464 RunConfig.mode) */
+#define FJG_MODE_BINARY 0
+#define FJG_MODE_FREE 1
+#define FJG_MODE_GENERIC 2
+
+/* output modes (SPEC.md:374 ExecOptions.output_mode) */
+#define FJG_OUT_COUNT 0
+#define FJG_OUT_ENUMERATE 1
+#define FJG_OUT_FACTORIZED_COUNT 2
+
+/* predicate comparators */
+#define FJG_CMP_EQ 0
+#define FJG_CMP_NE 1
+#define FJG_CMP_LT 2
+#define FJG_CMP_LE 3
+#define FJG_CMP_GT 4
+#define FJG_CMP_GE 5
+
+#define FJG_MAX_NODES 32
+
+typedef struct fjg_engine fjg_engine;
+typedef struct fjg_relation fjg_relation;
+typedef struct fjg_query fjg_query;
+
+/* ExecOptions. batch_size is the iter_batch size of
+ * Fig 13: on the device it bounds the number of cover
+ * candidates expanded per node launch (0 = engine default, 2^24). */
+typedef struct {
+  uint64_t batch_size;
+  int32_t dynamic_cover; /* §4.4 select_cover */
+  int32_t output_mode;   /* FJG_OUT_* */
+  int32_t min_var;       /* head-variable index aggregated with MIN, or -1 */
+  int32_t collect_timing;/* record build/join phase times (CUDA events) */
+} fjg_exec_options;
+
+/* Result: OutputSink counter + ExecStats/TrieStats
+ * (SPEC.md:377-380, :280-283). count is 128-bit (count_hi:count_lo). */
+typedef struct {
+  uint64_t count_lo;
+  uint64_t count_hi;
+  uint64_t checksum;          /* sum mult*fmix64(TupleHash(t)) mod 2^64 */
+  int64_t min_value;          /* valid iff has_min */
+  int32_t has_min;
+  int32_t num_nodes;
+  uint64_t output_rows;       /* enumerate mode: rows available via fjg_query_output */
+  uint64_t probes;            /* get() calls issued by the executor */
+  uint64_t probe_misses;
+  uint64_t node_body_entries[FJG_MAX_NODES];
+  uint64_t maps_built;        /* subtries forced (TrieStats.maps_built) */
+  uint64_t keys_inserted;     /* distinct keys inserted into COLT maps */
+  uint64_t forces;            /* force batches executed on the device */
+  uint64_t rows_forced;       /* offsets regrouped by forcing */
+  double build_ms;            /* device time in COLT forcing (if collect_timing) */
+  double join_ms;             /* device time in node kernels (if collect_timing) */
+  uint32_t kernel_launches;   /* kernels this library launched for the call */
+  uint32_t host_syncs;
+} fjg_result;
+
+typedef struct {
+  int32_t column;
+  int32_t cmp;      /* FJG_CMP_* */
+  int32_t is_column;/* 1: compare against column `rhs_column` (attr = attr form) */
+  int32_t rhs_column;
+  int64_t constant;
+} fjg_predicate;
+
+/* ---- errors ---- */
+const char* fjg_last_error(void);
+int fjg_abi_version(void);
+
+/* ---- plan compiler (host C++) ----
+ * Strings use the plan-file dialect of SPEC.md:171. Output buffers follow the
+ * snprintf convention: *needed receives strlen+1; FJG_E_RESOURCE if cap is
+ * too small. */
+/* run pipeline SPEC.md:475 up to schemas: decompose -> binary2fj ->
+ * (factor if FREE) -> (fj_to_gj_plan if GENERIC) -> validate */
+int fjg_compile_plan(const char* query_json, int mode, int factor_fixpoint, char* out, size_t cap,
+                     size_t* needed);
+/* op: "binary2fj" (arg: JSON list of relation names, a left-deep segment),
+ * "factor" / "factor_fixpoint" / "fj_to_gj" / "schemas" / "validate" /
+ * "gj_order" (arg: FJ plan JSON), "covers" / "vs" / "avs" (arg:
+ * {"plan": plan, "k": k}), "decompose" (arg: binary tree JSON),
+ * "head_vars" (arg ignored). */
+int fjg_plan_op(const char* op, const char* query_json, const char* arg_json, char* out, size_t cap,
+                size_t* needed);
+
+/* ---- engine (one per device/stream) ---- */
+int fjg_engine_create(int device, fjg_engine** out);
+void fjg_engine_destroy(fjg_engine* eng);
+/* Wait for all work of the engine's stream. */
+int fjg_engine_sync(fjg_engine* eng);
+
+/* ---- relations: immutable columnar int32 tables ---- */
+/* Copies host columns to the device (cudaMemcpyAsync per column). */
+int fjg_relation_create(fjg_engine* eng, const int32_t* const* host_cols, int ncols, uint64_t nrows,
+                        fjg_relation** out);
+/* Wraps (copy=0: zero-copy alias, caller keeps the memory alive) or copies
+ * (copy=1) device columns. */
+int fjg_relation_from_device(fjg_engine* eng, const int32_t* const* dev_cols, int ncols, uint64_t nrows,
+                             int copy, fjg_relation** out);
+/* apply_filter: conjunction of predicates, row order kept. */
+int fjg_relation_filter(const fjg_relation* in, const fjg_predicate* preds, int npreds,
+                        fjg_relation** out);
+uint64_t fjg_relation_rows(const fjg_relation* rel);
+int fjg_relation_cols(const fjg_relation* rel);
+const int32_t* fjg_relation_device_col(const fjg_relation* rel, int col);
+int fjg_relation_download(const fjg_relation* rel, int col, int32_t* host_out);
+void fjg_relation_destroy(fjg_relation* rel);
+
+/* ---- multi-GPU partitioning (north_star (c)) ----
+ * Hash-partition `in` on column `col` into nparts destinations:
+ * out_rel holds the rows grouped by destination (stable within a
+ * destination), counts[d] the rows for destination d. */
+int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_relation** out_rel,
+                           uint64_t* counts);
+
+/* ---- queries: build phase + join phase ----
+ * query_json: {"query":[{"rel":..,"vars":[..]},..]}; plan_json: a Free Join
+ * plan in the SPEC.md:171 dialect. atom_rels[i] binds query atom i; several
+ * atoms may bind the same relation (renamed self-joins) and
+ * then share device COLT levels. */
+int fjg_query_create(fjg_engine* eng, const char* query_json, const char* plan_json,
+                     fjg_relation* const* atom_rels, int natoms, fjg_query** out);
+/* One full execution: GHT new (BaseScan) for every atom, then
+ * join_vectorized (Fig 13) with lazy COLT forcing; the last node fuses the
+ * count/checksum/MIN aggregation (or writes tuples in enumerate mode). */
+int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out);
+/* Enumerate mode: copy up to cap_rows output tuples (head-variable order,
+ * row-major, num_head_vars int32 each, unsorted bag) to host_out. */
+int fjg_query_output(fjg_query* q, int32_t* host_out, uint64_t cap_rows, uint64_t* rows);
+int fjg_query_num_head_vars(const fjg_query* q);
+void fjg_query_destroy(fjg_query* q);
+
+/* ---- test hooks ---- */
+/* TupleHash (value.hpp:61-67) of `ntuples` int64 tuples of `arity` values,
+ * computed by a device kernel; used to pin the device hash against the
+ * reference KATs. */
+int fjg_device_tuple_hash(fjg_engine* eng, const int64_t* host_vals, int arity, uint64_t ntuples,
+                          uint64_t* host_out);
+uint64_t fjg_host_tuple_hash(const int64_t* vals, int arity);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FJG_H_ */

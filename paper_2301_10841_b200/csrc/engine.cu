@@ -1,0 +1,1564 @@
+// B200 Free Join executor: device COLT + vectorised node execution.
+//
+// Reference map (all behaviour restated from the SPEC/paper; no reference code
+// exists for this path):
+//   GHT new / BaseScan
+//   COLT force / get / iter   SPEC.md:295-330, Fig 12
+//   estimated_key_count
+//   select_cover (dynamic)
+//   join_vectorized (Fig 13)
+//   output sinks / counters
+//
+// Execution model: breadth-first within a chunk, depth-first over chunks.
+// Node k receives a frontier of bindings (SoA: bound variables, per-atom
+// current subtrie (id, len), multiplicity). One node =
+//   k_select   per binding: dynamic cover (min estimated_key_count, ties to the
+//              lowest position), candidate count, claims of unforced subtries
+//              every probe/keys-iteration of this node needs (lazy forcing in
+//              batch, deduplicated by CAS on the subtrie state)
+//   scan       inclusive scan of candidate counts (CUB)
+//   force      per (trie, level) with claims: insert -> assign -> scatter
+//   k_expand   per candidate (load-balanced over the scan): iterate the cover,
+//              probe every other subatom in node order, drop misses, compact
+//              survivors into the next frontier -- or, at the last node, fold
+//              count / checksum / MIN (or write tuples) in registers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fjg.h"
+#include "engine.cuh"
+#include "fj_errors.hpp"
+#include "fj_plan.hpp"
+
+namespace fjg {
+void set_last_error(const std::string& s);
+}
+
+using namespace fjg;
+
+// ============================================================================
+// errors
+// ============================================================================
+static void throw_cuda(cudaError_t e, const char* what, int line) {
+  std::string msg = std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " (engine.cu:" +
+                    std::to_string(line) + ")";
+  if (e == cudaErrorMemoryAllocation) throw fj::ResourceError(msg);
+  throw fj::EngineError(msg);
+}
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t _e = (x);                      \
+    if (_e != cudaSuccess) throw_cuda(_e, #x, __LINE__); \
+  } while (0)
+
+// ============================================================================
+// device helpers
+// ============================================================================
+__device__ __forceinline__ const int32_t* level_src(const DevTrie& T, int depth, int col) {
+  return depth == 0 ? T.base[col] : T.lev[depth - 1].cval[col];
+}
+
+__device__ __forceinline__ uint32_t key_word(int nk, const int32_t* vals) {
+  if (nk == 0) return 0u;
+  if (nk == 1) return static_cast<uint32_t>(vals[0]);
+  uint64_t h = fj::kTupleHashSeed;
+  for (int t = 0; t < nk; ++t) h = fj::tuple_hash_step(h, vals[t]);
+  return static_cast<uint32_t>(fj::fmix64(h));
+}
+
+__device__ __forceinline__ uint4 ld_slot(const Slot* s) {
+  return __ldg(reinterpret_cast<const uint4*>(s));
+}
+
+// COLT get (Fig 12 `get`: force then lookup). The subtrie is forced before
+// the probing kernel runs, so this is a pure lookup.
+__device__ __forceinline__ bool colt_get(const DevLevel& L, uint32_t p, int nk, const int32_t* vals,
+                                         uint32_t& q, uint32_t& len) {
+  const uint32_t kw = key_word(nk, vals);
+  uint64_t h = fj::slot_hash(p, kw) & L.mask;
+  while (true) {
+    uint4 s = ld_slot(L.table + h);
+    if (s.x == kEmpty) return false;
+    if (s.x == p && s.y == kw) {
+      bool eq = true;
+      if (nk >= 2)
+        for (int t = 0; t < nk; ++t)
+          if (L.cval[L.keycol[t]][s.z] != vals[t]) eq = false;
+      if (eq) {
+        q = s.z;
+        len = s.w;
+        return true;
+      }
+    }
+    h = (h + 1) & L.mask;
+  }
+}
+
+// subtrie of sub's atom for frontier entry e (root if the atom is untouched)
+__device__ __forceinline__ void subtrie_of(const DevNode& N, const DevSub& S, uint64_t e, uint32_t& p,
+                                           uint32_t& len) {
+  if ((N.in_atoms >> S.atom) & 1u) {
+    p = N.in.p[S.atom][e];
+    len = N.in.len[S.atom][e];
+  } else {
+    p = 0;
+    len = N.atom_n[S.atom];
+  }
+}
+
+// estimated_key_count: forced map -> #keys, vector -> length,
+// BaseScan -> cardinality; never forces.
+__device__ __forceinline__ uint64_t estimate(const DevTrie* tries, const DevSub& S, uint32_t p, uint32_t len) {
+  if (p == kSingleton) return 1;
+  const DevLevel& L = tries[S.trie].lev[S.depth];
+  uint32_t st = *((volatile uint32_t*)(L.state + (S.depth == 0 ? 0 : p)));
+  if (st == 2) return L.nkeys[S.depth == 0 ? 0 : p];
+  return len;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ============================================================================
+// k_select: cover choice, candidate counts, force claims
+// ============================================================================
+__device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters* ctr, const DevSub& S, uint32_t p,
+                                              uint32_t len, bool need) {
+  // Warp-level dedup of identical subtries (bindings of one parent are
+  // adjacent in the frontier), then a CAS on the state word.
+  const unsigned act = __activemask();
+  const unsigned want = __ballot_sync(act, need);
+  if (!need) return;
+  const unsigned grp = __match_any_sync(want, p);
+  const int leader = __ffs(grp) - 1;
+  if ((threadIdx.x & 31) != leader) return;
+  if (S.depth == 0) {
+    ctr->root_need[S.trie] = 1;
+    return;
+  }
+  const DevLevel& L = tries[S.trie].lev[S.depth];
+  if (atomicCAS(L.state + p, 0u, 1u) == 0u) {
+    L.cursor[p] = 0;
+    L.nkeys[p] = 0;
+    uint32_t idx = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], 1u);
+    L.list_p[idx] = p;
+    L.list_len[idx] = len;
+  }
+}
+
+__global__ void k_select(const DevNode* __restrict__ nd, const DevTrie* __restrict__ tries, uint64_t F,
+                         int dynamic, DevCounters* ctr) {
+  const DevNode& N = *nd;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t iters = (F + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t e = start + it * stride;
+    const bool ok = e < F;
+    int best = N.cov[0];
+    uint32_t bp = 0, bl = 0;
+    if (ok) {
+      subtrie_of(N, N.sub[best], e, bp, bl);
+      if (dynamic && N.ncov > 1) {
+        uint64_t best_est = estimate(tries, N.sub[best], bp, bl);
+        for (int ci = 1; ci < N.ncov; ++ci) {
+          const int s = N.cov[ci];
+          uint32_t p, l;
+          subtrie_of(N, N.sub[s], e, p, l);
+          const uint64_t est = estimate(tries, N.sub[s], p, l);
+          if (est < best_est) {
+            best_est = est;
+            best = s;
+            bp = p;
+            bl = l;
+          }
+        }
+      }
+      N.chosen[e] = (uint8_t)best;
+      N.m[e] = (bp == kSingleton) ? 1ull : (uint64_t)bl;
+    }
+    // claims: the keys-iterated cover and every probed subatom must be forced
+    for (int s = 0; s < N.nsub; ++s) {
+      const DevSub& S = N.sub[s];
+      uint32_t p = 0, l = 0;
+      bool need = false;
+      if (ok) {
+        subtrie_of(N, S, e, p, l);
+        need = (p != kSingleton) && (s != best || !S.stream);
+        if (need) {
+          const DevLevel& L = tries[S.trie].lev[S.depth];
+          need = *((volatile uint32_t*)(L.state + (S.depth == 0 ? 0 : p))) == 0u;
+        }
+      }
+      claim_subtrie(tries, ctr, S, p, l, need);
+    }
+  }
+}
+
+// ============================================================================
+// force: insert -> assign -> scatter -> finalize  (Fig 12 `force`)
+// ============================================================================
+// Position iteration over the union of claimed ranges. SINGLE: one subtrie
+// (p0, len0) given by value (the root BaseScan, or a lone claim).
+struct ForceRange {
+  const uint32_t* list_p;
+  const uint32_t* list_len;
+  const uint32_t* list_scan;  // inclusive
+  const uint32_t* list_count; // device count
+  uint32_t p0, len0;
+  int single;
+};
+
+__device__ __forceinline__ uint32_t force_total(const ForceRange& R) {
+  if (R.single) return R.len0;
+  const uint32_t c = *R.list_count;
+  return c ? R.list_scan[c - 1] : 0u;
+}
+
+__device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, uint32_t& p, uint32_t& pos) {
+  if (R.single) {
+    p = R.p0;
+    pos = R.p0 + i;
+    return;
+  }
+  uint32_t lo = 0, hi = *R.list_count - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (R.list_scan[mid] > i)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const uint32_t before = lo ? R.list_scan[lo - 1] : 0u;
+  p = R.list_p[lo];
+  pos = p + (i - before);
+}
+
+template <bool MULTI>
+__global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                               uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
+                               uint32_t* __restrict__ newslots, DevCounters* ctr) {
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[lev];
+  const uint32_t total = force_total(R);
+  const int nk = L.nk;
+  const int32_t* src[MAXK];
+  for (int t = 0; t < nk; ++t) src[t] = level_src(T, lev, L.keycol[t]);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, pos;
+    force_locate(R, i, p, pos);
+    int32_t vals[MAXK];
+    for (int t = 0; t < nk; ++t) vals[t] = src[t][pos];
+    const uint32_t kw = key_word(nk, vals);
+    const unsigned long long pk = ((unsigned long long)kw << 32) | p;
+    uint64_t h = fj::slot_hash(p, kw) & L.mask;
+    bool won = false;
+    while (true) {
+      unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
+      unsigned long long cur = *((volatile unsigned long long*)addr);
+      if (cur == kEmpty64) {
+        unsigned long long old = atomicCAS(addr, kEmpty64, pk);
+        if (old == kEmpty64) {
+          won = true;
+          if (MULTI) {
+            *((volatile uint32_t*)(L.srep + h)) = pos + 1;
+            __threadfence();
+          }
+          break;
+        }
+        cur = old;
+      }
+      if (cur == pk) {
+        if (!MULTI) break;
+        uint32_t r;
+        while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
+        }
+        bool eq = true;
+        for (int t = 0; t < nk; ++t)
+          if (src[t][r - 1] != vals[t]) eq = false;
+        if (eq) break;
+      }
+      h = (h + 1) & L.mask;
+    }
+    const uint32_t rank = atomicAdd(&L.table[h].len, 1u);
+    tmp_slot[pos] = (uint32_t)h;
+    tmp_rank[pos] = rank;
+    L.cnt[pos] = 0;  // child starts are written by k_force_assign
+    // warp-aggregated append of new slots
+    const unsigned act = __activemask();
+    const unsigned wmask = __ballot_sync(act, won);
+    if (won) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(wmask) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&ctr->newslots, (uint32_t)__popc(wmask));
+      base = __shfl_sync(wmask, base, leader);
+      newslots[base + __popc(wmask & ((1u << lane) - 1))] = (uint32_t)h;
+    }
+  }
+}
+
+// Child-range allocation: q = p + (running sum of child sizes of p).
+template <bool SINGLE>
+__global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0,
+                               const uint32_t* __restrict__ newslots, DevCounters* ctr) {
+  const DevLevel& L = tries[trie].lev[lev];
+  const uint32_t total = ctr->newslots;
+  typedef cub::BlockScan<uint32_t, 256> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t s_base;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t iters = (total + stride - 1) / stride;
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
+    const bool ok = i < total;
+    uint32_t h = 0, c = 0, p = 0;
+    if (ok) {
+      h = newslots[i];
+      p = L.table[h].p;
+      c = L.table[h].len;
+    }
+    uint32_t q = 0;
+    if (SINGLE) {
+      uint32_t excl, blk_total;
+      BS(tmp).ExclusiveSum(c, excl, blk_total);
+      if (threadIdx.x == 0) {
+        const uint32_t first = blockIdx.x * blockDim.x + it * stride;
+        if (first < total) {
+          const uint32_t nb = min((uint32_t)blockDim.x, total - first);
+          s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);
+          atomicAdd(&L.nkeys[p0], nb);
+        }
+      }
+      __syncthreads();
+      q = s_base + excl;
+      __syncthreads();
+    } else if (ok) {
+      const unsigned act = __activemask();
+      const unsigned grp = __match_any_sync(act, p);
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(grp) - 1;
+      uint32_t pre = 0, tot = 0;
+      unsigned m = grp;
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t cl = __shfl_sync(grp, c, l);
+        if (l < lane) pre += cl;
+        tot += cl;
+      }
+      uint32_t base = 0;
+      if (lane == leader) {
+        base = atomicAdd(&L.cursor[p], tot);
+        atomicAdd(&L.nkeys[p], (uint32_t)__popc(grp));
+      }
+      base = __shfl_sync(grp, base, leader);
+      q = p + base + pre;
+    }
+    if (ok) {
+      L.table[h].q = q;
+      L.cnt[q] = c;
+    }
+  }
+}
+
+__global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                                const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank) {
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[lev];
+  const uint32_t total = force_total(R);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, pos;
+    force_locate(R, i, p, pos);
+    const uint32_t h = tmp_slot[pos];
+    const uint32_t dst = L.table[h].q + tmp_rank[pos];
+    for (int c = 0; c < T.ncols; ++c) {
+      int32_t* out = L.cval[c];
+      if (out) out[dst] = level_src(T, lev, c)[pos];
+    }
+  }
+}
+
+__global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
+  const DevLevel& L = tries[trie].lev[lev];
+  if (R.single) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
+    return;
+  }
+  const uint32_t c = *R.list_count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+    L.state[R.list_p[i]] = 2u;
+}
+
+// ============================================================================
+// k_expand: iterate cover, probe, compact / aggregate  (Fig 13)
+// ============================================================================
+enum ExpandMode { EXPAND_WRITE = 0, EXPAND_COUNT = 1, EXPAND_ENUM = 2 };
+
+__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t lo, uint64_t hi, uint64_t x) {
+  // first index in [lo, hi] with a[idx] > x (a[hi] > x guaranteed)
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] > x)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_expand(const DevNode* __restrict__ nd, const DevTrie* __restrict__ tries,
+                                                uint64_t c0, uint64_t c1, uint64_t F, int min_var,
+                                                int32_t* __restrict__ out_tuples, uint64_t out_cap,
+                                                DevCounters* ctr) {
+  const DevNode& N = *nd;
+  __shared__ uint64_t s_lo, s_hi;
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_base;
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * blockDim.x; base < c1; base += (uint64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) {
+      s_lo = upper_bound_u64(N.scan, 0, F - 1, base);
+      const uint64_t last = min(base + blockDim.x, c1) - 1;
+      s_hi = upper_bound_u64(N.scan, s_lo, F - 1, last);
+    }
+    __syncthreads();
+    const uint64_t i = base + threadIdx.x;
+    bool alive = i < c1;
+    int32_t val[MAXV];
+    uint32_t cp[MAXA], cl[MAXA];
+    uint64_t mult = 1;
+    uint64_t e = 0;
+    if (alive) {
+      e = upper_bound_u64(N.scan, s_lo, s_hi, i);
+      const uint64_t j = i - (e ? N.scan[e - 1] : 0ull);
+      for (int v = 0; v < MAXV; ++v)
+        if ((N.in_vars >> v) & 1u) val[v] = N.in.var[v][e];
+      for (int a = 0; a < MAXA; ++a)
+        if ((N.in_atoms >> a) & 1u) {
+          cp[a] = N.in.p[a][e];
+          cl[a] = N.in.len[a][e];
+        }
+      if (N.in.mult) mult = N.in.mult[e];
+      // ---- iterate the chosen cover ----
+      const int ci = N.chosen[e];
+      const DevSub& S = N.sub[ci];
+      uint32_t p, len;
+      subtrie_of(N, S, e, p, len);
+      const DevTrie& T = tries[S.trie];
+      if (p == kSingleton) {
+        cp[S.atom] = kSingleton;
+        cl[S.atom] = 1;
+      } else {
+        const uint32_t pos = p + (uint32_t)j;
+        if (S.stream) {
+          // Fig 12 iter, suffix branch: stream the values at the offsets
+          for (int t = 0; t < S.nv; ++t) {
+            const int32_t x = level_src(T, S.depth, S.col[t])[pos];
+            const int v = S.var[t];
+            if ((S.bound_mask >> t) & 1) {
+              if (val[v] != x) alive = false;
+            } else {
+              val[v] = x;
+            }
+          }
+          cp[S.atom] = kSingleton;
+          cl[S.atom] = 1;
+        } else {
+          // Fig 12 iter, forced map: iterate distinct keys = child starts
+          const DevLevel& L = T.lev[S.depth];
+          const uint32_t c = L.cnt[pos];
+          if (c == 0) {
+            alive = false;
+          } else {
+            for (int t = 0; t < S.nv; ++t) {
+              const int32_t x = L.cval[S.col[t]][pos];
+              const int v = S.var[t];
+              if ((S.bound_mask >> t) & 1) {
+                if (val[v] != x) alive = false;
+              } else {
+                val[v] = x;
+              }
+            }
+            cp[S.atom] = pos;
+            cl[S.atom] = c;
+          }
+        }
+      }
+      if (alive) ++body;
+      // ---- probe every other subatom in node order ----
+      for (int s = 0; s < N.nsub && alive; ++s) {
+        if (s == ci) continue;
+        const DevSub& P = N.sub[s];
+        uint32_t pp, pl;
+        subtrie_of(N, P, e, pp, pl);
+        uint32_t q = kSingleton, ql = 1;
+        if (pp != kSingleton) {
+          int32_t key[MAXK];
+          for (int t = 0; t < P.nv; ++t) key[t] = val[P.var[t]];
+          ++probes;
+          if (!colt_get(tries[P.trie].lev[P.depth], P.depth == 0 ? 0u : pp, P.nv, key, q, ql)) {
+            ++misses;
+            alive = false;
+            break;
+          }
+        }
+        if (P.last)
+          mult *= ql;  // residual leaf vector: its offsets are the multiplicity
+        cp[P.atom] = q;
+        cl[P.atom] = ql;
+      }
+    }
+    if (MODE == EXPAND_WRITE) {
+      const unsigned bal = __ballot_sync(0xffffffffu, alive);
+      if (lane == 0) s_warp[warp] = __popc(bal);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+          const uint32_t t = s_warp[w];
+          s_warp[w] = tot;
+          tot += t;
+        }
+        s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
+      }
+      __syncthreads();
+      if (alive) {
+        const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
+        for (int v = 0; v < MAXV; ++v)
+          if ((N.out_vars >> v) & 1u) N.out.var[v][o] = val[v];
+        for (int a = 0; a < MAXA; ++a)
+          if ((N.out_atoms >> a) & 1u) {
+            N.out.p[a][o] = cp[a];
+            N.out.len[a][o] = cl[a];
+          }
+        if (N.out.mult) N.out.mult[o] = mult;
+      }
+    } else if (alive) {
+      if (MODE == EXPAND_COUNT) {
+        uint64_t h = fj::kTupleHashSeed;
+        for (int v = 0; v < N.nhead; ++v) h = fj::tuple_hash_step(h, (int64_t)val[v]);
+        acc_sum += mult * fj::checksum_word(h);
+        acc_lo += mult;
+        if (acc_lo < mult) ++acc_hi;
+        if (min_var >= 0) acc_min = min(acc_min, (long long)val[min_var]);
+      } else {
+        const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
+        for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
+          for (int v = 0; v < N.nhead; ++v) out_tuples[(o + r) * N.nhead + v] = val[v];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- flush per-thread accumulators: one atomic per warp ----
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  if (lane == 0) {
+    if (probes) atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+  }
+  if (MODE == EXPAND_COUNT) {
+    // 128-bit count: carry out of the low word
+    uint64_t lo = acc_lo, hi = acc_hi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+      const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      const uint64_t s = lo + l2;
+      hi += h2 + (s < lo ? 1 : 0);
+      lo = s;
+    }
+    acc_sum = warp_sum(acc_sum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+    if (lane == 0) {
+      if (lo) {
+        const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo);
+        if (old + lo < old) ++hi;
+      }
+      if (hi) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi);
+      if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+      if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+    }
+  }
+}
+
+// ============================================================================
+// misc kernels
+// ============================================================================
+__global__ void k_fill_slots(Slot* t, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(t)[i] = make_uint4(kEmpty, kEmpty, 0u, 0u);
+}
+
+__global__ void k_tuple_hash(const int64_t* vals, int arity, uint64_t n, uint64_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t h = fj::kTupleHashSeed;
+    for (int t = 0; t < arity; ++t) h = fj::tuple_hash_step(h, vals[i * arity + t]);
+    out[i] = h;
+  }
+}
+
+__device__ __forceinline__ bool cmp_eval(int cmp, int64_t a, int64_t b) {
+  switch (cmp) {
+    case FJG_CMP_EQ: return a == b;
+    case FJG_CMP_NE: return a != b;
+    case FJG_CMP_LT: return a < b;
+    case FJG_CMP_LE: return a <= b;
+    case FJG_CMP_GT: return a > b;
+    default: return a >= b;
+  }
+}
+
+struct DevPreds {
+  int n;
+  fjg_predicate p[8];
+  const int32_t* cols[MAXC];
+};
+
+__global__ void k_filter_flags(DevPreds P, uint64_t n, uint32_t* flags) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    for (int k = 0; k < P.n; ++k) {
+      const int64_t a = P.cols[P.p[k].column][i];
+      const int64_t b = P.p[k].is_column ? (int64_t)P.cols[P.p[k].rhs_column][i] : P.p[k].constant;
+      ok = ok && cmp_eval(P.p[k].cmp, a, b);
+    }
+    flags[i] = ok ? 1u : 0u;
+  }
+}
+
+__global__ void k_compact_col(const int32_t* in, const uint32_t* flags, const uint32_t* excl, uint64_t n, int32_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (flags[i]) out[excl[i]] = in[i];
+}
+
+__global__ void k_partition_flags(const int32_t* col, uint64_t n, int nparts, int part, uint32_t* flags) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    flags[i] = fj::partition_of(col[i], (uint32_t)nparts) == (uint32_t)part ? 1u : 0u;
+}
+
+// ============================================================================
+// host: memory pool
+// ============================================================================
+namespace {
+
+class Pool {
+ public:
+  explicit Pool(int dev) : dev_(dev) {}
+  ~Pool() {
+    for (auto& kv : free_) cudaFree(kv.second);
+    for (auto& kv : live_) cudaFree(kv.first);
+  }
+  void* alloc(size_t bytes) {
+    if (bytes == 0) bytes = 1;
+    const size_t gran = bytes >= (1u << 20) ? (2u << 20) : 512;
+    bytes = (bytes + gran - 1) / gran * gran;
+    auto it = free_.lower_bound(bytes);
+    if (it != free_.end() && it->first <= bytes * 2) {
+      void* p = it->second;
+      live_[p] = it->first;
+      free_.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      release_free();
+      e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw fj::ResourceError("device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                                cudaGetErrorString(e));
+      }
+    }
+    live_[p] = bytes;
+    return p;
+  }
+  void free(void* p) {
+    if (!p) return;
+    auto it = live_.find(p);
+    if (it == live_.end()) return;
+    free_.emplace(it->second, p);
+    live_.erase(it);
+  }
+  void release_free() {
+    for (auto& kv : free_) cudaFree(kv.second);
+    free_.clear();
+  }
+
+ private:
+  int dev_;
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> live_;
+};
+
+inline unsigned grid_for(uint64_t n, int threads = 256, unsigned cap = 148u * 16u) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+uint64_t pow2_at_least(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+// ============================================================================
+// host: handles
+// ============================================================================
+struct fjg_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Pool> pool;
+  uint32_t launches = 0;
+  uint32_t syncs = 0;
+  int num_sms = 148;
+};
+
+struct fjg_relation {
+  fjg_engine* eng = nullptr;
+  uint64_t nrows = 0;
+  int ncols = 0;
+  std::vector<int32_t*> cols;
+  std::vector<void*> owned;
+};
+
+namespace {
+
+struct ScopedDevice {
+  int prev = -1;
+  explicit ScopedDevice(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~ScopedDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+#define LAUNCH(eng, ...)          \
+  do {                            \
+    __VA_ARGS__;                  \
+    ++(eng)->launches;            \
+    CK(cudaGetLastError());       \
+  } while (0)
+
+struct PhysLevelHost {
+  std::vector<int> keycols;
+  bool multi = false;
+  uint64_t cap = 0;
+  uint64_t nsub = 0;  // entries of state/nkeys/cursor (1 at level 0)
+  bool dirty = true;
+};
+
+struct PhysTrieHost {
+  fjg_relation* rel = nullptr;
+  std::vector<std::vector<int>> levels;
+  std::vector<PhysLevelHost> lev;
+  DevTrie dev{};
+  bool root_forced = false;
+};
+
+struct AtomInfo {
+  int rel_index;
+  std::vector<int> vars;  // var ids, column order
+  std::vector<std::pair<int, int>> subs;  // (node, position) in node order
+  int trie = -1;
+};
+
+}  // namespace
+
+struct fjg_query {
+  fjg_engine* eng = nullptr;
+  fj::FreeJoinPlan plan;
+  std::vector<std::string> head;  // variable names, id order
+  std::vector<AtomInfo> atoms;
+  std::vector<fjg_relation*> rels;
+  std::vector<PhysTrieHost> tries;
+  std::vector<DevNode> nodes;  // host copies
+  DevNode* d_nodes = nullptr;
+  DevTrie* d_tries = nullptr;
+  DevCounters* d_ctr = nullptr;
+  DevCounters* h_ctr = nullptr;  // pinned
+  uint64_t* h_scratch = nullptr; // pinned
+  std::vector<void*> bufs;       // pool allocations of this query
+  uint64_t cap = 0;              // frontier capacity (candidates per chunk)
+  uint64_t max_n = 0;
+  uint32_t* tmp_slot = nullptr;
+  uint32_t* tmp_rank = nullptr;
+  uint32_t* newslots = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_tmp_bytes = 0;
+  int32_t* out_tuples = nullptr;
+  uint64_t out_cap = 0;
+  uint64_t out_rows = 0;
+  // per-execute stats
+  uint64_t maps_built = 0, forces = 0, rows_forced = 0;
+  bool dynamic = true;
+  uint64_t batch = 0;
+  int min_var = -1;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double build_ms = 0, join_ms = 0;
+  bool timing = false;
+
+  void* alloc(size_t bytes) {
+    void* p = eng->pool->alloc(bytes);
+    bufs.push_back(p);
+    return p;
+  }
+  ~fjg_query() {
+    if (eng) {
+      for (void* p : bufs) eng->pool->free(p);
+      if (h_ctr) cudaFreeHost(h_ctr);
+      if (h_scratch) cudaFreeHost(h_scratch);
+      if (ev0) cudaEventDestroy(ev0);
+      if (ev1) cudaEventDestroy(ev1);
+    }
+  }
+};
+
+// ============================================================================
+// query preparation
+// ============================================================================
+static void prepare_query(fjg_query* q) {
+  using fj::EngineError;
+  using fj::ValidationError;
+  const auto& plan = q->plan;
+  const size_t A = plan.query.size();
+  if (A > (size_t)MAXA) throw ValidationError("too many atoms for the device executor (max 16)");
+  if (plan.nodes.size() > (size_t)MAXN) throw ValidationError("too many plan nodes (max 32)");
+  q->head = fj::head_variables(plan.query);
+  if (q->head.size() > (size_t)MAXV) throw ValidationError("too many variables (max 16)");
+  std::map<std::string, int> vid;
+  for (size_t i = 0; i < q->head.size(); ++i) vid[q->head[i]] = (int)i;
+  std::map<std::string, int> aid;
+  q->atoms.resize(A);
+  for (size_t a = 0; a < A; ++a) {
+    aid[plan.query[a].relation] = (int)a;
+    for (auto& x : plan.query[a].vars) q->atoms[a].vars.push_back(vid[x]);
+    if (q->atoms[a].vars.empty()) throw ValidationError("nullary atoms are not supported on the device");
+    if ((int)q->atoms[a].vars.size() != q->rels[a]->ncols)
+      throw ValidationError("atom " + plan.query[a].relation + " has " + std::to_string(q->atoms[a].vars.size()) +
+                            " variables but its relation has " + std::to_string(q->rels[a]->ncols) + " columns");
+    if (q->rels[a]->ncols > MAXC) throw ValidationError("too many columns (max 8)");
+    if (q->rels[a]->nrows >= 0xFFFFFFF0ull) throw ValidationError("relation too large (rows must be < 2^32-16)");
+  }
+  for (size_t k = 0; k < plan.nodes.size(); ++k) {
+    const auto& subs = plan.nodes[k].subatoms;
+    if (subs.size() > (size_t)MAXS) throw ValidationError("too many subatoms in a node (max 12)");
+    for (size_t i = 0; i < subs.size(); ++i) {
+      auto it = aid.find(subs[i].relation);
+      if (it == aid.end()) throw ValidationError("plan references unknown relation " + subs[i].relation);
+      if (subs[i].vars.size() > (size_t)MAXK) throw ValidationError("subatom arity above 6");
+      q->atoms[it->second].subs.emplace_back((int)k, (int)i);
+    }
+  }
+  // column index of a variable within atom a
+  auto col_of = [&](int a, const std::string& x) {
+    const auto& vars = plan.query[a].vars;
+    for (size_t c = 0; c < vars.size(); ++c)
+      if (vars[c] == x) return (int)c;
+    throw EngineError("variable " + x + " not in atom");
+  };
+  // physical tries (share identical or prefix-equal level key columns)
+  for (size_t a = 0; a < A; ++a) {
+    std::vector<std::vector<int>> levels;
+    for (auto& [k, i] : q->atoms[a].subs) {
+      std::vector<int> cols;
+      for (auto& x : plan.nodes[k].subatoms[i].vars) cols.push_back(col_of((int)a, x));
+      levels.push_back(cols);
+    }
+    int found = -1;
+    for (size_t t = 0; t < q->tries.size(); ++t) {
+      auto& T = q->tries[t];
+      if (T.rel != q->rels[a]) continue;
+      size_t m = std::min(T.levels.size(), levels.size());
+      if (std::equal(levels.begin(), levels.begin() + m, T.levels.begin())) {
+        if (levels.size() > T.levels.size()) T.levels = levels;
+        found = (int)t;
+        break;
+      }
+    }
+    if (found < 0) {
+      if (q->tries.size() >= (size_t)MAXT) throw ValidationError("too many physical tries");
+      PhysTrieHost T;
+      T.rel = q->rels[a];
+      T.levels = levels;
+      q->tries.push_back(T);
+      found = (int)q->tries.size() - 1;
+    }
+    q->atoms[a].trie = found;
+  }
+  // allocate trie storage
+  for (size_t t = 0; t < q->tries.size(); ++t) {
+    auto& T = q->tries[t];
+    const uint64_t n = T.rel->nrows;
+    q->max_n = std::max(q->max_n, n);
+    if (T.levels.size() > (size_t)MAXL) throw ValidationError("too many trie levels (max 8)");
+    DevTrie& D = T.dev;
+    memset(&D, 0, sizeof(D));
+    D.n = (uint32_t)n;
+    D.ncols = T.rel->ncols;
+    D.nlev = (int)T.levels.size();
+    for (int c = 0; c < T.rel->ncols; ++c) D.base[c] = T.rel->cols[c];
+    T.lev.resize(T.levels.size());
+    for (size_t l = 0; l < T.levels.size(); ++l) {
+      auto& H = T.lev[l];
+      DevLevel& L = D.lev[l];
+      H.keycols = T.levels[l];
+      H.multi = H.keycols.size() >= 2;
+      H.nsub = l == 0 ? 1 : std::max<uint64_t>(n, 1);
+      H.cap = pow2_at_least(std::max<uint64_t>(2 * n, 16));
+      L.table = (Slot*)q->alloc(H.cap * sizeof(Slot));
+      L.mask = H.cap - 1;
+      L.srep = H.multi ? (uint32_t*)q->alloc(H.cap * 4) : nullptr;
+      L.state = (uint32_t*)q->alloc(H.nsub * 4);
+      L.nkeys = (uint32_t*)q->alloc(H.nsub * 4);
+      L.cursor = (uint32_t*)q->alloc(H.nsub * 4);
+      L.cnt = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
+      std::set<int> cols;
+      for (size_t l2 = l; l2 < T.levels.size(); ++l2) cols.insert(T.levels[l2].begin(), T.levels[l2].end());
+      for (int c : cols) L.cval[c] = (int32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
+      L.nk = (int)H.keycols.size();
+      for (int i = 0; i < L.nk; ++i) L.keycol[i] = H.keycols[i];
+      if (l > 0) {
+        L.list_p = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
+        L.list_len = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
+        L.list_scan = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
+      }
+    }
+  }
+  q->tmp_slot = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  q->tmp_rank = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  q->newslots = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  // static node descriptors
+  const size_t K = plan.nodes.size();
+  q->nodes.assign(K, DevNode{});
+  std::vector<uint32_t> bound_before(K + 1, 0);
+  for (size_t k = 0; k < K; ++k) {
+    uint32_t m = bound_before[k];
+    for (auto& s : plan.nodes[k].subatoms)
+      for (auto& x : s.vars) m |= 1u << vid[x];
+    bound_before[k + 1] = m;
+  }
+  for (size_t k = 0; k < K; ++k) {
+    DevNode& N = q->nodes[k];
+    memset(&N, 0, sizeof(N));
+    N.k = (int)k;
+    const auto& subs = plan.nodes[k].subatoms;
+    N.nsub = (int)subs.size();
+    N.is_last = k + 1 == K;
+    N.nhead = (int)q->head.size();
+    N.in_vars = bound_before[k];
+    N.out_vars = bound_before[k + 1];
+    auto cov = fj::covers(plan, k);
+    if (cov.empty()) throw ValidationError("node " + std::to_string(k) + " has no cover");
+    N.ncov = (int)cov.size();
+    for (size_t c = 0; c < cov.size(); ++c) N.cov[c] = (int)cov[c];
+    for (size_t a = 0; a < A; ++a) {
+      const auto& S = q->atoms[a].subs;
+      const bool before = !S.empty() && S.front().first < (int)k;
+      const bool at_or_after = !S.empty() && S.back().first >= (int)k;
+      const bool after = !S.empty() && S.back().first > (int)k;
+      const bool upto = !S.empty() && S.front().first <= (int)k;
+      if (before && at_or_after) N.in_atoms |= 1u << a;
+      if (upto && after) N.out_atoms |= 1u << a;
+      N.atom_n[a] = (uint32_t)q->rels[a]->nrows;
+    }
+    for (size_t i = 0; i < subs.size(); ++i) {
+      DevSub& D = N.sub[i];
+      const int a = aid[subs[i].relation];
+      D.atom = a;
+      D.trie = q->atoms[a].trie;
+      const auto& S = q->atoms[a].subs;
+      int depth = 0;
+      while (!(S[depth].first == (int)k && S[depth].second == (int)i)) ++depth;
+      D.depth = depth;
+      D.last = depth + 1 == (int)S.size();
+      D.nv = (int)subs[i].vars.size();
+      for (int t = 0; t < D.nv; ++t) {
+        D.var[t] = vid[subs[i].vars[t]];
+        D.col[t] = col_of(a, subs[i].vars[t]);
+        if ((N.in_vars >> D.var[t]) & 1u) D.bound_mask |= 1 << t;
+      }
+      bool later_vars = false;
+      for (size_t d = depth + 1; d < S.size(); ++d)
+        if (!plan.nodes[S[d].first].subatoms[S[d].second].vars.empty()) later_vars = true;
+      D.stream = !later_vars;
+    }
+  }
+  q->d_nodes = (DevNode*)q->alloc(K * sizeof(DevNode));
+  q->d_tries = (DevTrie*)q->alloc(q->tries.size() * sizeof(DevTrie));
+  q->d_ctr = (DevCounters*)q->alloc(sizeof(DevCounters));
+  CK(cudaMallocHost(&q->h_ctr, sizeof(DevCounters)));
+  CK(cudaMallocHost(&q->h_scratch, 64));
+  std::vector<DevTrie> dt;
+  for (auto& T : q->tries) dt.push_back(T.dev);
+  CK(cudaMemcpyAsync(q->d_tries, dt.data(), dt.size() * sizeof(DevTrie), cudaMemcpyHostToDevice, q->eng->stream));
+  CK(cudaEventCreate(&q->ev0));
+  CK(cudaEventCreate(&q->ev1));
+}
+
+// (Re)allocate per-node frontier buffers for a candidate capacity `cap`.
+static void ensure_frontiers(fjg_query* q, uint64_t cap) {
+  if (q->cap >= cap && q->cap) return;
+  const size_t K = q->nodes.size();
+  for (size_t k = 0; k < K; ++k) {
+    DevNode& N = q->nodes[k];
+    const uint64_t fin = k == 0 ? 1 : cap;  // entries entering node k
+    N.chosen = (uint8_t*)q->alloc(fin);
+    N.m = (uint64_t*)q->alloc(fin * 8);
+    N.scan = (uint64_t*)q->alloc(fin * 8);
+    if (k + 1 < K) {
+      DevFrontier& O = N.out;
+      memset(&O, 0, sizeof(O));
+      for (int v = 0; v < MAXV; ++v)
+        if ((N.out_vars >> v) & 1u) O.var[v] = (int32_t*)q->alloc(cap * 4);
+      for (int a = 0; a < MAXA; ++a)
+        if ((N.out_atoms >> a) & 1u) {
+          O.p[a] = (uint32_t*)q->alloc(cap * 4);
+          O.len[a] = (uint32_t*)q->alloc(cap * 4);
+        }
+      O.mult = (uint64_t*)q->alloc(cap * 8);
+      q->nodes[k + 1].in = O;
+    }
+  }
+  q->cap = cap;
+  // CUB temp storage for the largest scans
+  size_t b1 = 0, b2 = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, b1, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)cap));
+  CK(cub::DeviceScan::InclusiveSum(nullptr, b2, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                   (int64_t)std::max<uint64_t>(q->max_n, 1)));
+  size_t need = std::max(b1, b2);
+  if (need > q->cub_tmp_bytes) {
+    q->cub_tmp = q->alloc(need);
+    q->cub_tmp_bytes = need;
+  }
+  CK(cudaMemcpyAsync(q->d_nodes, q->nodes.data(), K * sizeof(DevNode), cudaMemcpyHostToDevice, q->eng->stream));
+}
+
+static void sync_counters(fjg_query* q) {
+  CK(cudaMemcpyAsync(q->h_ctr, q->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, q->eng->stream));
+  CK(cudaStreamSynchronize(q->eng->stream));
+  ++q->eng->syncs;
+}
+
+// Force the listed subtries of (trie t, level l): Fig 12 `force` in batch.
+static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, uint32_t len0, uint32_t count) {
+  fjg_engine* eng = q->eng;
+  auto& T = q->tries[t];
+  DevLevel& L = T.dev.lev[l];
+  ForceRange R{};
+  R.single = single ? 1 : 0;
+  R.p0 = p0;
+  R.len0 = len0;
+  uint64_t upper = len0;
+  if (!single) {
+    R.list_p = L.list_p;
+    R.list_len = L.list_len;
+    R.list_scan = L.list_scan;
+    R.list_count = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(q->d_ctr) +
+                                                     offsetof(DevCounters, list_count)) +
+                   (t * MAXL + l);
+    size_t bytes = q->cub_tmp_bytes;
+    CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, L.list_len, L.list_scan, (int64_t)count, eng->stream));
+    ++eng->launches;
+    upper = T.rel->nrows;
+  }
+  if (q->timing) CK(cudaEventRecord(q->ev0, eng->stream));
+  if (single) {
+    CK(cudaMemsetAsync(L.cursor + (l == 0 ? 0 : p0), 0, 4, eng->stream));
+    CK(cudaMemsetAsync(L.nkeys + (l == 0 ? 0 : p0), 0, 4, eng->stream));
+  }
+  CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, newslots), 0, 4, eng->stream));
+  const unsigned g = grid_for(upper, 256, eng->num_sms * 16);
+  if (T.lev[l].multi)
+    LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
+                                                                  q->newslots, q->d_ctr));
+  else
+    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
+                                                                   q->newslots, q->d_ctr));
+  const unsigned ga = grid_for(upper, 256, eng->num_sms * 8);
+  if (single)
+    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, p0, q->newslots, q->d_ctr));
+  else
+    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, q->newslots, q->d_ctr));
+  LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank));
+  LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R));
+  // keys inserted accumulate on the device
+  if (q->timing) {
+    CK(cudaEventRecord(q->ev1, eng->stream));
+    CK(cudaEventSynchronize(q->ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
+    q->build_ms += ms;
+  }
+  q->forces += 1;
+  q->maps_built += single ? 1 : count;
+  q->rows_forced += single ? len0 : 0;
+  T.lev[l].dirty = true;
+}
+
+__global__ void k_accum_keys(DevCounters* ctr) { ctr->keys_inserted += ctr->newslots; }
+
+static void run_node(fjg_query* q, int k, uint64_t F, int mode);
+
+static void force_claims(fjg_query* q, int k) {
+  // roots first, then claimed deeper subtries
+  fjg_engine* eng = q->eng;
+  DevCounters& H = *q->h_ctr;
+  bool any = false;
+  for (size_t t = 0; t < q->tries.size(); ++t) {
+    if (H.root_need[t] && !q->tries[t].root_forced) {
+      force_level(q, (int)t, 0, true, 0, (uint32_t)q->tries[t].rel->nrows, 1);
+      LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
+      q->tries[t].root_forced = true;
+      any = true;
+    }
+    for (int l = 1; l < (int)q->tries[t].levels.size(); ++l) {
+      const uint32_t c = H.list_count[t * MAXL + l];
+      if (c) {
+        force_level(q, (int)t, l, false, 0, 0, c);
+        LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
+        any = true;
+      }
+    }
+  }
+  if (any) {
+    CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, list_count), 0,
+                       sizeof(H.list_count) + sizeof(H.root_need), eng->stream));
+  }
+  (void)k;
+}
+
+static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
+  if (F == 0) return;
+  fjg_engine* eng = q->eng;
+  const DevNode& N = q->nodes[k];
+  DevNode* dN = q->d_nodes + k;
+  LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(dN, q->d_tries, F,
+                                                                                    q->dynamic ? 1 : 0, q->d_ctr));
+  size_t bytes = q->cub_tmp_bytes;
+  CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, N.m, N.scan, (int64_t)F, eng->stream));
+  ++eng->launches;
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, total_m), N.scan + (F - 1), 8,
+                     cudaMemcpyDeviceToDevice, eng->stream));
+  sync_counters(q);
+  const uint64_t M = q->h_ctr->total_m;
+  force_claims(q, k);
+  if (M == 0) return;
+  if (q->timing) CK(cudaEventRecord(q->ev0, eng->stream));
+  if (N.is_last) {
+    const unsigned g = grid_for(M, 256, eng->num_sms * 8);
+    if (mode == EXPAND_ENUM)
+      LAUNCH(eng, k_expand<EXPAND_ENUM><<<g, 256, 0, eng->stream>>>(dN, q->d_tries, 0, M, F, -1, q->out_tuples,
+                                                                     q->out_cap, q->d_ctr));
+    else
+      LAUNCH(eng, k_expand<EXPAND_COUNT><<<g, 256, 0, eng->stream>>>(dN, q->d_tries, 0, M, F, q->min_var,
+                                                                      nullptr, 0, q->d_ctr));
+    if (q->timing) {
+      CK(cudaEventRecord(q->ev1, eng->stream));
+      CK(cudaEventSynchronize(q->ev1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
+      q->join_ms += ms;
+    }
+    return;
+  }
+  for (uint64_t c0 = 0; c0 < M; c0 += q->batch) {
+    const uint64_t c1 = std::min(M, c0 + q->batch);
+    CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, survivors), 0, 4, eng->stream));
+    if (q->timing && c0) CK(cudaEventRecord(q->ev0, eng->stream));
+    LAUNCH(eng, k_expand<EXPAND_WRITE><<<grid_for(c1 - c0, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(
+                    dN, q->d_tries, c0, c1, F, -1, nullptr, 0, q->d_ctr));
+    if (q->timing) CK(cudaEventRecord(q->ev1, eng->stream));
+    sync_counters(q);
+    if (q->timing) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
+      q->join_ms += ms;
+    }
+    run_node(q, k + 1, q->h_ctr->survivors, mode);
+  }
+}
+
+static void reset_query(fjg_query* q) {
+  fjg_engine* eng = q->eng;
+  for (auto& T : q->tries) {
+    for (size_t l = 0; l < T.lev.size(); ++l) {
+      auto& H = T.lev[l];
+      DevLevel& L = T.dev.lev[l];
+      if (H.dirty) {
+        LAUNCH(eng, k_fill_slots<<<grid_for(H.cap, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(L.table, H.cap));
+        if (L.srep) CK(cudaMemsetAsync(L.srep, 0, H.cap * 4, eng->stream));
+        CK(cudaMemsetAsync(L.state, 0, H.nsub * 4, eng->stream));
+        H.dirty = false;
+      }
+    }
+    T.root_forced = false;
+  }
+  DevCounters z;
+  memset(&z, 0, sizeof(z));
+  z.minv = LLONG_MAX;
+  memcpy(q->h_ctr, &z, sizeof(z));
+  CK(cudaMemcpyAsync(q->d_ctr, q->h_ctr, sizeof(z), cudaMemcpyHostToDevice, eng->stream));
+  q->maps_built = q->forces = q->rows_forced = 0;
+  q->build_ms = q->join_ms = 0;
+}
+
+static void execute_once(fjg_query* q, int mode) {
+  reset_query(q);
+  run_node(q, 0, 1, mode);
+  sync_counters(q);
+}
+
+// ============================================================================
+// C-ABI (device side)
+// ============================================================================
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return FJG_OK;
+  } catch (const fj::Error& e) {
+    fjg::set_last_error(e.what());
+    return e.code();
+  } catch (const std::bad_alloc&) {
+    fjg::set_last_error("host allocation failed");
+    return FJG_E_RESOURCE;
+  } catch (const std::exception& e) {
+    fjg::set_last_error(e.what());
+    return FJG_E_ENGINE;
+  }
+}
+
+extern "C" {
+
+int fjg_engine_create(int device, fjg_engine** out) {
+  return guard([&] {
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw fj::ResourceError("no CUDA device " + std::to_string(device));
+    ScopedDevice sd(device);
+    CK(cudaSetDevice(device));
+    auto* e = new fjg_engine();
+    e->device = device;
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->pool.reset(new Pool(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    e->num_sms = prop.multiProcessorCount;
+    *out = e;
+  });
+}
+
+void fjg_engine_destroy(fjg_engine* eng) {
+  if (!eng) return;
+  ScopedDevice sd(eng->device);
+  cudaStreamSynchronize(eng->stream);
+  eng->pool.reset();
+  cudaStreamDestroy(eng->stream);
+  delete eng;
+}
+
+int fjg_engine_sync(fjg_engine* eng) {
+  return guard([&] { CK(cudaStreamSynchronize(eng->stream)); });
+}
+
+static fjg_relation* new_relation(fjg_engine* eng, int ncols, uint64_t nrows) {
+  if (ncols <= 0 || ncols > MAXC) throw fj::ValidationError("relation must have 1..8 columns");
+  if (nrows >= 0xFFFFFFF0ull) throw fj::ValidationError("relation too large (rows must be < 2^32-16)");
+  auto* r = new fjg_relation();
+  r->eng = eng;
+  r->nrows = nrows;
+  r->ncols = ncols;
+  for (int c = 0; c < ncols; ++c) {
+    void* p = eng->pool->alloc(std::max<uint64_t>(nrows, 1) * 4);
+    r->owned.push_back(p);
+    r->cols.push_back((int32_t*)p);
+  }
+  return r;
+}
+
+int fjg_relation_create(fjg_engine* eng, const int32_t* const* host_cols, int ncols, uint64_t nrows,
+                        fjg_relation** out) {
+  return guard([&] {
+    ScopedDevice sd(eng->device);
+    fjg_relation* r = new_relation(eng, ncols, nrows);
+    for (int c = 0; c < ncols; ++c)
+      if (nrows) CK(cudaMemcpyAsync(r->cols[c], host_cols[c], nrows * 4, cudaMemcpyHostToDevice, eng->stream));
+    *out = r;
+  });
+}
+
+int fjg_relation_from_device(fjg_engine* eng, const int32_t* const* dev_cols, int ncols, uint64_t nrows, int copy,
+                             fjg_relation** out) {
+  return guard([&] {
+    ScopedDevice sd(eng->device);
+    if (copy) {
+      fjg_relation* r = new_relation(eng, ncols, nrows);
+      for (int c = 0; c < ncols; ++c)
+        if (nrows) CK(cudaMemcpyAsync(r->cols[c], dev_cols[c], nrows * 4, cudaMemcpyDeviceToDevice, eng->stream));
+      *out = r;
+    } else {
+      if (ncols <= 0 || ncols > MAXC) throw fj::ValidationError("relation must have 1..8 columns");
+      auto* r = new fjg_relation();
+      r->eng = eng;
+      r->nrows = nrows;
+      r->ncols = ncols;
+      for (int c = 0; c < ncols; ++c) r->cols.push_back(const_cast<int32_t*>(dev_cols[c]));
+      *out = r;
+    }
+  });
+}
+
+int fjg_relation_filter(const fjg_relation* in, const fjg_predicate* preds, int npreds, fjg_relation** out) {
+  return guard([&] {
+    fjg_engine* eng = in->eng;
+    ScopedDevice sd(eng->device);
+    if (npreds > 8) throw fj::ValidationError("at most 8 predicates");
+    DevPreds P{};
+    P.n = npreds;
+    for (int i = 0; i < npreds; ++i) {
+      if (preds[i].column < 0 || preds[i].column >= in->ncols ||
+          (preds[i].is_column && (preds[i].rhs_column < 0 || preds[i].rhs_column >= in->ncols)))
+        throw fj::ValidationError("predicate references unknown column");
+      if (preds[i].cmp < 0 || preds[i].cmp > 5) throw fj::ValidationError("bad comparator");
+      P.p[i] = preds[i];
+    }
+    for (int c = 0; c < in->ncols; ++c) P.cols[c] = in->cols[c];
+    const uint64_t n = in->nrows;
+    uint32_t* flags = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
+    uint32_t* excl = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4 + 4);
+    uint32_t total = 0;
+    if (n) {
+      LAUNCH(eng, k_filter_flags<<<grid_for(n), 256, 0, eng->stream>>>(P, n, flags));
+      size_t bytes = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, excl, (int64_t)n));
+      void* tmp = eng->pool->alloc(bytes);
+      CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, flags, excl, (int64_t)n, eng->stream));
+      uint32_t last[2];
+      CK(cudaMemcpyAsync(&last[0], excl + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaMemcpyAsync(&last[1], flags + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      total = last[0] + last[1];
+      eng->pool->free(tmp);
+    }
+    fjg_relation* r = new_relation(eng, in->ncols, total);
+    for (int c = 0; c < in->ncols && n; ++c)
+      LAUNCH(eng, k_compact_col<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[c], flags, excl, n, r->cols[c]));
+    CK(cudaStreamSynchronize(eng->stream));
+    eng->pool->free(flags);
+    eng->pool->free(excl);
+    *out = r;
+  });
+}
+
+int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_relation** out_rel, uint64_t* counts) {
+  return guard([&] {
+    fjg_engine* eng = in->eng;
+    ScopedDevice sd(eng->device);
+    if (col < 0 || col >= in->ncols) throw fj::ValidationError("partition column out of range");
+    if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
+    const uint64_t n = in->nrows;
+    fjg_relation* r = new_relation(eng, in->ncols, n);
+    uint32_t* flags = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
+    uint32_t* excl = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, excl, (int64_t)std::max<uint64_t>(n, 1)));
+    void* tmp = eng->pool->alloc(bytes);
+    uint64_t base = 0;
+    for (int d = 0; d < nparts; ++d) {
+      uint32_t total = 0;
+      if (n) {
+        LAUNCH(eng, k_partition_flags<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[col], n, nparts, d, flags));
+        size_t b = bytes;
+        CK(cub::DeviceScan::ExclusiveSum(tmp, b, flags, excl, (int64_t)n, eng->stream));
+        uint32_t last[2];
+        CK(cudaMemcpyAsync(&last[0], excl + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+        CK(cudaMemcpyAsync(&last[1], flags + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+        CK(cudaStreamSynchronize(eng->stream));
+        total = last[0] + last[1];
+        for (int c = 0; c < in->ncols; ++c)
+          LAUNCH(eng, k_compact_col<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[c], flags, excl, n,
+                                                                        r->cols[c] + base));
+      }
+      counts[d] = total;
+      base += total;
+    }
+    CK(cudaStreamSynchronize(eng->stream));
+    eng->pool->free(flags);
+    eng->pool->free(excl);
+    eng->pool->free(tmp);
+    *out_rel = r;
+  });
+}
+
+uint64_t fjg_relation_rows(const fjg_relation* rel) { return rel ? rel->nrows : 0; }
+int fjg_relation_cols(const fjg_relation* rel) { return rel ? rel->ncols : 0; }
+const int32_t* fjg_relation_device_col(const fjg_relation* rel, int col) {
+  return (rel && col >= 0 && col < rel->ncols) ? rel->cols[col] : nullptr;
+}
+
+int fjg_relation_download(const fjg_relation* rel, int col, int32_t* host_out) {
+  return guard([&] {
+    ScopedDevice sd(rel->eng->device);
+    if (col < 0 || col >= rel->ncols) throw fj::ValidationError("column out of range");
+    if (rel->nrows)
+      CK(cudaMemcpyAsync(host_out, rel->cols[col], rel->nrows * 4, cudaMemcpyDeviceToHost, rel->eng->stream));
+    CK(cudaStreamSynchronize(rel->eng->stream));
+  });
+}
+
+void fjg_relation_destroy(fjg_relation* rel) {
+  if (!rel) return;
+  ScopedDevice sd(rel->eng->device);
+  cudaStreamSynchronize(rel->eng->stream);
+  for (void* p : rel->owned) rel->eng->pool->free(p);
+  delete rel;
+}
+
+int fjg_query_create(fjg_engine* eng, const char* query_json, const char* plan_json, fjg_relation* const* atom_rels,
+                     int natoms, fjg_query** out) {
+  return guard([&] {
+    ScopedDevice sd(eng->device);
+    auto q = std::make_unique<fjg_query>();
+    q->eng = eng;
+    auto qv = fj::json::parse(query_json);
+    auto query = fj::query_from_json(qv);
+    if ((int)query.size() != natoms)
+      throw fj::ValidationError("query has " + std::to_string(query.size()) + " atoms but " +
+                                std::to_string(natoms) + " relations were bound");
+    q->plan = fj::plan_from_json(fj::json::parse(plan_json), query);
+    std::string err = fj::validate(q->plan);
+    if (!err.empty()) throw fj::ValidationError("invalid plan: " + err);
+    for (int a = 0; a < natoms; ++a) {
+      if (!atom_rels[a]) throw fj::ValidationError("null relation bound to atom");
+      if (atom_rels[a]->eng != eng) throw fj::ValidationError("relation belongs to another engine");
+      q->rels.push_back(atom_rels[a]);
+    }
+    prepare_query(q.get());
+    *out = q.release();
+  });
+}
+
+int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
+  return guard([&] {
+    fjg_engine* eng = q->eng;
+    ScopedDevice sd(eng->device);
+    fjg_exec_options o{};
+    o.dynamic_cover = 1;
+    o.min_var = -1;
+    if (opts) o = *opts;
+    if (o.min_var >= (int)q->head.size()) throw fj::ValidationError("min_var out of range");
+    uint64_t batch = o.batch_size ? o.batch_size : (1ull << 24);
+    ensure_frontiers(q, batch);
+    q->dynamic = o.dynamic_cover != 0;
+    q->timing = o.collect_timing != 0;
+    q->batch = batch;
+    q->min_var = o.min_var;
+    const uint32_t l0 = eng->launches, s0 = eng->syncs;
+    execute_once(q, EXPAND_COUNT);
+    if (o.output_mode == FJG_OUT_ENUMERATE) {
+      const uint64_t rows = q->h_ctr->count_lo;
+      if (q->h_ctr->count_hi || rows > (1ull << 34) / std::max<uint64_t>(q->head.size(), 1))
+        throw fj::ResourceError("enumerated output too large to materialise");
+      const uint64_t need = std::max<uint64_t>(rows, 1) * q->head.size() * 4;
+      if (q->out_cap < rows || !q->out_tuples) {
+        q->out_tuples = (int32_t*)q->alloc(need);
+        q->out_cap = rows;
+      }
+      DevCounters keep = *q->h_ctr;
+      execute_once(q, EXPAND_ENUM);
+      q->out_rows = q->h_ctr->out_rows;
+      const DevCounters enum_ctr = *q->h_ctr;
+      *q->h_ctr = keep;
+      q->h_ctr->out_rows = enum_ctr.out_rows;
+      if (q->out_rows != rows) throw fj::EngineError("enumerate pass disagrees with count pass");
+    }
+    const DevCounters& H = *q->h_ctr;
+    fjg_result r{};
+    r.count_lo = H.count_lo;
+    r.count_hi = H.count_hi;
+    r.checksum = H.checksum;
+    r.has_min = (o.min_var >= 0 && H.minv != LLONG_MAX) ? 1 : 0;
+    r.min_value = r.has_min ? H.minv : 0;
+    r.num_nodes = (int)q->nodes.size();
+    r.output_rows = (o.output_mode == FJG_OUT_ENUMERATE) ? q->out_rows : 0;
+    r.probes = H.probes;
+    r.probe_misses = H.misses;
+    for (int k = 0; k < MAXN && k < FJG_MAX_NODES; ++k) r.node_body_entries[k] = H.body[k];
+    r.maps_built = q->maps_built;
+    r.keys_inserted = H.keys_inserted;
+    r.forces = q->forces;
+    r.rows_forced = q->rows_forced;
+    r.build_ms = q->build_ms;
+    r.join_ms = q->join_ms;
+    r.kernel_launches = eng->launches - l0;
+    r.host_syncs = eng->syncs - s0;
+    *out = r;
+  });
+}
+
+int fjg_query_output(fjg_query* q, int32_t* host_out, uint64_t cap_rows, uint64_t* rows) {
+  return guard([&] {
+    ScopedDevice sd(q->eng->device);
+    const uint64_t n = std::min(cap_rows, q->out_rows);
+    if (n) CK(cudaMemcpyAsync(host_out, q->out_tuples, n * q->head.size() * 4, cudaMemcpyDeviceToHost, q->eng->stream));
+    CK(cudaStreamSynchronize(q->eng->stream));
+    *rows = n;
+  });
+}
+
+int fjg_query_num_head_vars(const fjg_query* q) { return q ? (int)q->head.size() : 0; }
+
+void fjg_query_destroy(fjg_query* q) {
+  if (!q) return;
+  ScopedDevice sd(q->eng->device);
+  cudaStreamSynchronize(q->eng->stream);
+  delete q;
+}
+
+int fjg_device_tuple_hash(fjg_engine* eng, const int64_t* host_vals, int arity, uint64_t ntuples, uint64_t* host_out) {
+  return guard([&] {
+    ScopedDevice sd(eng->device);
+    if (ntuples == 0) return;
+    const size_t vb = std::max<size_t>((size_t)arity * ntuples * 8, 8);
+    int64_t* dv = (int64_t*)eng->pool->alloc(vb);
+    uint64_t* dout = (uint64_t*)eng->pool->alloc(ntuples * 8);
+    if (arity) CK(cudaMemcpyAsync(dv, host_vals, (size_t)arity * ntuples * 8, cudaMemcpyHostToDevice, eng->stream));
+    LAUNCH(eng, k_tuple_hash<<<grid_for(ntuples), 256, 0, eng->stream>>>(dv, arity, ntuples, dout));
+    CK(cudaMemcpyAsync(host_out, dout, ntuples * 8, cudaMemcpyDeviceToHost, eng->stream));
+    CK(cudaStreamSynchronize(eng->stream));
+    eng->pool->free(dv);
+    eng->pool->free(dout);
+  });
+}
+
+}  // extern "C"

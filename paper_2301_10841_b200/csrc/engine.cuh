@@ -1,0 +1,133 @@
+// Device-side data layout of the B200 Free Join executor.
+//
+// COLT on the device (reference: Fig 12)
+// ---------------------------------------------------------------------------
+// A *physical trie* is one relation plus the list of key-column groups per
+// level. Atoms over the same relation with the same level key columns (renamed
+// self-joins) share one physical trie: COLT is a
+// deterministic function of (relation, schema), so sharing is invisible.
+//
+// Subtries are identified by *positions*. The root (depth 0) is the BaseScan of
+// rows [0, n) (zero work at `new`). Forcing level l of a subtrie
+// whose offsets occupy positions [p, p+len) of domain l-1 regroups exactly
+// those positions in domain l, children contiguous: child groups are
+// sub-ranges [q, q+cnt) of [p, p+len), and a child's id is its start q. So
+//   - no offset vectors are allocated per node and no ids are handed out;
+//   - a level holds n-sized arrays indexed by position.
+// Instead of row offsets, forcing scatters the *column values* every deeper
+// level will read ("clustered columns", cval), so cover iteration streams
+// coalesced values instead of gathering through offsets.
+//
+// Per level l (l >= 0), with n = relation rows:
+//   table   open-addressing hash map (parent p, key) -> child (q, cnt);
+//           16-byte slots, linear probing, capacity pow2 >= 2n (load <= 0.5)
+//   state   per subtrie id: 0 unforced, 1 claimed for forcing, 2 forced
+//   nkeys   per subtrie id: distinct keys once forced (estimated_key_count)
+//   cursor  per subtrie id: child-range allocation cursor (force only)
+//   cnt     per position of domain l: child length at a child start, else 0
+//   cval[c] per position of domain l: column c (every column used at levels >= l)
+#pragma once
+
+#include <cstdint>
+
+#include "fj_hash.hpp"
+
+namespace fjg {
+
+constexpr int MAXV = 16;  // variables per query
+constexpr int MAXA = 16;  // atoms per query
+constexpr int MAXS = 12;  // subatoms per node
+constexpr int MAXK = 6;   // vars per subatom (key arity)
+constexpr int MAXC = 8;   // columns per relation
+constexpr int MAXL = 8;   // levels per physical trie
+constexpr int MAXT = 16;  // physical tries per query
+constexpr int MAXN = 32;  // plan nodes
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr uint64_t kEmpty64 = 0xFFFFFFFFFFFFFFFFull;
+constexpr uint32_t kSingleton = 0xFFFFFFFFu;  // streamed row: residual subtrie is [row]
+
+struct __align__(16) Slot {
+  uint32_t p;    // parent subtrie id (kEmpty = free slot)
+  uint32_t k;    // key word: the int32 key (arity 1), 0 (arity 0) or a 32-bit tuple hash
+  uint32_t q;    // child start position
+  uint32_t len;  // child length
+};
+
+struct DevLevel {
+  Slot* table;
+  uint64_t mask;
+  uint32_t* srep;    // arity >= 2 only: representative position + 1 during insertion
+  uint32_t* state;
+  uint32_t* nkeys;
+  uint32_t* cursor;
+  uint32_t* cnt;
+  int32_t* cval[MAXC];
+  int nk;
+  int keycol[MAXK];
+  uint32_t* list_p;    // subtries claimed for forcing
+  uint32_t* list_len;
+  uint32_t* list_scan;
+};
+
+struct DevTrie {
+  uint32_t n;
+  int ncols;
+  int nlev;
+  const int32_t* base[MAXC];
+  DevLevel lev[MAXL];
+};
+
+struct DevSub {
+  int atom;
+  int trie;
+  int depth;       // COLT level this subatom reads (= # earlier subatoms of its atom)
+  int nv;
+  int var[MAXK];
+  int col[MAXK];
+  int bound_mask;  // bit t: var[t] already bound at node entry (checked when iterated)
+  int stream;      // vars are all remaining vars of the atom (Fig 12 is_suffix)
+  int last;        // last subatom of its atom
+};
+
+struct DevFrontier {
+  int32_t* var[MAXV];
+  uint32_t* p[MAXA];
+  uint32_t* len[MAXA];
+  uint64_t* mult;
+};
+
+struct DevNode {
+  int k;
+  int nsub;
+  int ncov;
+  int is_last;
+  int cov[MAXS];
+  DevSub sub[MAXS];
+  uint32_t in_vars;    // bitmask of variables bound at node entry (avs)
+  uint32_t out_vars;   // bitmask bound after the node
+  uint32_t in_atoms;   // atoms with a subtrie slot at node entry
+  uint32_t out_atoms;  // atoms with a subtrie slot after the node
+  uint32_t atom_n[MAXA];
+  int nhead;
+  DevFrontier in, out;
+  uint8_t* chosen;     // per entry: chosen cover (subatom index)
+  uint64_t* m;         // per entry: candidates
+  uint64_t* scan;      // inclusive scan of m
+};
+
+struct DevCounters {
+  uint64_t count_lo, count_hi, checksum;
+  long long minv;
+  uint64_t probes, misses;
+  uint64_t body[MAXN];
+  uint64_t keys_inserted;
+  uint64_t out_rows;
+  uint64_t total_m;
+  uint32_t survivors;
+  uint32_t newslots;
+  uint32_t list_count[MAXT * MAXL];
+  uint32_t root_need[MAXT];
+};
+
+}  // namespace fjg

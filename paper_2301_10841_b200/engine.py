@@ -1,0 +1,226 @@
+"""Device engine, relations and queries (host side of the C-ABI).
+
+Mirrors the reference's trie/executor surface: relations are
+immutable columnar tables; a Query binds a validated Free Join plan to one
+relation per atom; Query.execute() runs the build phase (COLT `new`, lazy) and
+the join phase (Fig 13 join_vectorized with dynamic cover) on the GPU and
+returns the OutputSink counters plus ExecStats/TrieStats.
+"""
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+
+OUT_COUNT, OUT_ENUMERATE, OUT_FACTORIZED_COUNT = 0, 1, 2
+_OUT = {"count": OUT_COUNT, "enumerate": OUT_ENUMERATE, "factorized_count": OUT_FACTORIZED_COUNT}
+CMP = {"=": 0, "==": 0, "!=": 1, "<": 2, "<=": 3, ">": 4, ">=": 5}
+
+
+@dataclass
+class ExecResult:
+    count: int
+    checksum: int
+    min_value: object
+    probes: int
+    probe_misses: int
+    node_body_entries: list
+    maps_built: int
+    keys_inserted: int
+    forces: int
+    rows_forced: int
+    build_ms: float
+    join_ms: float
+    kernel_launches: int
+    host_syncs: int
+    output_rows: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class Engine:
+    """One CUDA device + stream + memory pool (fjg_engine)."""
+
+    def __init__(self, device=0):
+        h = C.c_void_p()
+        check(lib.fjg_engine_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if self._h:
+            lib.fjg_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        check(lib.fjg_engine_sync(self._h))
+
+    def relation(self, cols):
+        """load columns (host int32 arrays) -> device Relation (fjg_relation_create)."""
+        arrs = [np.ascontiguousarray(c, dtype=np.int32) for c in cols]
+        n = len(arrs[0]) if arrs else 0
+        if any(len(a) != n for a in arrs):
+            raise _capi.ValidationError("all columns must have identical length (SPEC.md:35)")
+        ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        h = C.c_void_p()
+        check(lib.fjg_relation_create(self._h, ptrs, len(arrs), n, C.byref(h)))
+        return Relation(self, h, keepalive=None)
+
+    def relation_from_device(self, ptrs, nrows, copy=False, keepalive=None):
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        h = C.c_void_p()
+        check(lib.fjg_relation_from_device(self._h, arr, len(ptrs), int(nrows), int(bool(copy)), C.byref(h)))
+        return Relation(self, h, keepalive=None if copy else keepalive)
+
+    def relation_from_torch(self, tensors, copy=False):
+        """Wrap CUDA int32 tensors (one per column) as a relation (zero-copy unless copy=True)."""
+        for t in tensors:
+            if not t.is_cuda or t.dtype.itemsize != 4 or not t.is_contiguous():
+                raise _capi.ValidationError("columns must be contiguous CUDA int32 tensors")
+        n = tensors[0].numel() if tensors else 0
+        return self.relation_from_device([t.data_ptr() for t in tensors], n, copy=copy, keepalive=list(tensors))
+
+    def query(self, query, plan, atom_relations):
+        return Query(self, query, plan, atom_relations)
+
+    def device_tuple_hash(self, tuples):
+        t = np.ascontiguousarray(np.asarray(tuples, dtype=np.int64))
+        if t.ndim == 1:
+            t = t.reshape(-1, 1) if t.size else t.reshape(0, 0)
+        n, arity = (t.shape[0], t.shape[1]) if t.ndim == 2 else (0, 0)
+        out = np.zeros(max(n, 1), dtype=np.uint64)
+        check(lib.fjg_device_tuple_hash(self._h, t.ctypes.data, arity, n, out.ctypes.data))
+        return out[:n]
+
+
+class Relation:
+    """Immutable device columnar relation."""
+
+    def __init__(self, engine, handle, keepalive=None):
+        self.engine = engine
+        self._h = handle
+        self._keep = keepalive
+
+    @property
+    def rows(self):
+        return int(lib.fjg_relation_rows(self._h))
+
+    @property
+    def ncols(self):
+        return int(lib.fjg_relation_cols(self._h))
+
+    def device_col(self, c):
+        return lib.fjg_relation_device_col(self._h, c)
+
+    def download(self):
+        out = []
+        for c in range(self.ncols):
+            a = np.empty(max(self.rows, 1), dtype=np.int32)
+            check(lib.fjg_relation_download(self._h, c, a.ctypes.data))
+            out.append(a[: self.rows])
+        return out
+
+    def filter(self, preds):
+        """apply_filter. preds: (col, op, const) or (col, op, ('col', c2))."""
+        arr = (_capi.Predicate * max(len(preds), 1))()
+        for i, (col, op, rhs) in enumerate(preds):
+            arr[i].column = col
+            arr[i].cmp = CMP[op]
+            if isinstance(rhs, tuple):
+                arr[i].is_column, arr[i].rhs_column = 1, rhs[1]
+            else:
+                arr[i].constant = int(rhs)
+        h = C.c_void_p()
+        check(lib.fjg_relation_filter(self._h, arr, len(preds), C.byref(h)))
+        return Relation(self.engine, h)
+
+    def partition(self, col, nparts):
+        """Hash-partition rows on `col` (multi-GPU sharding): (relation grouped by part, counts)."""
+        counts = (C.c_uint64 * nparts)()
+        h = C.c_void_p()
+        check(lib.fjg_relation_partition(self._h, col, nparts, C.byref(h), counts))
+        return Relation(self.engine, h), [int(x) for x in counts]
+
+    def close(self):
+        if self._h:
+            lib.fjg_relation_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Query:
+    """A validated Free Join plan bound to one relation per query atom."""
+
+    def __init__(self, engine, query, plan, atom_relations):
+        self.engine = engine
+        if isinstance(query, dict):
+            qd = query
+        elif isinstance(query, str):
+            qd = json.loads(query)
+        else:
+            qd = {"query": query}
+        self.atoms = qd["query"]
+        self.query_json = json.dumps({"query": self.atoms})
+        self.plan = plan
+        self.plan_json = plan if isinstance(plan, str) else json.dumps([[[r, list(v)] for (r, v) in n] for n in plan])
+        self.relations = list(atom_relations)
+        arr = (C.c_void_p * len(self.relations))(*[r._h.value for r in self.relations])
+        h = C.c_void_p()
+        check(lib.fjg_query_create(engine._h, self.query_json.encode(), self.plan_json.encode(), arr,
+                                   len(self.relations), C.byref(h)))
+        self._h = h
+        self.head = []
+        for a in self.atoms:
+            for v in a["vars"]:
+                if v not in self.head:
+                    self.head.append(v)
+
+    def execute(self, batch_size=0, dynamic_cover=True, output_mode="count", min_var=None, timing=False):
+        o = _capi.ExecOptions()
+        o.batch_size = int(batch_size)
+        o.dynamic_cover = int(bool(dynamic_cover))
+        o.output_mode = _OUT[output_mode] if isinstance(output_mode, str) else int(output_mode)
+        o.min_var = -1 if min_var is None else (self.head.index(min_var) if isinstance(min_var, str) else int(min_var))
+        o.collect_timing = int(bool(timing))
+        r = _capi.Result()
+        check(lib.fjg_execute(self._h, C.byref(o), C.byref(r)))
+        nn = r.num_nodes
+        return ExecResult(count=(r.count_hi << 64) | r.count_lo, checksum=r.checksum,
+                          min_value=(r.min_value if r.has_min else None), probes=r.probes,
+                          probe_misses=r.probe_misses, node_body_entries=list(r.node_body_entries[:nn]),
+                          maps_built=r.maps_built, keys_inserted=r.keys_inserted, forces=r.forces,
+                          rows_forced=r.rows_forced, build_ms=r.build_ms, join_ms=r.join_ms,
+                          kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
+
+    def enumerate(self, batch_size=0, dynamic_cover=True):
+        """Enumerate mode: (tuples as an (n, |head|) int32 array in head-variable order, ExecResult)."""
+        r = self.execute(batch_size=batch_size, dynamic_cover=dynamic_cover, output_mode="enumerate")
+        nv = len(self.head)
+        buf = np.empty((max(r.output_rows, 1), nv), dtype=np.int32)
+        rows = C.c_uint64(0)
+        check(lib.fjg_query_output(self._h, buf.ctypes.data, r.output_rows, C.byref(rows)))
+        return buf[: rows.value], r
+
+    def close(self):
+        if self._h:
+            lib.fjg_query_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
