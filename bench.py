@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark: Free Join query throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config triangle] [--impl ours|reference]
+
+A step = one full query execution (COLT build phase + join phase)
+over inputs already resident in HBM. `value` = (input tuples + output tuples)
+per second over the whole job; `e2e` = the same metric through the public
+C-ABI with host (pinned) input buffers copied inside the timed region.
+For N>1 (torchrun), relations holding the first plan variable are
+hash-partitioned across ranks by an NCCL all-to-all and the rest all-gathered
+(paper_2301_10841_b200/dist.py); the exchange is inside the timed step.
+--impl reference times the CPU restatement of the reference path (oracle/)
+on all host cores over a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "join tuples/sec (input+output) per query"
+UNIT = "tuples/s"
+L2_BYTES = 126 * (1 << 20)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="triangle")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-target-s", type=float, default=30.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def workload(name):
+    from paper_2301_10841_b200 import configs
+    return configs.CONFIGS[name]()
+
+
+class Clocks:
+    """nvidia-smi sampler DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def node_entry_bytes(plan, query, k):
+    """Bytes of one frontier entry entering node k (SoA: bound vars int32,
+    open-atom subtrie (id,len) 2x u32, multiplicity u64) + chosen u8 + scan u64."""
+    atoms = {a["rel"]: a for a in query}
+    bound = set()
+    for j in range(k):
+        for (_, vs) in plan[j]:
+            bound.update(vs)
+    open_atoms = 0
+    for name in atoms:
+        nodes = [j for j, node in enumerate(plan) for (r, _) in node if r == name]
+        if nodes and min(nodes) < k <= max(nodes):
+            open_atoms += 1
+    return 4 * len(bound) + 8 * open_atoms + (8 if k > 0 else 0) + 1 + 8
+
+
+def last_node_bytes(plan, query, res):
+    """SURVEY.md §8(d) sector model for the fused last-node kernel of one launch:
+    32 B per probe (one sector per get) + the contiguous streams: frontier
+    entries, cover values (int32 per candidate per cover variable)."""
+    k = len(plan) - 1
+    F = res.node_inputs[k]
+    M = res.last_node_candidates
+    P = res.node_probes[k]
+    nv = max(len(vs) for (_, vs) in plan[k])
+    seq = F * node_entry_bytes(plan, query, k) + M * 4 * nv
+    return 32 * P + 32 * ((seq + 31) // 32)
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU leg ---
+def _orc_run(w, plan, cols, min_var, T, P):
+    from oracle import oracle
+    t0 = time.perf_counter()
+    r = oracle.execute(w.query, plan, cols, part=0, nparts=P, nthreads=T, min_var=min_var)
+    return time.perf_counter() - t0, r
+
+
+def cpu_plan(w, plan, min_var, T):
+    """Two-point calibration of the oracle on T threads: t(P) = B + W/P for T of
+    P first-variable partitions (B: per-thread build, W: join work)."""
+    cols = w.atom_columns()
+    t16, _ = _orc_run(w, plan, cols, min_var, T, 16 * T)
+    t4, _ = _orc_run(w, plan, cols, min_var, T, 4 * T)
+    W = max(t4 - t16, 0.0) / (1.0 / (4 * T) - 1.0 / (16 * T))
+    B = max(t16 - W / (16 * T), 0.0)
+    return B, W
+
+
+def cpu_sample(w, plan, min_var, target_s, threads=None, calib=None):
+    """Time the oracle (CPU restatement of the reference path) on all host
+    threads. Thread t runs first-variable hash partition t of P with its own
+    trie set; P = T is the whole query. P is the smallest
+    multiple of T whose predicted time fits target_s."""
+    T = threads or max(1, min(os.cpu_count() or 1, 64))
+    B, W = calib or cpu_plan(w, plan, min_var, T)
+    P = T
+    while B + W / P > target_s and P < (1 << 16):
+        P *= 2
+    dt, r = _orc_run(w, plan, w.atom_columns(), min_var, T, P)
+    frac = T / P
+    tuples = w.input_tuples() * frac + r["count"]
+    what = "the whole query" if P == T else f"{T} of {P} first-variable hash partitions ({frac:.4f} of the query)"
+    return {"value": tuples / dt, "unit": UNIT, "cores": T, "kind": "port",
+            "sample": f"{what}; {T} threads, one independent trie set each"
+                      + ("" if P == T else "; input tuples scaled by the fraction"),
+            "seconds": dt, "sample_output_tuples": r["count"], "calib": (B, W)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2301_10841_b200 import plan as P
+    w = workload(args.config)
+    plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+    head = P.head_variables(w.query)
+    mv = head.index(w.min_var) if w.min_var else -1
+    T = max(1, min(os.cpu_count() or 1, 64))
+    calib = cpu_plan(w, plan, mv, T)
+    target = max(1.0, min(60.0, 200.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample(w, plan, mv, target, threads=T, calib=calib)
+    vals, secs, last = [], [], None
+    for _ in range(args.steps):
+        last = cpu_sample(w, plan, mv, target, threads=T, calib=calib)
+        vals.append(last["value"])
+        secs.append(last["seconds"])
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators)",
+            "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "parallelism": "cpu-threads"},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port",
+                             "sample": last["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg ---
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    import paper_2301_10841_b200 as fjg
+    from paper_2301_10841_b200 import plan as P
+
+    w = workload(args.config)
+    plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+    head = P.head_variables(w.query)
+    mv = w.min_var
+    eng = fjg.Engine(local)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr, device=torch.device("cuda", local))
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    if world > 1:
+        from paper_2301_10841_b200 import dist as D
+        sharded = D.ShardedQuery(eng, w, plan, world, rank)
+        step = lambda timing=False: sharded.execute(min_var=mv, timing=timing)  # noqa: E731
+        input_tuples_local = sharded.input_tuples_local
+    else:
+        q, _, rels = fjg.prepare_workload(eng, w)
+        step = lambda timing=False: q.execute(min_var=mv, timing=timing, batch_size=args.batch)  # noqa: E731
+        input_tuples_local = w.input_tuples()
+
+    for _ in range(max(args.warmup, 1)):
+        res = step()
+    # ---- timed region: K steps, device events on the engine stream ----
+    clocks = Clocks(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    eng.sync()
+    clocks.start()
+    t_wall0 = time.perf_counter()
+    evs = []
+    results = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = step(timing=True)
+        e1.record(stream)
+        with torch.cuda.stream(stream):
+            flush.add_(1)  # L2 flush between timed steps (outside the event pair)
+        evs.append((e0, e1))
+        results.append(res)
+    eng.sync()
+    torch.cuda.synchronize()
+    barrier(world)
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for (a, b) in evs]
+    dev_ms_total = sum(step_ms)
+    dev_ms_total = allreduce_max(dev_ms_total, world)
+    ms_per_step = dev_ms_total / args.steps
+    out_local = results[-1].count
+    units_local = input_tuples_local + out_local
+    units = allreduce_sum(units_local, world)
+    value = units / (ms_per_step / 1000.0)
+    launches = sum(r.kernel_launches for r in results)
+
+    # ---- roofline: fused last-node kernel (dominant; see profiles/) ----
+    hbm, hbm_kind = peaks()
+    r0 = results[-1]
+    last_ms = statistics.mean(r.last_node_ms / max(r.last_node_launches, 1) for r in results)
+    last_bytes = last_node_bytes(plan, w.query, r0) / max(r0.last_node_launches, 1)
+    achieved = last_bytes / (last_ms / 1000.0) / 1e9 if last_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        e2e = e2e_leg(fjg, eng, w, stream, mv, args.e2e_steps, flush)
+
+    # ---- CPU baseline (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_sample(w, plan, head.index(mv) if mv else -1, args.cpu_target_s)
+            for k in ("seconds", "sample_output_tuples", "calib"):
+                cpu.pop(k, None)
+        except Exception as ex:  # the CPU leg must not sink the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators, resident in HBM)",
+            "config": {"workload": w.name, **w.params, "plan_mode": w.mode,
+                       "parallelism": f"hash-partition x{world}" if world > 1 else "single-gpu",
+                       "l2": "flushed between timed steps (2x126MB write)",
+                       "input_tuples": w.input_tuples(), "output_tuples": out_local if world == 1 else None},
+            "result": {"count": res.count, "checksum": f"{res.checksum:#018x}"},
+            "phases_ms": {"build": statistics.mean(r.build_ms for r in results),
+                          "join": statistics.mean(r.join_ms for r in results),
+                          "last_node": last_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "k_expand<EXPAND_COUNT> (fused last node)",
+                         "algorithmic_bytes_per_launch": last_bytes, "peak_kind": hbm_kind},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "wall_s": t_wall,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def e2e_leg(fjg, eng, w, stream, mv, steps, flush):
+    """Public API end to end: pinned host columns -> fjg_relation_create (H2D)
+    -> filter -> plan compile -> fjg_query_create -> fjg_execute -> result D2H."""
+    import torch
+    host = {name: [torch.from_numpy(c).pin_memory() for c in cols] for name, cols in w.relations.items()}
+    h2d = sum(t.numel() * 4 for cols in host.values() for t in cols)
+    d2h = 8 * 160  # result counters block (fjg_result / DevCounters) per step
+    times = []
+    units = None
+    for i in range(steps + 1):
+        eng.sync()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        rels = {}
+        for name, cols in host.items():
+            r = eng.relation_host_ptrs([c.data_ptr() for c in cols], cols[0].numel())
+            if w.filters.get(name):
+                r = r.filter(w.filters[name])
+            rels[name] = r
+        q, _, _ = fjg.prepare_workload(eng, w, device_relations=rels)
+        res = q.execute(min_var=mv)
+        e1.record(stream)
+        eng.sync()
+        wall = time.perf_counter() - t0
+        q.close()
+        for r in rels.values():
+            r.close()
+        with torch.cuda.stream(stream):
+            flush.add_(1)
+        if i > 0:  # first iteration warms the memory pool
+            times.append(max(e0.elapsed_time(e1) / 1000.0, 0.0) or wall)
+        units = w.input_tuples() + res.count
+    t = statistics.median(times)
+    return {"value": units / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": 1000 * t, "steps": steps}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -83,13 +83,18 @@ typedef struct {
   uint64_t output_rows;       /* enumerate mode: rows available via fjg_query_output */
   uint64_t probes;            /* get() calls issued by the executor */
   uint64_t probe_misses;
-  uint64_t node_body_entries[FJG_MAX_NODES];
+  uint64_t node_body_entries[FJG_MAX_NODES]; /* cover tuples iterated per node */
+  uint64_t node_probes[FJG_MAX_NODES];       /* get() calls per node */
+  uint64_t node_inputs[FJG_MAX_NODES];       /* bindings entering each node */
   uint64_t maps_built;        /* subtries forced (TrieStats.maps_built) */
   uint64_t keys_inserted;     /* distinct keys inserted into COLT maps */
   uint64_t forces;            /* force batches executed on the device */
   uint64_t rows_forced;       /* offsets regrouped by forcing */
   double build_ms;            /* device time in COLT forcing (if collect_timing) */
   double join_ms;             /* device time in node kernels (if collect_timing) */
+  double last_node_ms;        /* device time of the fused last-node kernel (if collect_timing) */
+  uint64_t last_node_launches;
+  uint64_t last_node_candidates; /* cover candidates expanded by the last node */
   uint32_t kernel_launches;   /* kernels this library launched for the call */
   uint32_t host_syncs;
 } fjg_result;
@@ -125,6 +130,8 @@ int fjg_plan_op(const char* op, const char* query_json, const char* arg_json, ch
 /* ---- engine (one per device/stream) ---- */
 int fjg_engine_create(int device, fjg_engine** out);
 void fjg_engine_destroy(fjg_engine* eng);
+/* The engine's cudaStream_t (for event timing by the caller). */
+void* fjg_engine_stream(fjg_engine* eng);
 /* Wait for all work of the engine's stream. */
 int fjg_engine_sync(fjg_engine* eng);
 

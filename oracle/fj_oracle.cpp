@@ -166,6 +166,68 @@ struct KeyHash {
   size_t operator()(const Key& k) const { return fmix64(tuple_hash(k.v, k.n)); }
 };
 
+// Flat open-addressing map Key -> Node* (the HashMap<Tuple, COLT> of Fig 12),
+// insertion-ordered entries, linear probing on a power-of-two index.
+struct Node;
+struct FlatMap {
+  std::vector<uint64_t> hs;   // per index slot: 0 empty, else entry+1 in low 32 bits, hash tag high
+  std::vector<Key> keys;
+  std::vector<Node*> vals;
+  uint64_t mask = 0;
+  size_t size() const { return keys.size(); }
+  void reserve(size_t n) {
+    uint64_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    if (cap > mask + 1) rehash(cap);
+  }
+  void rehash(uint64_t cap) {
+    hs.assign(cap, 0);
+    mask = cap - 1;
+    for (size_t e = 0; e < keys.size(); ++e) place(KeyHash()(keys[e]), e);
+  }
+  void place(uint64_t h, size_t e) {
+    uint64_t i = h & mask;
+    while (hs[i]) i = (i + 1) & mask;
+    hs[i] = ((h >> 32) << 32) | (uint64_t)(e + 1);
+  }
+  Node* find(const Key& k) const {
+    if (keys.empty()) return nullptr;
+    const uint64_t h = KeyHash()(k);
+    uint64_t i = h & mask;
+    while (hs[i]) {
+      const uint64_t e = (hs[i] & 0xffffffffULL) - 1;
+      if ((hs[i] >> 32) == (h >> 32) && keys[e] == k) return vals[e];
+      i = (i + 1) & mask;
+    }
+    return nullptr;
+  }
+  // returns the slot for k, inserting a null value if absent
+  Node*& get_or_insert(const Key& k, bool& inserted) {
+    if (2 * (keys.size() + 1) > mask + 1) rehash(std::max<uint64_t>(16, 2 * (mask + 1)));
+    const uint64_t h = KeyHash()(k);
+    uint64_t i = h & mask;
+    while (hs[i]) {
+      const uint64_t e = (hs[i] & 0xffffffffULL) - 1;
+      if ((hs[i] >> 32) == (h >> 32) && keys[e] == k) {
+        inserted = false;
+        return vals[e];
+      }
+      i = (i + 1) & mask;
+    }
+    keys.push_back(k);
+    vals.push_back(nullptr);
+    hs[i] = ((h >> 32) << 32) | (uint64_t)keys.size();
+    inserted = true;
+    return vals.back();
+  }
+  void swap(FlatMap& o) {
+    hs.swap(o.hs);
+    keys.swap(o.keys);
+    vals.swap(o.vals);
+    std::swap(mask, o.mask);
+  }
+};
+
 // ------------------------------------------------------------------ COLT ----
 enum Backend { SIMPLE = 0, SLT = 1, COLT = 2 };
 
@@ -178,7 +240,7 @@ struct Node {
   enum Kind : uint8_t { BaseScan, Vec, Map } kind = Vec;
   int level = 0;                    // schema level this node keys on
   std::vector<uint32_t> offs;       // Vec
-  std::unordered_map<Key, Node*, KeyHash> map;  // Map
+  FlatMap map;                      // Map
   uint64_t rows = 0;                // offsets under this node
 };
 
@@ -208,21 +270,19 @@ struct Colt {
   // force (Fig 12 `force`): group offsets by key; idempotent.
   void force(Node& nd) {
     if (nd.kind == Node::Map) return;
-    std::unordered_map<Key, Node*, KeyHash> m;
+    FlatMap m;
+    m.reserve(std::min<uint64_t>(length(nd), 1u << 16));
     auto visit = [&](uint64_t i) {
       Key k = key_at(nd.level, i);
-      auto it = m.find(k);
-      Node* c;
-      if (it == m.end()) {
+      bool ins;
+      Node*& slot = m.get_or_insert(k, ins);
+      if (ins) {
         arena.emplace_back(new Node());
-        c = arena.back().get();
-        c->kind = Node::Vec;
-        c->level = nd.level + 1;
-        m.emplace(k, c);
-      } else {
-        c = it->second;
+        slot = arena.back().get();
+        slot->kind = Node::Vec;
+        slot->level = nd.level + 1;
       }
-      c->offs.push_back((uint32_t)i);
+      slot->offs.push_back((uint32_t)i);
     };
     uint64_t rows = 0;
     if (nd.kind == Node::BaseScan) {
@@ -236,7 +296,7 @@ struct Colt {
     nd.kind = Node::Map;
     nd.map.swap(m);
     nd.rows = rows;
-    for (auto& kv : nd.map) kv.second->rows = kv.second->offs.size();
+    for (Node* c : nd.map.vals) c->rows = c->offs.size();
     stats.maps_built += 1;
     stats.forces += 1;
     stats.keys_inserted += nd.map.size();
@@ -251,7 +311,7 @@ struct Colt {
       std::function<void(Node&)> rec = [&](Node& nd) {
         if (nd.level >= map_levels) return;
         force(nd);
-        for (auto& kv : nd.map) rec(*kv.second);
+        for (Node* c : nd.map.vals) rec(*c);
       };
       rec(root);
     } else if (b == SLT) {
@@ -308,9 +368,9 @@ struct Exec {
     if (res.count_lo < old) ++res.count_hi;
   }
   // output (Fig 8 line `output(tuple)`): leaf multiplicities, SURVEY App. A.4
-  void emit(const int64_t* vals, const std::vector<Sub>& subs) {
+  void emit(const int64_t* vals, const Sub* subs, int A) {
     uint64_t mult = 1;
-    for (size_t a = 0; a < subs.size(); ++a)
+    for (int a = 0; a < A; ++a)
       if (!subs[a].singleton) mult *= tries[a]->length(*subs[a].node);
     if (mult == 0) return;
     add_count(mult);
@@ -346,24 +406,29 @@ struct Exec {
     }
     Colt& T = *tries[atom];
     T.force(*sub.node);
-    auto it = sub.node->map.find(key);
-    if (it == sub.node->map.end()) {
+    Node* c = sub.node->map.find(key);
+    if (!c) {
       ++res.misses;
       return false;
     }
-    out.node = it->second;
+    out.node = c;
     out.singleton = false;
     return true;
   }
 
-  struct Cand {
-    std::vector<int64_t> vals;
-    std::vector<Sub> subs;
+  // per-node batch buffers (Fig 13 `tup_subtries`), reused across calls
+  struct Batch {
+    std::vector<int64_t> vals;  // n x nvars
+    std::vector<Sub> subs;      // n x natoms
+    std::vector<char> alive;
+    size_t n = 0;
   };
+  std::vector<Batch> batches;
 
-  void join(int k, std::vector<int64_t>& vals, std::vector<Sub>& subs) {
+  void join(int k, const int64_t* vals, const Sub* subs) {
+    const int A = (int)tries.size();
     if (k == (int)nodes.size()) {
-      emit(vals.data(), subs);
+      emit(vals, subs, A);
       return;
     }
     const PNode& N = nodes[k];
@@ -371,9 +436,9 @@ struct Exec {
       uint64_t mult = 1;
       std::set<int> suffix_atoms;
       for (size_t j = k; j < nodes.size(); ++j) suffix_atoms.insert(nodes[j].subs[0].atom);
-      for (size_t a = 0; a < subs.size(); ++a) {
+      for (int a = 0; a < A; ++a) {
         uint64_t len = subs[a].singleton ? 1 : tries[a]->length(*subs[a].node);
-        if (suffix_atoms.count((int)a) || !subs[a].singleton) mult *= len;
+        if (suffix_atoms.count(a) || !subs[a].singleton) mult *= len;
       }
       add_count(mult);
       res.factorized = 1;
@@ -396,72 +461,82 @@ struct Exec {
     const PSub& C = N.subs[ci];
     Colt& CT = *tries[C.atom];
     const Sub csub = subs[C.atom];
-    // iter / iter_batch over the cover (Fig 12 iter, Fig 13 iter_batch)
-    std::vector<Cand> batch;
+    Batch& B = batches[k];
+    const size_t cap = batch_size();
+    B.n = 0;
+    B.vals.resize(cap * nvars);
+    B.subs.resize(cap * A);
+    B.alive.resize(cap);
+    Key key;
     auto flush = [&]() {
       // probe each other trie over the whole surviving batch (Fig 13)
-      std::vector<char> alive(batch.size(), 1);
+      for (size_t b = 0; b < B.n; ++b) B.alive[b] = 1;
       for (size_t s = 0; s < N.subs.size(); ++s) {
         if ((int)s == ci) continue;
         const PSub& P = N.subs[s];
-        for (size_t b = 0; b < batch.size(); ++b) {
-          if (!alive[b]) continue;
-          Key key;
+        for (size_t b = 0; b < B.n; ++b) {
+          if (!B.alive[b]) continue;
+          const int64_t* v = &B.vals[b * nvars];
           key.n = (int)P.vars.size();
-          for (int t = 0; t < key.n; ++t) key.v[t] = batch[b].vals[P.vars[t]];
+          for (int t = 0; t < key.n; ++t) key.v[t] = v[P.vars[t]];
           Sub out;
-          if (!get(P.atom, batch[b].subs[P.atom], key, out))
-            alive[b] = 0;
+          Sub& cur = B.subs[b * A + P.atom];
+          if (!get(P.atom, cur, key, out))
+            B.alive[b] = 0;
           else
-            batch[b].subs[P.atom] = out;
+            cur = out;
         }
       }
-      for (size_t b = 0; b < batch.size(); ++b)
-        if (alive[b]) join(k + 1, batch[b].vals, batch[b].subs);
-      batch.clear();
+      const size_t n = B.n;
+      B.n = 0;
+      for (size_t b = 0; b < n; ++b)
+        if (B.alive[b]) join(k + 1, &B.vals[b * nvars], &B.subs[b * A]);
     };
-    auto offer = [&](const Key& t, const Sub& residual) {
-      Cand c;
-      c.vals = vals;
+    // B must not be reused while recursing: deeper nodes use batches[k+1..]
+    auto offer = [&](const int64_t* t, const Sub& residual) {
+      int64_t* v = &B.vals[B.n * nvars];
+      std::copy(vals, vals + nvars, v);
       for (int i = 0; i < (int)C.vars.size(); ++i) {
-        const int v = C.vars[i];
-        if ((N.avs_mask >> v) & 1u) {
-          if (c.vals[v] != t.v[i]) return;  // cover re-binds a bound variable: must agree
+        const int x = C.vars[i];
+        if ((N.avs_mask >> x) & 1u) {
+          if (v[x] != t[i]) return;  // cover re-binds a bound variable: must agree
         } else {
-          c.vals[v] = t.v[i];
+          v[x] = t[i];
         }
       }
-      if (k == 0 && nparts > 1 && partition_of(c.vals[part_var], (uint32_t)nparts) != (uint32_t)part) return;
+      if (k == 0 && nparts > 1 && partition_of(v[part_var], (uint32_t)nparts) != (uint32_t)part) return;
       ++res.body[k];
-      c.subs = subs;
-      c.subs[C.atom] = residual;
-      batch.push_back(std::move(c));
-      if (batch.size() >= batch_size()) flush();
+      Sub* sb = &B.subs[B.n * A];
+      std::copy(subs, subs + A, sb);
+      sb[C.atom] = residual;
+      if (++B.n >= cap) flush();
     };
+    int64_t t[MAXK];
     if (csub.singleton) {
-      Key t;
-      t.n = 0;
       offer(t, csub);
     } else if (C.stream && csub.node->kind != Node::Map) {
       // suffix vector: stream values at the offsets, each row its own tuple
-      auto row = [&](uint32_t i) {
-        Key t;
-        t.n = (int)C.cols.size();
-        for (int q = 0; q < t.n; ++q) t.v[q] = CT.rel->at(C.cols[q], i);
-        Sub r;
-        r.singleton = true;
-        offer(t, r);
-      };
-      if (csub.node->kind == Node::BaseScan)
-        for (uint64_t i = 0; i < CT.rel->n; ++i) row((uint32_t)i);
-      else
-        for (uint32_t i : csub.node->offs) row(i);
+      Sub r;
+      r.singleton = true;
+      const int nc = (int)C.cols.size();
+      if (csub.node->kind == Node::BaseScan) {
+        for (uint64_t i = 0; i < CT.rel->n; ++i) {
+          for (int q = 0; q < nc; ++q) t[q] = CT.rel->at(C.cols[q], i);
+          offer(t, r);
+        }
+      } else {
+        for (uint32_t i : csub.node->offs) {
+          for (int q = 0; q < nc; ++q) t[q] = CT.rel->at(C.cols[q], i);
+          offer(t, r);
+        }
+      }
     } else {
       CT.force(*csub.node);
-      for (auto& kv : csub.node->map) {
+      const FlatMap& mp = csub.node->map;
+      for (size_t e = 0; e < mp.size(); ++e) {
         Sub r;
-        r.node = kv.second;
-        offer(kv.first, r);
+        r.node = mp.vals[e];
+        offer(mp.keys[e].v, r);
       }
     }
     flush();
@@ -575,7 +650,8 @@ static Result run_one(const Prepared& P, const std::vector<Relation>& rels, int 
     ex.tries.push_back(std::move(T));
   }
   std::vector<int64_t> vals(ex.nvars, 0);
-  ex.join(0, vals, subs);
+  ex.batches.resize(P.nodes.size() + 1);
+  ex.join(0, vals.data(), subs.data());
   for (auto& T : ex.tries) {
     ex.res.maps_built += T->stats.maps_built;
     ex.res.keys_inserted += T->stats.keys_inserted;
@@ -656,7 +732,8 @@ static void fill(orc_result* out, const orc::Result& r) {
 
 // Execute a Free Join plan on the CPU. part/nparts: only bindings whose first
 // plan variable hashes to `part` (independent trie set).
-// nthreads > 1 runs nparts = nthreads partitions in parallel threads and sums.
+// nthreads > 1: thread t runs partition part+t of P = max(nparts, nthreads)
+// (part=0, nparts<=nthreads covers the whole query) and the results are summed.
 int orc_execute(const char* query_json, const char* plan_json, const int32_t* const* const* atom_cols,
                 const int* atom_ncols, const uint64_t* atom_rows, int natoms, int backend, uint64_t batch_size,
                 int dynamic, int output_mode, int min_var, int part, int nparts, int nthreads, orc_result* out,
@@ -678,7 +755,8 @@ int orc_execute(const char* query_json, const char* plan_json, const int32_t* co
       for (int t = 0; t < nthreads; ++t)
         th.emplace_back([&, t] {
           try {
-            rs[t] = orc::run_one(P, rels, backend, batch_size, dynamic, output_mode, min_var, t, nthreads,
+            const int PP = std::max(nparts, nthreads);
+            rs[t] = orc::run_one(P, rels, backend, batch_size, dynamic, output_mode, min_var, (part + t) % PP, PP,
                                  cp ? &cs[t] : nullptr);
           } catch (const std::exception& e) {
             errs[t] = e.what();

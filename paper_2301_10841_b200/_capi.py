@@ -51,9 +51,12 @@ class Result(C.Structure):
     _fields_ = [("count_lo", C.c_uint64), ("count_hi", C.c_uint64), ("checksum", C.c_uint64),
                 ("min_value", C.c_int64), ("has_min", C.c_int32), ("num_nodes", C.c_int32),
                 ("output_rows", C.c_uint64), ("probes", C.c_uint64), ("probe_misses", C.c_uint64),
-                ("node_body_entries", C.c_uint64 * MAX_NODES), ("maps_built", C.c_uint64),
+                ("node_body_entries", C.c_uint64 * MAX_NODES), ("node_probes", C.c_uint64 * MAX_NODES),
+                ("node_inputs", C.c_uint64 * MAX_NODES), ("maps_built", C.c_uint64),
                 ("keys_inserted", C.c_uint64), ("forces", C.c_uint64), ("rows_forced", C.c_uint64),
-                ("build_ms", C.c_double), ("join_ms", C.c_double), ("kernel_launches", C.c_uint32),
+                ("build_ms", C.c_double), ("join_ms", C.c_double), ("last_node_ms", C.c_double),
+                ("last_node_launches", C.c_uint64), ("last_node_candidates", C.c_uint64),
+                ("kernel_launches", C.c_uint32),
                 ("host_syncs", C.c_uint32)]
 
 
@@ -75,6 +78,7 @@ def _load():
         "fjg_engine_create": (I, [I, C.POINTER(P)]),
         "fjg_engine_destroy": (None, [P]),
         "fjg_engine_sync": (I, [P]),
+        "fjg_engine_stream": (P, [P]),
         "fjg_relation_create": (I, [P, C.POINTER(P), I, U64, C.POINTER(P)]),
         "fjg_relation_from_device": (I, [P, C.POINTER(P), I, U64, I, C.POINTER(P)]),
         "fjg_relation_filter": (I, [P, C.POINTER(Predicate), I, C.POINTER(P)]),
@@ -103,7 +107,7 @@ lib = _load()
 
 # every symbol include/fjg.h declares (checked by tests/test_capi.py)
 EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_op", "fjg_engine_create",
-            "fjg_engine_destroy", "fjg_engine_sync", "fjg_relation_create", "fjg_relation_from_device",
+            "fjg_engine_destroy", "fjg_engine_sync", "fjg_engine_stream", "fjg_relation_create", "fjg_relation_from_device",
             "fjg_relation_filter", "fjg_relation_rows", "fjg_relation_cols", "fjg_relation_device_col",
             "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition", "fjg_query_create",
             "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_destroy",

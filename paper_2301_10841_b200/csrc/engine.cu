@@ -573,7 +573,10 @@ __global__ void __launch_bounds__(256) k_expand(const DevNode* __restrict__ nd, 
   misses = warp_sum(misses);
   body = warp_sum(body);
   if (lane == 0) {
-    if (probes) atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
     if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
     if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
   }
@@ -739,6 +742,7 @@ struct fjg_engine {
   uint32_t launches = 0;
   uint32_t syncs = 0;
   int num_sms = 148;
+  DevCounters* h_ctr = nullptr;  // pinned; shared by the engine's queries (execute is synchronous)
 };
 
 struct fjg_relation {
@@ -806,7 +810,6 @@ struct fjg_query {
   DevTrie* d_tries = nullptr;
   DevCounters* d_ctr = nullptr;
   DevCounters* h_ctr = nullptr;  // pinned
-  uint64_t* h_scratch = nullptr; // pinned
   std::vector<void*> bufs;       // pool allocations of this query
   uint64_t cap = 0;              // frontier capacity (candidates per chunk)
   uint64_t max_n = 0;
@@ -823,9 +826,36 @@ struct fjg_query {
   bool dynamic = true;
   uint64_t batch = 0;
   int min_var = -1;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  double build_ms = 0, join_ms = 0;
+  // non-blocking phase timer: event pairs resolved after the final sync
+  std::vector<cudaEvent_t> events;
+  std::vector<std::pair<int, int>> marks;  // (event index, phase) ; phase<0 = start
+  size_t ev_used = 0;
+  double phase_ms[3] = {0, 0, 0};          // 0 force (build), 1 node kernels, 2 last node
+  double build_ms = 0, join_ms = 0, last_ms = 0;
+  uint64_t last_launches = 0, last_candidates = 0;
+  uint64_t node_inputs[MAXN] = {0};
   bool timing = false;
+  void mark(cudaStream_t st, int tag) {
+    if (!timing) return;
+    if (ev_used == events.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) throw fj::ResourceError("cudaEventCreate failed");
+      events.push_back(e);
+    }
+    if (cudaEventRecord(events[ev_used], st) != cudaSuccess) throw fj::EngineError("cudaEventRecord failed");
+    marks.emplace_back((int)ev_used, tag);
+    ++ev_used;
+  }
+  void resolve_marks() {
+    // marks come in (start, end) pairs: tag = -1 start, tag >= 0 end of phase tag
+    for (size_t i = 0; i + 1 < marks.size(); i += 2) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, events[marks[i].first], events[marks[i + 1].first]);
+      phase_ms[marks[i + 1].second] += ms;
+    }
+    marks.clear();
+    ev_used = 0;
+  }
 
   void* alloc(size_t bytes) {
     void* p = eng->pool->alloc(bytes);
@@ -835,10 +865,7 @@ struct fjg_query {
   ~fjg_query() {
     if (eng) {
       for (void* p : bufs) eng->pool->free(p);
-      if (h_ctr) cudaFreeHost(h_ctr);
-      if (h_scratch) cudaFreeHost(h_scratch);
-      if (ev0) cudaEventDestroy(ev0);
-      if (ev1) cudaEventDestroy(ev1);
+      for (auto e : events) cudaEventDestroy(e);
     }
   }
 };
@@ -1016,13 +1043,10 @@ static void prepare_query(fjg_query* q) {
   q->d_nodes = (DevNode*)q->alloc(K * sizeof(DevNode));
   q->d_tries = (DevTrie*)q->alloc(q->tries.size() * sizeof(DevTrie));
   q->d_ctr = (DevCounters*)q->alloc(sizeof(DevCounters));
-  CK(cudaMallocHost(&q->h_ctr, sizeof(DevCounters)));
-  CK(cudaMallocHost(&q->h_scratch, 64));
+  q->h_ctr = q->eng->h_ctr;
   std::vector<DevTrie> dt;
   for (auto& T : q->tries) dt.push_back(T.dev);
   CK(cudaMemcpyAsync(q->d_tries, dt.data(), dt.size() * sizeof(DevTrie), cudaMemcpyHostToDevice, q->eng->stream));
-  CK(cudaEventCreate(&q->ev0));
-  CK(cudaEventCreate(&q->ev1));
 }
 
 // (Re)allocate per-node frontier buffers for a candidate capacity `cap`.
@@ -1091,7 +1115,7 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     ++eng->launches;
     upper = T.rel->nrows;
   }
-  if (q->timing) CK(cudaEventRecord(q->ev0, eng->stream));
+  q->mark(eng->stream, -1);
   if (single) {
     CK(cudaMemsetAsync(L.cursor + (l == 0 ? 0 : p0), 0, 4, eng->stream));
     CK(cudaMemsetAsync(L.nkeys + (l == 0 ? 0 : p0), 0, 4, eng->stream));
@@ -1112,13 +1136,7 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank));
   LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   // keys inserted accumulate on the device
-  if (q->timing) {
-    CK(cudaEventRecord(q->ev1, eng->stream));
-    CK(cudaEventSynchronize(q->ev1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
-    q->build_ms += ms;
-  }
+  q->mark(eng->stream, 0);
   q->forces += 1;
   q->maps_built += single ? 1 : count;
   q->rows_forced += single ? len0 : 0;
@@ -1159,6 +1177,7 @@ static void force_claims(fjg_query* q, int k) {
 
 static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (F == 0) return;
+  q->node_inputs[k] += F;
   fjg_engine* eng = q->eng;
   const DevNode& N = q->nodes[k];
   DevNode* dN = q->d_nodes + k;
@@ -1173,8 +1192,8 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   const uint64_t M = q->h_ctr->total_m;
   force_claims(q, k);
   if (M == 0) return;
-  if (q->timing) CK(cudaEventRecord(q->ev0, eng->stream));
   if (N.is_last) {
+    q->mark(eng->stream, -1);
     const unsigned g = grid_for(M, 256, eng->num_sms * 8);
     if (mode == EXPAND_ENUM)
       LAUNCH(eng, k_expand<EXPAND_ENUM><<<g, 256, 0, eng->stream>>>(dN, q->d_tries, 0, M, F, -1, q->out_tuples,
@@ -1182,28 +1201,19 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     else
       LAUNCH(eng, k_expand<EXPAND_COUNT><<<g, 256, 0, eng->stream>>>(dN, q->d_tries, 0, M, F, q->min_var,
                                                                       nullptr, 0, q->d_ctr));
-    if (q->timing) {
-      CK(cudaEventRecord(q->ev1, eng->stream));
-      CK(cudaEventSynchronize(q->ev1));
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
-      q->join_ms += ms;
-    }
+    q->mark(eng->stream, 2);
+    q->last_launches += 1;
+    q->last_candidates += M;
     return;
   }
   for (uint64_t c0 = 0; c0 < M; c0 += q->batch) {
     const uint64_t c1 = std::min(M, c0 + q->batch);
     CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, survivors), 0, 4, eng->stream));
-    if (q->timing && c0) CK(cudaEventRecord(q->ev0, eng->stream));
+    q->mark(eng->stream, -1);
     LAUNCH(eng, k_expand<EXPAND_WRITE><<<grid_for(c1 - c0, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(
                     dN, q->d_tries, c0, c1, F, -1, nullptr, 0, q->d_ctr));
-    if (q->timing) CK(cudaEventRecord(q->ev1, eng->stream));
+    q->mark(eng->stream, 1);
     sync_counters(q);
-    if (q->timing) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
-      q->join_ms += ms;
-    }
     run_node(q, k + 1, q->h_ctr->survivors, mode);
   }
 }
@@ -1229,13 +1239,22 @@ static void reset_query(fjg_query* q) {
   memcpy(q->h_ctr, &z, sizeof(z));
   CK(cudaMemcpyAsync(q->d_ctr, q->h_ctr, sizeof(z), cudaMemcpyHostToDevice, eng->stream));
   q->maps_built = q->forces = q->rows_forced = 0;
-  q->build_ms = q->join_ms = 0;
+  q->build_ms = q->join_ms = q->last_ms = 0;
+  q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = 0;
+  q->last_launches = q->last_candidates = 0;
+  for (int k = 0; k < MAXN; ++k) q->node_inputs[k] = 0;
+  q->marks.clear();
+  q->ev_used = 0;
 }
 
 static void execute_once(fjg_query* q, int mode) {
   reset_query(q);
   run_node(q, 0, 1, mode);
   sync_counters(q);
+  q->resolve_marks();
+  q->build_ms = q->phase_ms[0];
+  q->join_ms = q->phase_ms[1] + q->phase_ms[2];
+  q->last_ms = q->phase_ms[2];
 }
 
 // ============================================================================
@@ -1274,6 +1293,7 @@ int fjg_engine_create(int device, fjg_engine** out) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     e->num_sms = prop.multiProcessorCount;
+    CK(cudaMallocHost(&e->h_ctr, sizeof(DevCounters)));
     *out = e;
   });
 }
@@ -1283,9 +1303,12 @@ void fjg_engine_destroy(fjg_engine* eng) {
   ScopedDevice sd(eng->device);
   cudaStreamSynchronize(eng->stream);
   eng->pool.reset();
+  if (eng->h_ctr) cudaFreeHost(eng->h_ctr);
   cudaStreamDestroy(eng->stream);
   delete eng;
 }
+
+void* fjg_engine_stream(fjg_engine* eng) { return eng ? (void*)eng->stream : nullptr; }
 
 int fjg_engine_sync(fjg_engine* eng) {
   return guard([&] { CK(cudaStreamSynchronize(eng->stream)); });
@@ -1513,13 +1536,20 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     r.output_rows = (o.output_mode == FJG_OUT_ENUMERATE) ? q->out_rows : 0;
     r.probes = H.probes;
     r.probe_misses = H.misses;
-    for (int k = 0; k < MAXN && k < FJG_MAX_NODES; ++k) r.node_body_entries[k] = H.body[k];
+    for (int k = 0; k < MAXN && k < FJG_MAX_NODES; ++k) {
+      r.node_body_entries[k] = H.body[k];
+      r.node_probes[k] = H.node_probes[k];
+      r.node_inputs[k] = q->node_inputs[k];
+    }
     r.maps_built = q->maps_built;
     r.keys_inserted = H.keys_inserted;
     r.forces = q->forces;
     r.rows_forced = q->rows_forced;
     r.build_ms = q->build_ms;
     r.join_ms = q->join_ms;
+    r.last_node_ms = q->last_ms;
+    r.last_node_launches = q->last_launches;
+    r.last_node_candidates = q->last_candidates;
     r.kernel_launches = eng->launches - l0;
     r.host_syncs = eng->syncs - s0;
     *out = r;

@@ -121,6 +121,7 @@ struct DevCounters {
   long long minv;
   uint64_t probes, misses;
   uint64_t body[MAXN];
+  uint64_t node_probes[MAXN];
   uint64_t keys_inserted;
   uint64_t out_rows;
   uint64_t total_m;

@@ -28,12 +28,17 @@ class ExecResult:
     probes: int
     probe_misses: int
     node_body_entries: list
+    node_probes: list
+    node_inputs: list
     maps_built: int
     keys_inserted: int
     forces: int
     rows_forced: int
     build_ms: float
     join_ms: float
+    last_node_ms: float
+    last_node_launches: int
+    last_node_candidates: int
     kernel_launches: int
     host_syncs: int
     output_rows: int = 0
@@ -63,6 +68,11 @@ class Engine:
     def sync(self):
         check(lib.fjg_engine_sync(self._h))
 
+    @property
+    def stream_ptr(self):
+        """cudaStream_t the engine launches on (wrap with torch.cuda.ExternalStream)."""
+        return lib.fjg_engine_stream(self._h)
+
     def relation(self, cols):
         """load columns (host int32 arrays) -> device Relation (fjg_relation_create)."""
         arrs = [np.ascontiguousarray(c, dtype=np.int32) for c in cols]
@@ -73,6 +83,13 @@ class Engine:
         h = C.c_void_p()
         check(lib.fjg_relation_create(self._h, ptrs, len(arrs), n, C.byref(h)))
         return Relation(self, h, keepalive=None)
+
+    def relation_host_ptrs(self, ptrs, nrows):
+        """fjg_relation_create from raw host column pointers (e.g. pinned buffers)."""
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        h = C.c_void_p()
+        check(lib.fjg_relation_create(self._h, arr, len(ptrs), int(nrows), C.byref(h)))
+        return Relation(self, h)
 
     def relation_from_device(self, ptrs, nrows, copy=False, keepalive=None):
         arr = (C.c_void_p * len(ptrs))(*ptrs)
@@ -201,8 +218,11 @@ class Query:
         return ExecResult(count=(r.count_hi << 64) | r.count_lo, checksum=r.checksum,
                           min_value=(r.min_value if r.has_min else None), probes=r.probes,
                           probe_misses=r.probe_misses, node_body_entries=list(r.node_body_entries[:nn]),
+                          node_probes=list(r.node_probes[:nn]), node_inputs=list(r.node_inputs[:nn]),
                           maps_built=r.maps_built, keys_inserted=r.keys_inserted, forces=r.forces,
                           rows_forced=r.rows_forced, build_ms=r.build_ms, join_ms=r.join_ms,
+                          last_node_ms=r.last_node_ms, last_node_launches=r.last_node_launches,
+                          last_node_candidates=r.last_node_candidates,
                           kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
 
     def enumerate(self, batch_size=0, dynamic_cover=True):
