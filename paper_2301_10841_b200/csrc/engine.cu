@@ -68,63 +68,24 @@ __device__ __forceinline__ const int32_t* level_src(const DevTrie& T, int depth,
   return depth == 0 ? T.base[col] : T.lev[depth - 1].cval[col];
 }
 
-__device__ __forceinline__ uint32_t key_word(int nk, const int32_t* vals) {
+template <int N>
+__device__ __forceinline__ uint32_t key_word_r(int nk, const int32_t (&vals)[N]) {
   if (nk == 0) return 0u;
   if (nk == 1) return static_cast<uint32_t>(vals[0]);
   uint64_t h = fj::kTupleHashSeed;
-  for (int t = 0; t < nk; ++t) h = fj::tuple_hash_step(h, vals[t]);
+#pragma unroll
+  for (int t = 0; t < N; ++t)
+    if (t < nk) h = fj::tuple_hash_step(h, vals[t]);
   return static_cast<uint32_t>(fj::fmix64(h));
 }
 
-__device__ __forceinline__ uint4 ld_slot(const Slot* s) {
-  return __ldg(reinterpret_cast<const uint4*>(s));
+// first slot of key word kw inside the region [2p, 2p+2len) of subtrie p
+__device__ __forceinline__ uint64_t region_start(uint32_t p, uint32_t len, uint32_t kw) {
+  const uint32_t h = (uint32_t)(fj::fmix64((uint64_t)kw * 0x9e3779b97f4a7c15ull) >> 32);
+  return 2ull * p + (((uint64_t)h * (2ull * len)) >> 32);
 }
 
-// COLT get (Fig 12 `get`: force then lookup). The subtrie is forced before
-// the probing kernel runs, so this is a pure lookup.
-__device__ __forceinline__ bool colt_get(const DevLevel& L, uint32_t p, int nk, const int32_t* vals,
-                                         uint32_t& q, uint32_t& len) {
-  const uint32_t kw = key_word(nk, vals);
-  uint64_t h = fj::slot_hash(p, kw) & L.mask;
-  while (true) {
-    uint4 s = ld_slot(L.table + h);
-    if (s.x == kEmpty) return false;
-    if (s.x == p && s.y == kw) {
-      bool eq = true;
-      if (nk >= 2)
-        for (int t = 0; t < nk; ++t)
-          if (L.cval[L.keycol[t]][s.z] != vals[t]) eq = false;
-      if (eq) {
-        q = s.z;
-        len = s.w;
-        return true;
-      }
-    }
-    h = (h + 1) & L.mask;
-  }
-}
-
-// subtrie of sub's atom for frontier entry e (root if the atom is untouched)
-__device__ __forceinline__ void subtrie_of(const DevNode& N, const DevSub& S, uint64_t e, uint32_t& p,
-                                           uint32_t& len) {
-  if ((N.in_atoms >> S.atom) & 1u) {
-    p = N.in.p[S.atom][e];
-    len = N.in.len[S.atom][e];
-  } else {
-    p = 0;
-    len = N.atom_n[S.atom];
-  }
-}
-
-// estimated_key_count: forced map -> #keys, vector -> length,
-// BaseScan -> cardinality; never forces.
-__device__ __forceinline__ uint64_t estimate(const DevTrie* tries, const DevSub& S, uint32_t p, uint32_t len) {
-  if (p == kSingleton) return 1;
-  const DevLevel& L = tries[S.trie].lev[S.depth];
-  uint32_t st = *((volatile uint32_t*)(L.state + (S.depth == 0 ? 0 : p)));
-  if (st == 2) return L.nkeys[S.depth == 0 ? 0 : p];
-  return len;
-}
+__device__ __forceinline__ uint4 ld_slot(const Slot* s) { return __ldg(reinterpret_cast<const uint4*>(s)); }
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
@@ -133,10 +94,58 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// COLT get (Fig 12 `get` = force, then lookup): the subtrie was forced by an
+// earlier kernel of this node, so this is a pure lookup in its slot region.
+__device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len, const int32_t (&key)[MAXK],
+                                         uint32_t& q, uint32_t& ql) {
+  const int nk = P.nv;
+  const uint32_t kw = key_word_r(nk, key);
+  const uint64_t lo = 2ull * p, hi = lo + 2ull * len;
+  uint64_t i = region_start(p, len, kw);
+  const Slot* __restrict__ table = P.table;
+  while (true) {
+    const uint4 s = ld_slot(table + i);
+    if (s.y == kEmpty) return false;
+    if (s.x == kw) {
+      bool eq = true;
+      if (nk >= 2) {
+#pragma unroll
+        for (int t = 0; t < MAXK; ++t)
+          if (t < nk && __ldg(P.kcmp[t] + s.y) != key[t]) eq = false;
+      }
+      if (eq) {
+        q = s.y;
+        ql = s.z;
+        return true;
+      }
+    }
+    if (++i == hi) i = lo;
+  }
+}
+
+__device__ __forceinline__ void subtrie_of(const KSub& S, uint64_t e, uint32_t& p, uint32_t& len) {
+  if (S.in_p) {
+    p = __ldg(S.in_p + e);
+    len = __ldg(S.in_len + e);
+  } else {
+    p = 0;
+    len = S.root_n;
+  }
+}
+
+// estimated_key_count: forced map -> #keys, vector -> its
+// length, BaseScan -> cardinality. Never forces.
+__device__ __forceinline__ uint64_t estimate(const KSub& S, uint32_t p, uint32_t len) {
+  if (p == kSingleton) return 1;
+  const uint32_t id = S.depth == 0 ? 0u : p;
+  if (*((volatile const uint32_t*)(S.state + id)) == 2u) return S.nkeys[id];
+  return len;
+}
+
 // ============================================================================
 // k_select: cover choice, candidate counts, force claims
 // ============================================================================
-__device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters* ctr, const DevSub& S, uint32_t p,
+__device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters* ctr, const KSub& S, uint32_t p,
                                               uint32_t len, bool need) {
   // Warp-level dedup of identical subtries (bindings of one parent are
   // adjacent in the frontier), then a CAS on the state word.
@@ -145,7 +154,7 @@ __device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters*
   if (!need) return;
   const unsigned grp = __match_any_sync(want, p);
   const int leader = __ffs(grp) - 1;
-  if ((threadIdx.x & 31) != leader) return;
+  if ((int)(threadIdx.x & 31) != leader) return;
   if (S.depth == 0) {
     ctr->root_need[S.trie] = 1;
     return;
@@ -154,15 +163,14 @@ __device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters*
   if (atomicCAS(L.state + p, 0u, 1u) == 0u) {
     L.cursor[p] = 0;
     L.nkeys[p] = 0;
-    uint32_t idx = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], 1u);
+    const uint32_t idx = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], 1u);
     L.list_p[idx] = p;
     L.list_len[idx] = len;
   }
 }
 
-__global__ void k_select(const DevNode* __restrict__ nd, const DevTrie* __restrict__ tries, uint64_t F,
+__global__ void k_select(const __grid_constant__ KNode N, const DevTrie* __restrict__ tries, uint64_t F,
                          int dynamic, DevCounters* ctr) {
-  const DevNode& N = *nd;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t iters = (F + stride - 1) / stride;
@@ -172,15 +180,15 @@ __global__ void k_select(const DevNode* __restrict__ nd, const DevTrie* __restri
     int best = N.cov[0];
     uint32_t bp = 0, bl = 0;
     if (ok) {
-      subtrie_of(N, N.sub[best], e, bp, bl);
+      subtrie_of(N.sub[best], e, bp, bl);
       if (dynamic && N.ncov > 1) {
-        uint64_t best_est = estimate(tries, N.sub[best], bp, bl);
+        uint64_t best_est = estimate(N.sub[best], bp, bl);
         for (int ci = 1; ci < N.ncov; ++ci) {
           const int s = N.cov[ci];
           uint32_t p, l;
-          subtrie_of(N, N.sub[s], e, p, l);
-          const uint64_t est = estimate(tries, N.sub[s], p, l);
-          if (est < best_est) {
+          subtrie_of(N.sub[s], e, p, l);
+          const uint64_t est = estimate(N.sub[s], p, l);
+          if (est < best_est) {  // ties keep the lowest position
             best_est = est;
             best = s;
             bp = p;
@@ -193,16 +201,13 @@ __global__ void k_select(const DevNode* __restrict__ nd, const DevTrie* __restri
     }
     // claims: the keys-iterated cover and every probed subatom must be forced
     for (int s = 0; s < N.nsub; ++s) {
-      const DevSub& S = N.sub[s];
+      const KSub& S = N.sub[s];
       uint32_t p = 0, l = 0;
       bool need = false;
       if (ok) {
-        subtrie_of(N, S, e, p, l);
+        subtrie_of(S, e, p, l);
         need = (p != kSingleton) && (s != best || !S.stream);
-        if (need) {
-          const DevLevel& L = tries[S.trie].lev[S.depth];
-          need = *((volatile uint32_t*)(L.state + (S.depth == 0 ? 0 : p))) == 0u;
-        }
+        if (need) need = *((volatile const uint32_t*)(S.state + (S.depth == 0 ? 0u : p))) == 0u;
       }
       claim_subtrie(tries, ctr, S, p, l, need);
     }
@@ -210,15 +215,15 @@ __global__ void k_select(const DevNode* __restrict__ nd, const DevTrie* __restri
 }
 
 // ============================================================================
-// force: insert -> assign -> scatter -> finalize  (Fig 12 `force`)
+// force: clear -> insert -> assign -> scatter -> finalize  (Fig 12 `force`)
 // ============================================================================
-// Position iteration over the union of claimed ranges. SINGLE: one subtrie
-// (p0, len0) given by value (the root BaseScan, or a lone claim).
+// Position iteration over the union of claimed ranges. single: one subtrie
+// (p0, len0) given by value (the root BaseScan).
 struct ForceRange {
   const uint32_t* list_p;
   const uint32_t* list_len;
-  const uint32_t* list_scan;  // inclusive
-  const uint32_t* list_count; // device count
+  const uint32_t* list_scan;   // inclusive
+  const uint32_t* list_count;  // device count
   uint32_t p0, len0;
   int single;
 };
@@ -229,9 +234,11 @@ __device__ __forceinline__ uint32_t force_total(const ForceRange& R) {
   return c ? R.list_scan[c - 1] : 0u;
 }
 
-__device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, uint32_t& p, uint32_t& pos) {
+__device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, uint32_t& p, uint32_t& len,
+                                             uint32_t& pos) {
   if (R.single) {
     p = R.p0;
+    len = R.len0;
     pos = R.p0 + i;
     return;
   }
@@ -245,7 +252,27 @@ __device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, ui
   }
   const uint32_t before = lo ? R.list_scan[lo - 1] : 0u;
   p = R.list_p[lo];
+  len = R.list_len[lo];
   pos = p + (i - before);
+}
+
+// clear the slot regions (2 slots per position) and child counts of the
+// claimed subtries
+__global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
+  const DevLevel& L = tries[trie].lev[lev];
+  const uint32_t total = force_total(R);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
+    uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * pos;
+    t[0] = make_uint4(kEmpty, kEmpty, 0u, 0u);
+    t[1] = make_uint4(kEmpty, kEmpty, 0u, 0u);
+    L.cnt[pos] = 0;
+    if (L.srep) {
+      L.srep[2ull * pos] = 0;
+      L.srep[2ull * pos + 1] = 0;
+    }
+  }
 }
 
 template <bool MULTI>
@@ -257,23 +284,27 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
   const uint32_t total = force_total(R);
   const int nk = L.nk;
   const int32_t* src[MAXK];
-  for (int t = 0; t < nk; ++t) src[t] = level_src(T, lev, L.keycol[t]);
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) src[t] = t < nk ? level_src(T, lev, L.keycol[t]) : nullptr;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t p, pos;
-    force_locate(R, i, p, pos);
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
     int32_t vals[MAXK];
-    for (int t = 0; t < nk; ++t) vals[t] = src[t][pos];
-    const uint32_t kw = key_word(nk, vals);
-    const unsigned long long pk = ((unsigned long long)kw << 32) | p;
-    uint64_t h = fj::slot_hash(p, kw) & L.mask;
+#pragma unroll
+    for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
+    const uint32_t kw = key_word_r(nk, vals);
+    const unsigned long long mine = ((unsigned long long)kPending << 32) | kw;
+    const uint64_t lo = 2ull * p, hi = lo + 2ull * len;
+    uint64_t h = region_start(p, len, kw);
     bool won = false;
     while (true) {
       unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
       unsigned long long cur = *((volatile unsigned long long*)addr);
       if (cur == kEmpty64) {
-        unsigned long long old = atomicCAS(addr, kEmpty64, pk);
+        const unsigned long long old = atomicCAS(addr, kEmpty64, mine);
         if (old == kEmpty64) {
           won = true;
+          L.table[h].p = p;
           if (MULTI) {
             *((volatile uint32_t*)(L.srep + h)) = pos + 1;
             __threadfence();
@@ -282,22 +313,22 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
         }
         cur = old;
       }
-      if (cur == pk) {
+      if ((uint32_t)cur == kw) {
         if (!MULTI) break;
         uint32_t r;
         while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
         }
         bool eq = true;
-        for (int t = 0; t < nk; ++t)
-          if (src[t][r - 1] != vals[t]) eq = false;
+#pragma unroll
+        for (int t = 0; t < MAXK; ++t)
+          if (t < nk && src[t][r - 1] != vals[t]) eq = false;
         if (eq) break;
       }
-      h = (h + 1) & L.mask;
+      if (++h == hi) h = lo;
     }
     const uint32_t rank = atomicAdd(&L.table[h].len, 1u);
     tmp_slot[pos] = (uint32_t)h;
     tmp_rank[pos] = rank;
-    L.cnt[pos] = 0;  // child starts are written by k_force_assign
     // warp-aggregated append of new slots
     const unsigned act = __activemask();
     const unsigned wmask = __ballot_sync(act, won);
@@ -382,8 +413,8 @@ __global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int
   const DevLevel& L = T.lev[lev];
   const uint32_t total = force_total(R);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t p, pos;
-    force_locate(R, i, p, pos);
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
     const uint32_t h = tmp_slot[pos];
     const uint32_t dst = L.table[h].q + tmp_rank[pos];
     for (int c = 0; c < T.ncols; ++c) {
@@ -409,11 +440,12 @@ __global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, in
 // ============================================================================
 enum ExpandMode { EXPAND_WRITE = 0, EXPAND_COUNT = 1, EXPAND_ENUM = 2 };
 
-__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t lo, uint64_t hi, uint64_t x) {
+__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ a, uint64_t lo, uint64_t hi,
+                                                    uint64_t x) {
   // first index in [lo, hi] with a[idx] > x (a[hi] > x guaranteed)
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
-    if (a[mid] > x)
+    if (__ldg(a + mid) > x)
       hi = mid;
     else
       lo = mid + 1;
@@ -421,111 +453,150 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t 
   return lo;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_expand(const DevNode* __restrict__ nd, const DevTrie* __restrict__ tries,
-                                                uint64_t c0, uint64_t c1, uint64_t F, int min_var,
-                                                int32_t* __restrict__ out_tuples, uint64_t out_cap,
-                                                DevCounters* ctr) {
-  const DevNode& N = *nd;
-  __shared__ uint64_t s_lo, s_hi;
-  __shared__ uint32_t s_warp[8];
+// Load-balanced search, pass 1: bounds[t] = entry owning candidate c0 + t*TILE
+// (bounds[ntiles] = F-1). Each k_expand tile then searches only
+// [bounds[t], bounds[t+1]] instead of the whole scan.
+constexpr int TILE = 256;
+constexpr uint64_t kLastChunk = 1ull << 28;  // last-node candidates per launch
+__global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1,
+                              uint64_t* __restrict__ bounds) {
+  const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    bounds[t] = (t == ntiles) ? F - 1 : upper_bound_u64(scan, 0, F - 1, c0 + t * TILE);
+}
+
+// Register-resident helpers: W bounds the variables / atoms of the query at
+// compile time so every per-candidate array stays in registers.
+template <int W>
+__device__ __forceinline__ int32_t sel(const int32_t (&a)[W], int v) {
+  int32_t x = 0;
+#pragma unroll
+  for (int u = 0; u < W; ++u)
+    if (u == v) x = a[u];
+  return x;
+}
+
+template <int W>
+__device__ __forceinline__ void put(int32_t (&a)[W], int v, int32_t x) {
+#pragma unroll
+  for (int u = 0; u < W; ++u)
+    if (u == v) a[u] = x;
+}
+
+template <int W>
+__device__ __forceinline__ void put2(uint32_t (&a)[W], uint32_t (&b)[W], int v, uint32_t x, uint32_t y) {
+#pragma unroll
+  for (int u = 0; u < W; ++u)
+    if (u == v) {
+      a[u] = x;
+      b[u] = y;
+    }
+}
+
+// One candidate: iterate the chosen cover at position j of entry e, then probe
+// every other subatom of the node in order. Returns false if the candidate dies.
+template <int MODE, int W>
+__device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64_t j, int32_t (&val)[W],
+                                              uint32_t (&cp)[W], uint32_t (&cl)[W], uint64_t& mult,
+                                              uint64_t& probes, uint64_t& misses) {
+#pragma unroll
+  for (int v = 0; v < W; ++v)
+    if ((N.in_vars >> v) & 1u) val[v] = __ldg(N.in_var[v] + e);
+  if (MODE == EXPAND_WRITE) {
+#pragma unroll
+    for (int a = 0; a < W; ++a)
+      if ((N.in_atoms >> a) & 1u) {
+        cp[a] = __ldg(N.in_p[a] + e);
+        cl[a] = __ldg(N.in_len[a] + e);
+      }
+  }
+  if (N.in_mult) mult = __ldg(N.in_mult + e);
+  // ---- iterate the chosen cover (Fig 12 iter) ----
+  const int ci = N.chosen[e];
+  const KSub& S = N.sub[ci];
+  uint32_t p, len;
+  subtrie_of(S, e, p, len);
+  if (p == kSingleton) {
+    put2(cp, cl, S.atom, kSingleton, 1u);
+  } else {
+    const uint32_t pos = p + (uint32_t)j;
+    if (!S.stream) {
+      // forced map: distinct keys are the child starts
+      const uint32_t c = __ldg(S.cnt + pos);
+      if (c == 0) return false;
+      put2(cp, cl, S.atom, pos, c);
+    } else {
+      put2(cp, cl, S.atom, kSingleton, 1u);  // suffix: stream values at the offsets
+    }
+#pragma unroll
+    for (int t = 0; t < MAXK; ++t)
+      if (t < S.nv) {
+        const int32_t x = __ldg(S.src[t] + pos);
+        const int v = S.var[t];
+        if ((S.bound_mask >> t) & 1) {
+          if (sel(val, v) != x) return false;  // cover re-binds a bound variable
+        } else {
+          put(val, v, x);
+        }
+      }
+  }
+  // ---- probe every other subatom in node order (Fig 13 inner loop) ----
+  for (int s = 0; s < N.nsub; ++s) {
+    if (s == ci) continue;
+    const KSub& P = N.sub[s];
+    uint32_t pp, pl;
+    subtrie_of(P, e, pp, pl);
+    uint32_t q = kSingleton, ql = 1;
+    if (pp != kSingleton) {
+      int32_t key[MAXK];
+#pragma unroll
+      for (int t = 0; t < MAXK; ++t) key[t] = t < P.nv ? sel(val, P.var[t]) : 0;
+      ++probes;
+      if (!colt_get(P, pp, pl, key, q, ql)) {
+        ++misses;
+        return false;
+      }
+    }
+    if (P.last)
+      mult *= ql;  // residual leaf vector: its offsets are the multiplicity
+    else
+      put2(cp, cl, P.atom, q, ql);
+  }
+  return true;
+}
+
+template <int MODE, int W>
+__global__ void __launch_bounds__(TILE) k_expand(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                 uint64_t F, const uint64_t* __restrict__ bounds, int min_var,
+                                                 int32_t* __restrict__ out_tuples, uint64_t out_cap,
+                                                 DevCounters* ctr) {
+  __shared__ uint32_t s_warp[TILE / 32];
   __shared__ uint32_t s_base;
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
   long long acc_min = LLONG_MAX;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t* __restrict__ scan = N.scan;
 
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * blockDim.x; base < c1; base += (uint64_t)gridDim.x * blockDim.x) {
-    if (threadIdx.x == 0) {
-      s_lo = upper_bound_u64(N.scan, 0, F - 1, base);
-      const uint64_t last = min(base + blockDim.x, c1) - 1;
-      s_hi = upper_bound_u64(N.scan, s_lo, F - 1, last);
-    }
-    __syncthreads();
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
     const uint64_t i = base + threadIdx.x;
     bool alive = i < c1;
-    int32_t val[MAXV];
-    uint32_t cp[MAXA], cl[MAXA];
+    int32_t val[W];
+    uint32_t cp[W], cl[W];
     uint64_t mult = 1;
-    uint64_t e = 0;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      val[u] = 0;
+      cp[u] = 0;
+      cl[u] = 0;
+    }
     if (alive) {
-      e = upper_bound_u64(N.scan, s_lo, s_hi, i);
-      const uint64_t j = i - (e ? N.scan[e - 1] : 0ull);
-      for (int v = 0; v < MAXV; ++v)
-        if ((N.in_vars >> v) & 1u) val[v] = N.in.var[v][e];
-      for (int a = 0; a < MAXA; ++a)
-        if ((N.in_atoms >> a) & 1u) {
-          cp[a] = N.in.p[a][e];
-          cl[a] = N.in.len[a][e];
-        }
-      if (N.in.mult) mult = N.in.mult[e];
-      // ---- iterate the chosen cover ----
-      const int ci = N.chosen[e];
-      const DevSub& S = N.sub[ci];
-      uint32_t p, len;
-      subtrie_of(N, S, e, p, len);
-      const DevTrie& T = tries[S.trie];
-      if (p == kSingleton) {
-        cp[S.atom] = kSingleton;
-        cl[S.atom] = 1;
-      } else {
-        const uint32_t pos = p + (uint32_t)j;
-        if (S.stream) {
-          // Fig 12 iter, suffix branch: stream the values at the offsets
-          for (int t = 0; t < S.nv; ++t) {
-            const int32_t x = level_src(T, S.depth, S.col[t])[pos];
-            const int v = S.var[t];
-            if ((S.bound_mask >> t) & 1) {
-              if (val[v] != x) alive = false;
-            } else {
-              val[v] = x;
-            }
-          }
-          cp[S.atom] = kSingleton;
-          cl[S.atom] = 1;
-        } else {
-          // Fig 12 iter, forced map: iterate distinct keys = child starts
-          const DevLevel& L = T.lev[S.depth];
-          const uint32_t c = L.cnt[pos];
-          if (c == 0) {
-            alive = false;
-          } else {
-            for (int t = 0; t < S.nv; ++t) {
-              const int32_t x = L.cval[S.col[t]][pos];
-              const int v = S.var[t];
-              if ((S.bound_mask >> t) & 1) {
-                if (val[v] != x) alive = false;
-              } else {
-                val[v] = x;
-              }
-            }
-            cp[S.atom] = pos;
-            cl[S.atom] = c;
-          }
-        }
-      }
+      const uint64_t e = upper_bound_u64(scan, lo, hi, i);
+      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+      alive = run_candidate<MODE, W>(N, e, j, val, cp, cl, mult, probes, misses);
       if (alive) ++body;
-      // ---- probe every other subatom in node order ----
-      for (int s = 0; s < N.nsub && alive; ++s) {
-        if (s == ci) continue;
-        const DevSub& P = N.sub[s];
-        uint32_t pp, pl;
-        subtrie_of(N, P, e, pp, pl);
-        uint32_t q = kSingleton, ql = 1;
-        if (pp != kSingleton) {
-          int32_t key[MAXK];
-          for (int t = 0; t < P.nv; ++t) key[t] = val[P.var[t]];
-          ++probes;
-          if (!colt_get(tries[P.trie].lev[P.depth], P.depth == 0 ? 0u : pp, P.nv, key, q, ql)) {
-            ++misses;
-            alive = false;
-            break;
-          }
-        }
-        if (P.last)
-          mult *= ql;  // residual leaf vector: its offsets are the multiplicity
-        cp[P.atom] = q;
-        cl[P.atom] = ql;
-      }
     }
     if (MODE == EXPAND_WRITE) {
       const unsigned bal = __ballot_sync(0xffffffffu, alive);
@@ -533,40 +604,46 @@ __global__ void __launch_bounds__(256) k_expand(const DevNode* __restrict__ nd, 
       __syncthreads();
       if (threadIdx.x == 0) {
         uint32_t tot = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-          const uint32_t t = s_warp[w];
+        for (int w = 0; w < TILE / 32; ++w) {
+          const uint32_t c = s_warp[w];
           s_warp[w] = tot;
-          tot += t;
+          tot += c;
         }
         s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
       }
       __syncthreads();
       if (alive) {
         const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
-        for (int v = 0; v < MAXV; ++v)
-          if ((N.out_vars >> v) & 1u) N.out.var[v][o] = val[v];
-        for (int a = 0; a < MAXA; ++a)
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+          if ((N.out_vars >> v) & 1u) N.out_var[v][o] = val[v];
+#pragma unroll
+        for (int a = 0; a < W; ++a)
           if ((N.out_atoms >> a) & 1u) {
-            N.out.p[a][o] = cp[a];
-            N.out.len[a][o] = cl[a];
+            N.out_p[a][o] = cp[a];
+            N.out_len[a][o] = cl[a];
           }
-        if (N.out.mult) N.out.mult[o] = mult;
+        if (N.out_mult) N.out_mult[o] = mult;
       }
+      __syncthreads();
     } else if (alive) {
       if (MODE == EXPAND_COUNT) {
         uint64_t h = fj::kTupleHashSeed;
-        for (int v = 0; v < N.nhead; ++v) h = fj::tuple_hash_step(h, (int64_t)val[v]);
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+          if (v < N.nhead) h = fj::tuple_hash_step(h, (int64_t)val[v]);
         acc_sum += mult * fj::checksum_word(h);
         acc_lo += mult;
         if (acc_lo < mult) ++acc_hi;
-        if (min_var >= 0) acc_min = min(acc_min, (long long)val[min_var]);
+        if (min_var >= 0) acc_min = min(acc_min, (long long)sel(val, min_var));
       } else {
         const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
         for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
-          for (int v = 0; v < N.nhead; ++v) out_tuples[(o + r) * N.nhead + v] = val[v];
+#pragma unroll
+          for (int v = 0; v < W; ++v)
+            if (v < N.nhead) out_tuples[(o + r) * N.nhead + v] = val[v];
       }
     }
-    __syncthreads();
   }
   // ---- flush per-thread accumulators: one atomic per warp ----
   probes = warp_sum(probes);
@@ -606,14 +683,22 @@ __global__ void __launch_bounds__(256) k_expand(const DevNode* __restrict__ nd, 
   }
 }
 
+// host-side dispatch on the query width (max(#vars, #atoms) -> 4 / 8 / 16)
+template <int MODE>
+static void launch_expand(int width, unsigned grid, cudaStream_t st, const KNode& nd, uint64_t c0, uint64_t c1,
+                          uint64_t F, const uint64_t* bounds, int min_var, int32_t* out, uint64_t cap,
+                          DevCounters* ctr) {
+  if (width <= 4)
+    k_expand<MODE, 4><<<grid, TILE, 0, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
+  else if (width <= 8)
+    k_expand<MODE, 8><<<grid, TILE, 0, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
+  else
+    k_expand<MODE, 16><<<grid, TILE, 0, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
+}
+
 // ============================================================================
 // misc kernels
 // ============================================================================
-__global__ void k_fill_slots(Slot* t, uint64_t n) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    reinterpret_cast<uint4*>(t)[i] = make_uint4(kEmpty, kEmpty, 0u, 0u);
-}
-
 __global__ void k_tuple_hash(const int64_t* vals, int arity, uint64_t n, uint64_t* out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t h = fj::kTupleHashSeed;
@@ -805,8 +890,8 @@ struct fjg_query {
   std::vector<AtomInfo> atoms;
   std::vector<fjg_relation*> rels;
   std::vector<PhysTrieHost> tries;
-  std::vector<DevNode> nodes;  // host copies
-  DevNode* d_nodes = nullptr;
+  std::vector<DevNode> nodes;   // host-side node descriptors
+  std::vector<KNode> knodes;    // resolved kernel plans (constant bank)
   DevTrie* d_tries = nullptr;
   DevCounters* d_ctr = nullptr;
   DevCounters* h_ctr = nullptr;  // pinned
@@ -826,6 +911,9 @@ struct fjg_query {
   bool dynamic = true;
   uint64_t batch = 0;
   int min_var = -1;
+  int width = 16;  // max(#variables, #atoms): selects the register-resident kernel variant
+  uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
+  uint64_t bounds_cap = 0;
   // non-blocking phase timer: event pairs resolved after the final sync
   std::vector<cudaEvent_t> events;
   std::vector<std::pair<int, int>> marks;  // (event index, phase) ; phase<0 = start
@@ -881,6 +969,7 @@ static void prepare_query(fjg_query* q) {
   if (A > (size_t)MAXA) throw ValidationError("too many atoms for the device executor (max 16)");
   if (plan.nodes.size() > (size_t)MAXN) throw ValidationError("too many plan nodes (max 32)");
   q->head = fj::head_variables(plan.query);
+  q->width = (int)std::max(q->head.size(), A);
   if (q->head.size() > (size_t)MAXV) throw ValidationError("too many variables (max 16)");
   std::map<std::string, int> vid;
   for (size_t i = 0; i < q->head.size(); ++i) vid[q->head[i]] = (int)i;
@@ -961,9 +1050,8 @@ static void prepare_query(fjg_query* q) {
       H.keycols = T.levels[l];
       H.multi = H.keycols.size() >= 2;
       H.nsub = l == 0 ? 1 : std::max<uint64_t>(n, 1);
-      H.cap = pow2_at_least(std::max<uint64_t>(2 * n, 16));
+      H.cap = 2 * std::max<uint64_t>(n, 1);  // 2 slots per position: per-subtrie regions
       L.table = (Slot*)q->alloc(H.cap * sizeof(Slot));
-      L.mask = H.cap - 1;
       L.srep = H.multi ? (uint32_t*)q->alloc(H.cap * 4) : nullptr;
       L.state = (uint32_t*)q->alloc(H.nsub * 4);
       L.nkeys = (uint32_t*)q->alloc(H.nsub * 4);
@@ -1040,13 +1128,75 @@ static void prepare_query(fjg_query* q) {
       D.stream = !later_vars;
     }
   }
-  q->d_nodes = (DevNode*)q->alloc(K * sizeof(DevNode));
   q->d_tries = (DevTrie*)q->alloc(q->tries.size() * sizeof(DevTrie));
   q->d_ctr = (DevCounters*)q->alloc(sizeof(DevCounters));
   q->h_ctr = q->eng->h_ctr;
   std::vector<DevTrie> dt;
   for (auto& T : q->tries) dt.push_back(T.dev);
   CK(cudaMemcpyAsync(q->d_tries, dt.data(), dt.size() * sizeof(DevTrie), cudaMemcpyHostToDevice, q->eng->stream));
+}
+
+// Resolve each node's descriptor into the constant-bank kernel plan.
+static void build_knodes(fjg_query* q) {
+  const size_t K = q->nodes.size();
+  q->knodes.assign(K, KNode{});
+  for (size_t k = 0; k < K; ++k) {
+    const DevNode& N = q->nodes[k];
+    KNode& G = q->knodes[k];
+    memset(&G, 0, sizeof(G));
+    G.k = N.k;
+    G.nsub = N.nsub;
+    G.ncov = N.ncov;
+    G.nhead = N.nhead;
+    G.is_last = N.is_last;
+    for (int c = 0; c < N.ncov; ++c) G.cov[c] = (int8_t)N.cov[c];
+    G.in_vars = N.in_vars;
+    G.out_vars = N.out_vars;
+    G.in_atoms = N.in_atoms;
+    G.out_atoms = N.out_atoms;
+    for (int v = 0; v < MAXV; ++v) {
+      G.in_var[v] = N.in.var[v];
+      G.out_var[v] = N.out.var[v];
+    }
+    for (int a = 0; a < MAXA; ++a) {
+      G.in_p[a] = N.in.p[a];
+      G.in_len[a] = N.in.len[a];
+      G.out_p[a] = N.out.p[a];
+      G.out_len[a] = N.out.len[a];
+    }
+    G.in_mult = N.in.mult;
+    G.out_mult = N.out.mult;
+    G.chosen = N.chosen;
+    G.m = N.m;
+    G.scan = N.scan;
+    for (int i = 0; i < N.nsub; ++i) {
+      const DevSub& D = N.sub[i];
+      KSub& S = G.sub[i];
+      const DevTrie& T = q->tries[D.trie].dev;
+      const DevLevel& L = T.lev[D.depth];
+      for (int t = 0; t < D.nv; ++t) {
+        S.src[t] = D.stream ? (D.depth == 0 ? T.base[D.col[t]] : T.lev[D.depth - 1].cval[D.col[t]])
+                            : L.cval[D.col[t]];
+        S.kcmp[t] = L.cval[D.col[t]];
+        S.var[t] = (int8_t)D.var[t];
+      }
+      S.cnt = L.cnt;
+      S.table = L.table;
+      S.state = L.state;
+      S.nkeys = L.nkeys;
+      const bool open = (N.in_atoms >> D.atom) & 1u;
+      S.in_p = open ? N.in.p[D.atom] : nullptr;
+      S.in_len = open ? N.in.len[D.atom] : nullptr;
+      S.root_n = N.atom_n[D.atom];
+      S.nv = (uint8_t)D.nv;
+      S.bound_mask = (uint8_t)D.bound_mask;
+      S.stream = (uint8_t)D.stream;
+      S.last = (uint8_t)D.last;
+      S.atom = (uint8_t)D.atom;
+      S.trie = (uint8_t)D.trie;
+      S.depth = (uint8_t)D.depth;
+    }
+  }
 }
 
 // (Re)allocate per-node frontier buffers for a candidate capacity `cap`.
@@ -1074,6 +1224,11 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
     }
   }
   q->cap = cap;
+  const uint64_t nb = std::max<uint64_t>(cap, kLastChunk) / TILE + 2;
+  if (nb > q->bounds_cap) {
+    q->bounds = (uint64_t*)q->alloc(nb * 8);
+    q->bounds_cap = nb;
+  }
   // CUB temp storage for the largest scans
   size_t b1 = 0, b2 = 0;
   CK(cub::DeviceScan::InclusiveSum(nullptr, b1, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)cap));
@@ -1084,7 +1239,7 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
     q->cub_tmp = q->alloc(need);
     q->cub_tmp_bytes = need;
   }
-  CK(cudaMemcpyAsync(q->d_nodes, q->nodes.data(), K * sizeof(DevNode), cudaMemcpyHostToDevice, q->eng->stream));
+  build_knodes(q);
 }
 
 static void sync_counters(fjg_query* q) {
@@ -1122,6 +1277,7 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   }
   CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, newslots), 0, 4, eng->stream));
   const unsigned g = grid_for(upper, 256, eng->num_sms * 16);
+  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   if (T.lev[l].multi)
     LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
                                                                   q->newslots, q->d_ctr));
@@ -1180,8 +1336,8 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   q->node_inputs[k] += F;
   fjg_engine* eng = q->eng;
   const DevNode& N = q->nodes[k];
-  DevNode* dN = q->d_nodes + k;
-  LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(dN, q->d_tries, F,
+  const KNode& KN = q->knodes[k];
+  LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(KN, q->d_tries, F,
                                                                                     q->dynamic ? 1 : 0, q->d_ctr));
   size_t bytes = q->cub_tmp_bytes;
   CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, N.m, N.scan, (int64_t)F, eng->stream));
@@ -1194,13 +1350,18 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (M == 0) return;
   if (N.is_last) {
     q->mark(eng->stream, -1);
-    const unsigned g = grid_for(M, 256, eng->num_sms * 8);
-    if (mode == EXPAND_ENUM)
-      LAUNCH(eng, k_expand<EXPAND_ENUM><<<g, 256, 0, eng->stream>>>(dN, q->d_tries, 0, M, F, -1, q->out_tuples,
-                                                                     q->out_cap, q->d_ctr));
-    else
-      LAUNCH(eng, k_expand<EXPAND_COUNT><<<g, 256, 0, eng->stream>>>(dN, q->d_tries, 0, M, F, q->min_var,
-                                                                      nullptr, 0, q->d_ctr));
+    for (uint64_t c0 = 0; c0 < M; c0 += kLastChunk) {
+      const uint64_t c1 = std::min(M, c0 + kLastChunk);
+      const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
+      LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
+      const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
+      if (mode == EXPAND_ENUM)
+        LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1,
+                                               q->out_tuples, q->out_cap, q->d_ctr));
+      else
+        LAUNCH(eng, launch_expand<EXPAND_COUNT>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, q->min_var,
+                                                nullptr, 0, q->d_ctr));
+    }
     q->mark(eng->stream, 2);
     q->last_launches += 1;
     q->last_candidates += M;
@@ -1210,8 +1371,10 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     const uint64_t c1 = std::min(M, c0 + q->batch);
     CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, survivors), 0, 4, eng->stream));
     q->mark(eng->stream, -1);
-    LAUNCH(eng, k_expand<EXPAND_WRITE><<<grid_for(c1 - c0, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(
-                    dN, q->d_tries, c0, c1, F, -1, nullptr, 0, q->d_ctr));
+    const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
+    LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
+    LAUNCH(eng, launch_expand<EXPAND_WRITE>(q->width, grid_for(c1 - c0, TILE, eng->num_sms * 8), eng->stream, KN,
+                                            c0, c1, F, q->bounds, -1, nullptr, 0, q->d_ctr));
     q->mark(eng->stream, 1);
     sync_counters(q);
     run_node(q, k + 1, q->h_ctr->survivors, mode);
@@ -1224,9 +1387,7 @@ static void reset_query(fjg_query* q) {
     for (size_t l = 0; l < T.lev.size(); ++l) {
       auto& H = T.lev[l];
       DevLevel& L = T.dev.lev[l];
-      if (H.dirty) {
-        LAUNCH(eng, k_fill_slots<<<grid_for(H.cap, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(L.table, H.cap));
-        if (L.srep) CK(cudaMemsetAsync(L.srep, 0, H.cap * 4, eng->stream));
+      if (H.dirty) {  // slot regions and child counts are cleared by the force that claims them
         CK(cudaMemsetAsync(L.state, 0, H.nsub * 4, eng->stream));
         H.dirty = false;
       }

@@ -47,17 +47,22 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr uint64_t kEmpty64 = 0xFFFFFFFFFFFFFFFFull;
 constexpr uint32_t kSingleton = 0xFFFFFFFFu;  // streamed row: residual subtrie is [row]
 
+// Hash map slots. A forced subtrie occupying positions [p, p+len) owns the
+// slot region [2p, 2p+2len) of its level's 2n-slot array (load <= 0.5):
+// regions of distinct subtries are disjoint, so no parent id is needed in the
+// key, probes of one binding stay inside one compact region, and forcing a
+// subtrie clears exactly its own region (no per-query table reset).
 struct __align__(16) Slot {
-  uint32_t p;    // parent subtrie id (kEmpty = free slot)
   uint32_t k;    // key word: the int32 key (arity 1), 0 (arity 0) or a 32-bit tuple hash
-  uint32_t q;    // child start position
+  uint32_t q;    // child start position (kEmpty: free slot, kPending: inserted, unassigned)
   uint32_t len;  // child length
+  uint32_t p;    // owning subtrie id (written at insertion, read by k_force_assign)
 };
+constexpr uint32_t kPending = 0xFFFFFFFEu;
 
 struct DevLevel {
-  Slot* table;
-  uint64_t mask;
-  uint32_t* srep;    // arity >= 2 only: representative position + 1 during insertion
+  Slot* table;       // 2n slots
+  uint32_t* srep;    // arity >= 2 only, per slot: representative position + 1 during insertion
   uint32_t* state;
   uint32_t* nkeys;
   uint32_t* cursor;
@@ -114,6 +119,41 @@ struct DevNode {
   uint8_t* chosen;     // per entry: chosen cover (subatom index)
   uint64_t* m;         // per entry: candidates
   uint64_t* scan;      // inclusive scan of m
+};
+
+// Kernel-side plan of one subatom, every pointer resolved on the host, passed
+// in the constant bank (__grid_constant__ KNode) so the per-candidate code
+// reads no descriptors from memory.
+struct KSub {
+  const int32_t* src[MAXK];   // cover iteration values per var (stream: domain depth-1; keys: cval of depth)
+  const int32_t* kcmp[MAXK];  // probe key compare for arity >= 2: cval of depth at the child start
+  const uint32_t* cnt;        // cnt of depth (keys-mode iteration)
+  const Slot* table;          // slots of depth
+  const uint32_t* state;      // state of depth (estimated_key_count, claims)
+  const uint32_t* nkeys;
+  const uint32_t* in_p;       // frontier subtrie column of this atom (null: root)
+  const uint32_t* in_len;
+  uint32_t root_n;
+  int8_t var[MAXK];
+  uint8_t nv, bound_mask, stream, last, atom, trie, depth, pad;
+};
+
+struct KNode {
+  int k, nsub, ncov, nhead, is_last;
+  int8_t cov[MAXS];
+  uint32_t in_vars, out_vars, in_atoms, out_atoms;
+  const int32_t* in_var[MAXV];
+  int32_t* out_var[MAXV];
+  const uint32_t* in_p[MAXA];
+  const uint32_t* in_len[MAXA];
+  uint32_t* out_p[MAXA];
+  uint32_t* out_len[MAXA];
+  const uint64_t* in_mult;
+  uint64_t* out_mult;
+  uint8_t* chosen;
+  uint64_t* m;
+  uint64_t* scan;
+  KSub sub[MAXS];
 };
 
 struct DevCounters {
