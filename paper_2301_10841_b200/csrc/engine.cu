@@ -79,13 +79,18 @@ __device__ __forceinline__ uint32_t key_word_r(int nk, const int32_t (&vals)[N])
   return static_cast<uint32_t>(fj::fmix64(h));
 }
 
-// first slot of key word kw inside the region [2p, 2p+2len) of subtrie p
-__device__ __forceinline__ uint64_t region_start(uint32_t p, uint32_t len, uint32_t kw) {
-  const uint32_t h = (uint32_t)(fj::fmix64((uint64_t)kw * 0x9e3779b97f4a7c15ull) >> 32);
-  return 2ull * p + (((uint64_t)h * (2ull * len)) >> 32);
+// first bucket (4 slots) of key word kw inside the region of subtrie (p, len)
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
 }
-
-__device__ __forceinline__ uint4 ld_slot(const Slot* s) { return __ldg(reinterpret_cast<const uint4*>(s)); }
+__device__ __forceinline__ uint64_t region_bucket(uint32_t p, uint32_t len, uint32_t kw) {
+  return (uint64_t)p + (((uint64_t)fmix32(kw ^ 0x9e3779b9u) * len) >> 32);
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
@@ -95,31 +100,41 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // COLT get (Fig 12 `get` = force, then lookup): the subtrie was forced by an
-// earlier kernel of this node, so this is a pure lookup in its slot region.
+// earlier kernel of this node, so this is a pure lookup in its slot region:
+// read a bucket (one sector, as two 16-byte halves), stop at a match or at the
+// first free slot.
 __device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len, const int32_t (&key)[MAXK],
                                          uint32_t& q, uint32_t& ql) {
   const int nk = P.nv;
   const uint32_t kw = key_word_r(nk, key);
-  const uint64_t lo = 2ull * p, hi = lo + 2ull * len;
-  uint64_t i = region_start(p, len, kw);
-  const Slot* __restrict__ table = P.table;
+  uint64_t b = region_bucket(p, len, kw);
+  const uint64_t blo = p, bhi = (uint64_t)p + len;
+  const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
   while (true) {
-    const uint4 s = ld_slot(table + i);
-    if (s.y == kEmpty) return false;
-    if (s.x == kw) {
-      bool eq = true;
-      if (nk >= 2) {
 #pragma unroll
-        for (int t = 0; t < MAXK; ++t)
-          if (t < nk && __ldg(P.kcmp[t] + s.y) != key[t]) eq = false;
-      }
-      if (eq) {
-        q = s.y;
-        ql = s.z;
-        return true;
+    for (int half = 0; half < 2; ++half) {
+      const uint4 s = __ldg(tb + 2 * b + half);
+      // slot (s.x, s.y) then (s.z, s.w)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const uint32_t sk = w ? s.z : s.x, sq = w ? s.w : s.y;
+        if (sq == kEmpty) return false;
+        if (sk == kw) {
+          bool eq = true;
+          if (nk >= 2) {
+#pragma unroll
+            for (int t = 0; t < MAXK; ++t)
+              if (t < nk && __ldg(P.kcmp[t] + sq) != key[t]) eq = false;
+          }
+          if (eq) {
+            q = sq;
+            ql = __ldg(P.cnt + sq);
+            return true;
+          }
+        }
       }
     }
-    if (++i == hi) i = lo;
+    if (++b == bhi) b = blo;
   }
 }
 
@@ -256,8 +271,8 @@ __device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, ui
   pos = p + (i - before);
 }
 
-// clear the slot regions (2 slots per position) and child counts of the
-// claimed subtries
+// clear the slot regions (one 4-slot bucket per position) and child counts of
+// the claimed subtries
 __global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
   const DevLevel& L = tries[trie].lev[lev];
   const uint32_t total = force_total(R);
@@ -265,20 +280,21 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int l
     uint32_t p, len, pos;
     force_locate(R, i, p, len, pos);
     uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * pos;
-    t[0] = make_uint4(kEmpty, kEmpty, 0u, 0u);
-    t[1] = make_uint4(kEmpty, kEmpty, 0u, 0u);
+    t[0] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    t[1] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     L.cnt[pos] = 0;
-    if (L.srep) {
-      L.srep[2ull * pos] = 0;
-      L.srep[2ull * pos + 1] = 0;
-    }
+    if (L.srep) reinterpret_cast<uint4*>(L.srep)[pos] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
+// Insert every offset of the claimed subtries: claim a slot for its key (CAS
+// on the 8-byte slot), then count it (the pending slot's q word is the group
+// counter; the returned value is the offset's rank inside its child group).
 template <bool MULTI>
 __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
                                uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
-                               uint32_t* __restrict__ newslots, DevCounters* ctr) {
+                               uint32_t* __restrict__ newslots, uint32_t* __restrict__ newslot_p,
+                               DevCounters* ctr) {
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[lev];
   const uint32_t total = force_total(R);
@@ -293,18 +309,17 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
 #pragma unroll
     for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
     const uint32_t kw = key_word_r(nk, vals);
-    const unsigned long long mine = ((unsigned long long)kPending << 32) | kw;
-    const uint64_t lo = 2ull * p, hi = lo + 2ull * len;
-    uint64_t h = region_start(p, len, kw);
+    const unsigned long long mine = ((unsigned long long)kPendBit << 32) | kw;
+    const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
+    uint64_t h = 4ull * region_bucket(p, len, kw);
     bool won = false;
     while (true) {
       unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
       unsigned long long cur = *((volatile unsigned long long*)addr);
-      if (cur == kEmpty64) {
-        const unsigned long long old = atomicCAS(addr, kEmpty64, mine);
-        if (old == kEmpty64) {
+      if ((uint32_t)(cur >> 32) == kEmpty) {
+        const unsigned long long old = atomicCAS(addr, cur, mine);
+        if (old == cur) {
           won = true;
-          L.table[h].p = p;
           if (MULTI) {
             *((volatile uint32_t*)(L.srep + h)) = pos + 1;
             __threadfence();
@@ -326,7 +341,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
       }
       if (++h == hi) h = lo;
     }
-    const uint32_t rank = atomicAdd(&L.table[h].len, 1u);
+    const uint32_t rank = atomicAdd(&L.table[h].q, 1u) & ~kPendBit;
     tmp_slot[pos] = (uint32_t)h;
     tmp_rank[pos] = rank;
     // warp-aggregated append of new slots
@@ -338,7 +353,9 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
       uint32_t base = 0;
       if (lane == leader) base = atomicAdd(&ctr->newslots, (uint32_t)__popc(wmask));
       base = __shfl_sync(wmask, base, leader);
-      newslots[base + __popc(wmask & ((1u << lane) - 1))] = (uint32_t)h;
+      const uint32_t o = base + __popc(wmask & ((1u << lane) - 1));
+      newslots[o] = (uint32_t)h;
+      newslot_p[o] = p;
     }
   }
 }
@@ -346,7 +363,8 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
 // Child-range allocation: q = p + (running sum of child sizes of p).
 template <bool SINGLE>
 __global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0,
-                               const uint32_t* __restrict__ newslots, DevCounters* ctr) {
+                               const uint32_t* __restrict__ newslots, const uint32_t* __restrict__ newslot_p,
+                               DevCounters* ctr) {
   const DevLevel& L = tries[trie].lev[lev];
   const uint32_t total = ctr->newslots;
   typedef cub::BlockScan<uint32_t, 256> BS;
@@ -360,8 +378,8 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int 
     uint32_t h = 0, c = 0, p = 0;
     if (ok) {
       h = newslots[i];
-      p = L.table[h].p;
-      c = L.table[h].len;
+      p = newslot_p[i];
+      c = L.table[h].q & ~kPendBit;
     }
     uint32_t q = 0;
     if (SINGLE) {
@@ -468,30 +486,33 @@ __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uin
 
 // Register-resident helpers: W bounds the variables / atoms of the query at
 // compile time so every per-candidate array stays in registers.
+// (arithmetic blends: a plain `if (u == v) a[u] = x` is pattern-matched back
+// into an indexed local-memory store)
 template <int W>
 __device__ __forceinline__ int32_t sel(const int32_t (&a)[W], int v) {
   int32_t x = 0;
 #pragma unroll
-  for (int u = 0; u < W; ++u)
-    if (u == v) x = a[u];
+  for (int u = 0; u < W; ++u) x |= a[u] & -(int32_t)(u == v);
   return x;
 }
 
 template <int W>
 __device__ __forceinline__ void put(int32_t (&a)[W], int v, int32_t x) {
 #pragma unroll
-  for (int u = 0; u < W; ++u)
-    if (u == v) a[u] = x;
+  for (int u = 0; u < W; ++u) {
+    const int32_t m = -(int32_t)(u == v);
+    a[u] = (x & m) | (a[u] & ~m);
+  }
 }
 
 template <int W>
 __device__ __forceinline__ void put2(uint32_t (&a)[W], uint32_t (&b)[W], int v, uint32_t x, uint32_t y) {
 #pragma unroll
-  for (int u = 0; u < W; ++u)
-    if (u == v) {
-      a[u] = x;
-      b[u] = y;
-    }
+  for (int u = 0; u < W; ++u) {
+    const uint32_t m = 0u - (uint32_t)(u == v);
+    a[u] = (x & m) | (a[u] & ~m);
+    b[u] = (y & m) | (b[u] & ~m);
+  }
 }
 
 // One candidate: iterate the chosen cover at position j of entry e, then probe
@@ -901,6 +922,7 @@ struct fjg_query {
   uint32_t* tmp_slot = nullptr;
   uint32_t* tmp_rank = nullptr;
   uint32_t* newslots = nullptr;
+  uint32_t* newslot_p = nullptr;
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
   int32_t* out_tuples = nullptr;
@@ -1050,7 +1072,7 @@ static void prepare_query(fjg_query* q) {
       H.keycols = T.levels[l];
       H.multi = H.keycols.size() >= 2;
       H.nsub = l == 0 ? 1 : std::max<uint64_t>(n, 1);
-      H.cap = 2 * std::max<uint64_t>(n, 1);  // 2 slots per position: per-subtrie regions
+      H.cap = 4 * std::max<uint64_t>(n, 1);  // one 4-slot bucket per position: per-subtrie regions
       L.table = (Slot*)q->alloc(H.cap * sizeof(Slot));
       L.srep = H.multi ? (uint32_t*)q->alloc(H.cap * 4) : nullptr;
       L.state = (uint32_t*)q->alloc(H.nsub * 4);
@@ -1072,6 +1094,8 @@ static void prepare_query(fjg_query* q) {
   q->tmp_slot = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->tmp_rank = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->newslots = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  q->newslot_p = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  if (q->max_n >= (1ull << 31)) throw ValidationError("relations must have fewer than 2^31 rows");
   // static node descriptors
   const size_t K = plan.nodes.size();
   q->nodes.assign(K, DevNode{});
@@ -1280,15 +1304,17 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   if (T.lev[l].multi)
     LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
-                                                                  q->newslots, q->d_ctr));
+                                                                  q->newslots, q->newslot_p, q->d_ctr));
   else
     LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
-                                                                   q->newslots, q->d_ctr));
+                                                                   q->newslots, q->newslot_p, q->d_ctr));
   const unsigned ga = grid_for(upper, 256, eng->num_sms * 8);
   if (single)
-    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, p0, q->newslots, q->d_ctr));
+    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, p0, q->newslots, q->newslot_p,
+                                                                  q->d_ctr));
   else
-    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, q->newslots, q->d_ctr));
+    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, q->newslots,
+                                                                   q->newslot_p, q->d_ctr));
   LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank));
   LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   // keys inserted accumulate on the device

@@ -48,20 +48,20 @@ constexpr uint64_t kEmpty64 = 0xFFFFFFFFFFFFFFFFull;
 constexpr uint32_t kSingleton = 0xFFFFFFFFu;  // streamed row: residual subtrie is [row]
 
 // Hash map slots. A forced subtrie occupying positions [p, p+len) owns the
-// slot region [2p, 2p+2len) of its level's 2n-slot array (load <= 0.5):
-// regions of distinct subtries are disjoint, so no parent id is needed in the
-// key, probes of one binding stay inside one compact region, and forcing a
-// subtrie clears exactly its own region (no per-query table reset).
-struct __align__(16) Slot {
-  uint32_t k;    // key word: the int32 key (arity 1), 0 (arity 0) or a 32-bit tuple hash
-  uint32_t q;    // child start position (kEmpty: free slot, kPending: inserted, unassigned)
-  uint32_t len;  // child length
-  uint32_t p;    // owning subtrie id (written at insertion, read by k_force_assign)
+// slot region [4p, 4p+4len) of its level's 4n-slot array: len buckets of 4
+// slots, one 32-byte sector each (load <= 0.25). Regions of distinct subtries
+// are disjoint, so no parent id is needed in the key, the probes of one
+// binding stay inside one compact region, a probe is almost always one
+// sector, and forcing a subtrie clears exactly its own region (no per-query
+// table reset). The child length lives in cnt[q] (read on hits only).
+struct __align__(8) Slot {
+  uint32_t k;  // key word: the int32 key (arity 1), 0 (arity 0) or a 32-bit tuple hash
+  uint32_t q;  // child start (kEmpty: free; kPendBit|count while the force is inserting)
 };
-constexpr uint32_t kPending = 0xFFFFFFFEu;
+constexpr uint32_t kPendBit = 0x80000000u;  // positions are < 2^31
 
 struct DevLevel {
-  Slot* table;       // 2n slots
+  Slot* table;       // 4n slots
   uint32_t* srep;    // arity >= 2 only, per slot: representative position + 1 during insertion
   uint32_t* state;
   uint32_t* nkeys;
