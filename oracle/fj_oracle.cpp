@@ -233,6 +233,7 @@ enum Backend { SIMPLE = 0, SLT = 1, COLT = 2 };
 
 struct TrieStats {
   uint64_t maps_built = 0, keys_inserted = 0, forces = 0;
+  uint32_t level_mask = 0;  // bit l: some map was built at schema level l
 };
 
 // NodeBody: Map | Vec (row offsets) | BaseScan.
@@ -299,6 +300,7 @@ struct Colt {
     for (Node* c : nd.map.vals) c->rows = c->offs.size();
     stats.maps_built += 1;
     stats.forces += 1;
+    stats.level_mask |= 1u << nd.level;
     stats.keys_inserted += nd.map.size();
   }
   // eager materialisation for simple (all map levels) / slt (level 0)
@@ -348,6 +350,8 @@ struct Result {
   uint64_t body[32] = {0};
   uint64_t maps_built = 0, keys_inserted = 0, forces = 0;
   int factorized = 0;
+  uint64_t atom_maps[16] = {0}, atom_keys[16] = {0};
+  uint32_t atom_levels[16] = {0};
 };
 
 struct Exec {
@@ -652,10 +656,16 @@ static Result run_one(const Prepared& P, const std::vector<Relation>& rels, int 
   std::vector<int64_t> vals(ex.nvars, 0);
   ex.batches.resize(P.nodes.size() + 1);
   ex.join(0, vals.data(), subs.data());
-  for (auto& T : ex.tries) {
+  for (size_t a = 0; a < ex.tries.size(); ++a) {
+    const auto& T = ex.tries[a];
     ex.res.maps_built += T->stats.maps_built;
     ex.res.keys_inserted += T->stats.keys_inserted;
     ex.res.forces += T->stats.forces;
+    if (a < 16) {
+      ex.res.atom_maps[a] = T->stats.maps_built;
+      ex.res.atom_keys[a] = T->stats.keys_inserted;
+      ex.res.atom_levels[a] = T->stats.level_mask;
+    }
   }
   ex.res.has_min = (min_var >= 0 && ex.res.minv != INT64_MAX) ? 1 : 0;
   return ex.res;
@@ -699,6 +709,8 @@ typedef struct {
   uint64_t probes, probe_misses;
   uint64_t node_body_entries[32];
   uint64_t maps_built, keys_inserted, forces;
+  uint64_t atom_maps_built[16], atom_keys_inserted[16];
+  uint32_t atom_levels_forced[16];
 } orc_result;
 
 static thread_local std::string g_err;
@@ -728,6 +740,11 @@ static void fill(orc_result* out, const orc::Result& r) {
   out->maps_built = r.maps_built;
   out->keys_inserted = r.keys_inserted;
   out->forces = r.forces;
+  for (int a = 0; a < 16; ++a) {
+    out->atom_maps_built[a] = r.atom_maps[a];
+    out->atom_keys_inserted[a] = r.atom_keys[a];
+    out->atom_levels_forced[a] = r.atom_levels[a];
+  }
 }
 
 // Execute a Free Join plan on the CPU. part/nparts: only bindings whose first
@@ -779,6 +796,11 @@ int orc_execute(const char* query_json, const char* plan_json, const int32_t* co
         total.maps_built += r.maps_built;
         total.keys_inserted += r.keys_inserted;
         total.forces += r.forces;
+        for (int a = 0; a < 16; ++a) {
+          total.atom_maps[a] += r.atom_maps[a];
+          total.atom_keys[a] += r.atom_keys[a];
+          total.atom_levels[a] |= r.atom_levels[a];
+        }
         if (cp) coll.insert(coll.end(), cs[t].begin(), cs[t].end());
       }
     }

@@ -17,7 +17,9 @@ class OrcResult(C.Structure):
     _fields_ = [("count_lo", C.c_uint64), ("count_hi", C.c_uint64), ("checksum", C.c_uint64),
                 ("min_value", C.c_int64), ("has_min", C.c_int32), ("factorized", C.c_int32),
                 ("probes", C.c_uint64), ("probe_misses", C.c_uint64), ("node_body_entries", C.c_uint64 * 32),
-                ("maps_built", C.c_uint64), ("keys_inserted", C.c_uint64), ("forces", C.c_uint64)]
+                ("maps_built", C.c_uint64), ("keys_inserted", C.c_uint64), ("forces", C.c_uint64),
+                ("atom_maps_built", C.c_uint64 * 16), ("atom_keys_inserted", C.c_uint64 * 16),
+                ("atom_levels_forced", C.c_uint32 * 16)]
 
 
 _lib = None
@@ -94,7 +96,10 @@ def execute(query, plan, atom_cols, backend="colt", batch_size=1000, dynamic_cov
            "min": res.min_value if res.has_min else None, "factorized": bool(res.factorized),
            "probes": res.probes, "probe_misses": res.probe_misses,
            "node_body_entries": list(res.node_body_entries), "maps_built": res.maps_built,
-           "keys_inserted": res.keys_inserted, "forces": res.forces}
+           "keys_inserted": res.keys_inserted, "forces": res.forces,
+           "atom_maps_built": list(res.atom_maps_built[:len(atom_cols)]),
+           "atom_keys_inserted": list(res.atom_keys_inserted[:len(atom_cols)]),
+           "atom_levels_forced": list(res.atom_levels_forced[:len(atom_cols)])}
     nv = len({v for a in json.loads(_qjson(query))["query"] for v in a["vars"]})
     if om == 1:
         arr = np.ctypeslib.as_array(C.cast(tp, C.POINTER(C.c_int64)), shape=(max(nt.value * nv, 1),))

@@ -1,0 +1,193 @@
+"""GPU parity: the sm_100a executor behind the C-ABI against the CPU oracle
+(bit-exact count, checksum, MIN; bag equality in enumerate mode)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2301_10841_b200 as fjg
+from oracle import oracle
+from paper_2301_10841_b200 import configs, plan as P
+
+from randq import bag_equal, random_query
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "configs_full.json")
+
+
+def gpu_execute(engine, q, plan, cols, shared=None, **kw):
+    """Bind one device relation per atom (or per shared group) and execute."""
+    rels, keep = [], {}
+    for i, c in enumerate(cols):
+        key = shared[i] if shared else i
+        if key not in keep:
+            keep[key] = engine.relation(c)
+        rels.append(keep[key])
+    qq = engine.query({"query": q["query"] if isinstance(q, dict) else q}, plan, rels)
+    if kw.pop("enumerate", False):
+        rows, r = qq.enumerate(**kw)
+        return r, rows
+    return qq.execute(**kw), None
+
+
+def check(engine, q, plan, cols, shared=None, enumerate=False, min_var=None, **kw):
+    ref = oracle.execute(q, plan, cols, output_mode="enumerate" if enumerate else "count",
+                         min_var=-1 if min_var is None else min_var, dynamic_cover=kw.get("dynamic_cover", True))
+    r, rows = gpu_execute(engine, q, plan, cols, shared=shared, enumerate=enumerate, min_var=min_var, **kw)
+    assert r.count == ref["count"], (r.count, ref["count"])
+    assert r.checksum == ref["checksum"], (hex(r.checksum), hex(ref["checksum"]))
+    if min_var is not None:
+        assert r.min_value == ref["min"]
+    if enumerate:
+        assert bag_equal(rows, ref["tuples"])
+    return r, ref
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_queries(engine, block):
+    """SPEC.md:434 property: random skewed instances with duplicates, all plan modes."""
+    rng = np.random.default_rng(4242 + block)
+    n = 0
+    while n < 40:
+        q, cols = random_query(rng)
+        if len(oracle.brute_force(q, cols)) > 50000:
+            continue
+        n += 1
+        for mode in ("binary", "free", "generic"):
+            plan = P.compile_plan(q, mode)
+            dyn = bool(rng.random() < 0.7)
+            batch = int(rng.choice([0, 3, 7, 1000]))
+            check(engine, q, plan, cols, enumerate=(n % 4 == 0), dynamic_cover=dyn, batch_size=batch)
+
+
+def test_self_joins_share_tries(engine):
+    """Renamed self-joins bound to one relation share physical COLT levels."""
+    rng = np.random.default_rng(77)
+    for _ in range(25):
+        nv = int(rng.integers(3, 6))
+        pool = [f"v{i}" for i in range(nv)]
+        natoms = int(rng.integers(2, 5))
+        q = {"query": [{"rel": f"E{a}", "vars": [str(x) for x in rng.choice(pool, 2, replace=False)]}
+                       for a in range(natoms)]}
+        dom = int(rng.integers(3, 12))
+        E = [rng.integers(0, dom, 40).astype(np.int32), rng.integers(0, dom, 40).astype(np.int32)]
+        cols = [E] * natoms
+        for mode in ("free", "generic"):
+            check(engine, q, P.compile_plan(q, mode), cols, shared=[0] * natoms)
+
+
+def test_edge_cases(engine):
+    tri = [{"rel": "R", "vars": ["x", "y"]}, {"rel": "S", "vars": ["y", "z"]}, {"rel": "T", "vars": ["x", "z"]}]
+    e = np.zeros(0, np.int32)
+    one = [np.array([1], np.int32), np.array([2], np.int32)]
+    dup = [np.array([1, 1, 1, 2], np.int32), np.array([2, 2, 2, 3], np.int32)]
+    ext = [np.array([-2**31, 2**31 - 1, 0, -1], np.int32), np.array([2**31 - 1, -2**31, -1, 0], np.int32)]
+    for mode in ("binary", "free", "generic"):
+        plan = P.compile_plan(tri, mode)
+        check(engine, tri, plan, [[e, e], one, one])                 # empty relation
+        check(engine, tri, plan, [one, [one[1], one[1]], one])       # single rows
+        check(engine, tri, plan, [dup, [dup[1], dup[1]], dup], enumerate=True)  # multiplicities
+        check(engine, tri, plan, [ext, ext, ext], enumerate=True)    # int32 extremes
+    # Cartesian product (empty-vars probe subatoms) and arity-2 probe keys
+    cart = [{"rel": "A", "vars": ["x"]}, {"rel": "B", "vars": ["y"]}, {"rel": "C", "vars": ["x", "y"]}]
+    cc = [[np.array([1, 2, 2], np.int32)], [np.array([5, 6], np.int32)],
+          [np.array([1, 2, 2, 3], np.int32), np.array([5, 6, 6, 5], np.int32)]]
+    for mode in ("binary", "free", "generic"):
+        check(engine, cart, P.compile_plan(cart, mode), cc, enumerate=True)
+    wide = [{"rel": "R", "vars": ["a", "b", "c"]}, {"rel": "S", "vars": ["a", "b", "c", "d"]}]
+    rng = np.random.default_rng(3)
+    wc = [[rng.integers(0, 3, 60).astype(np.int32) for _ in range(3)],
+          [rng.integers(0, 3, 60).astype(np.int32) for _ in range(4)]]
+    check(engine, wide, P.compile_plan(wide, "binary"), wc, enumerate=True)  # arity-3 probe key
+
+
+def test_batch_and_cover_invariance(engine):
+    w = configs.triangle(scale=11, m=12000, seed=9)
+    plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+    ref = oracle.execute(w.query, plan, w.atom_columns())
+    for batch in (0, 1000, 7777):
+        for dyn in (True, False):
+            r, _ = gpu_execute(engine, {"query": w.query}, plan, w.atom_columns(), shared=[0, 0, 0],
+                               batch_size=batch, dynamic_cover=dyn)
+            assert (r.count, r.checksum) == (ref["count"], ref["checksum"])
+
+
+@pytest.mark.parametrize("name", ["chain", "triangle", "star", "clique4"])
+def test_configs_small(engine, name):
+    small = {"chain": lambda: configs.chain(n=50000, domain=50000),
+             "triangle": lambda: configs.triangle(scale=14, m=200000, seed=3),
+             "star": lambda: configs.star(nf=2_000_000, dims=(40000, 60000, 16000, 2000)),
+             "clique4": lambda: configs.clique4(scale=14, m=150000)}[name]()
+    res, q, plan, _ = fjg.run_workload(engine, small)
+    mv = q.head.index(small.min_var) if small.min_var else -1
+    ref = oracle.execute(small.query, plan, small.atom_columns(), min_var=mv, nthreads=os.cpu_count() or 1)
+    assert (res.count, res.checksum) == (ref["count"], ref["checksum"])
+    if small.min_var:
+        assert res.min_value == ref["min"]
+    assert res.kernel_launches > 0
+
+
+def _golden(name):
+    if not os.path.exists(GOLDEN):
+        pytest.skip("no golden file")
+    g = json.load(open(GOLDEN))
+    if name not in g:
+        pytest.skip(f"no golden for {name}")
+    return g[name]
+
+
+@pytest.mark.parametrize("name", ["chain", "triangle", "star", "clique4"])
+def test_configs_full_vs_golden(engine, name):
+    """BASELINE.json configs at full size vs the oracle's committed results."""
+    g = _golden(name)
+    w = configs.CONFIGS[name]()
+    assert w.params == g["params"]
+    res, q, plan, _ = fjg.run_workload(engine, w)
+    assert [[(r, list(v)) for (r, v) in n] for n in plan] == [[(r, list(v)) for (r, v) in n] for n in g["plan"]]
+    assert res.count == g["count"]
+    assert f"{res.checksum:#018x}" == g["checksum"]
+    if w.min_var:
+        assert res.min_value == g["min"]
+
+
+def test_chain_full_sorted_output(engine):
+    """C1: full materialised output compared with the oracle's (sorted)."""
+    w = configs.chain()
+    q, plan, _ = fjg.prepare_workload(engine, w)
+    rows, r = q.enumerate()
+    ref = oracle.execute(w.query, plan, w.atom_columns(), output_mode="enumerate", nthreads=os.cpu_count() or 1)
+    assert r.count == len(rows) == ref["count"]
+    assert bag_equal(rows, ref["tuples"])
+
+
+def test_filter_and_partition_kernels(engine):
+    rng = np.random.default_rng(1)
+    c0 = rng.integers(-1000, 1000, 100000).astype(np.int32)
+    c1 = rng.integers(-1000, 1000, 100000).astype(np.int32)
+    rel = engine.relation([c0, c1])
+    f = rel.filter([(0, "<", 10), (1, ">=", -500)]).download()
+    keep = (c0 < 10) & (c1 >= -500)
+    assert (f[0] == c0[keep]).all() and (f[1] == c1[keep]).all()
+    g = rel.filter([(0, "=", ("col", 1))]).download()
+    assert (g[0] == c0[c0 == c1]).all()
+    part, counts = rel.partition(0, 4)
+    cols = part.download()
+    dest = np.array([oracle.partition_of(v, 4) for v in c0])
+    off = 0
+    for d in range(4):
+        assert counts[d] == int((dest == d).sum())
+        assert (cols[0][off:off + counts[d]] == c0[dest == d]).all()  # stable within a destination
+        assert (cols[1][off:off + counts[d]] == c1[dest == d]).all()
+        off += counts[d]
+
+
+def test_counters(engine):
+    """ExecStats: probes/misses/body entries agree with the oracle where forcing order is pinned (chain)."""
+    w = configs.chain(n=20000, domain=30000)
+    res, q, plan, _ = fjg.run_workload(engine, w)
+    ref = oracle.execute(w.query, plan, w.atom_columns())
+    assert res.probes == ref["probes"]
+    assert res.probe_misses == ref["probe_misses"]
+    assert res.node_body_entries == ref["node_body_entries"][:len(plan)]
+    assert res.maps_built >= 2  # S and T roots forced, R never (BaseScan)

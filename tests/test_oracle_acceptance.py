@@ -1,0 +1,133 @@
+"""SPEC acceptance criteria on the CPU oracle: the checker
+itself is pinned against a brute-force nested-loop join and the SPEC's
+counter miniatures before it is trusted for GPU parity."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2301_10841_b200 import plan as P
+
+from randq import bag_equal, random_query
+
+
+def clover(n):
+    """Fig 2 instance: x0..x3 = 0..3."""
+    R = [(0, 100)] + [(1, 1000 + i) for i in range(1, n + 1)] + [(2, 2000 + i) for i in range(1, n + 1)]
+    S = [(0, 200)] + [(2, 3000 + i) for i in range(1, n + 1)] + [(3, 4000 + i) for i in range(1, n + 1)]
+    T = [(0, 300)] + [(3, 5000 + i) for i in range(1, n + 1)] + [(1, 6000 + i) for i in range(1, n + 1)]
+    cols = lambda rows: [np.array([r[0] for r in rows], np.int32), np.array([r[1] for r in rows], np.int32)]
+    q = [{"rel": "R", "vars": ["x", "a"]}, {"rel": "S", "vars": ["x", "b"]}, {"rel": "T", "vars": ["x", "c"]}]
+    return q, [cols(R), cols(S), cols(T)]
+
+
+@pytest.mark.parametrize("seed_block", range(4))
+def test_acceptance1_oracle_equivalence(seed_block):
+    """#1: random (query, instance) x {mode, backend, batch in {1,3,1000}, dynamic} == brute force."""
+    rng = np.random.default_rng(1000 + seed_block)
+    done = 0
+    while done < 50:
+        q, cols = random_query(rng)
+        truth = oracle.brute_force(q, cols)
+        if len(truth) > 20000:
+            continue
+        done += 1
+        for mode in ("binary", "free", "generic"):
+            plan = P.compile_plan(q, mode)
+            for backend in ("simple", "slt", "colt"):
+                for batch in (1, 3, 1000):
+                    for dyn in (False, True):
+                        r = oracle.execute(q, plan, cols, backend=backend, batch_size=batch, dynamic_cover=dyn,
+                                           output_mode="enumerate")
+                        assert r["count"] == len(truth)
+                        assert bag_equal(r["tuples"], truth), (q, mode, backend, batch, dyn)
+
+
+@pytest.mark.parametrize("n", [10, 100, 1000])
+def test_acceptance2_clover_asymptotics(n):
+    q, cols = clover(n)
+    unf = oracle.execute(q, P.compile_plan(q, "binary"), cols, dynamic_cover=False)
+    fac = oracle.execute(q, P.compile_plan(q, "free"), cols, dynamic_cover=False)
+    assert unf["count"] == fac["count"] == 1
+    assert unf["node_body_entries"][1] >= n * n
+    assert fac["node_body_entries"][1] == 1
+    assert fac["probes"] <= 10 * n
+
+
+def test_acceptance4_colt_laziness():
+    q, cols = clover(20)
+    r = oracle.execute(q, P.compile_plan(q, "free"), cols, backend="colt")
+    assert r["atom_maps_built"][0] == 0            # R: BaseScan only
+    for a in (1, 2):                               # S, T: at most one map level
+        assert bin(r["atom_levels_forced"][a]).count("1") <= 1
+    # Example 4.4: extended clover with U(b); S(b) as cover builds no level-1 map for S
+    q2 = q + [{"rel": "U", "vars": ["b"]}]
+    U = [np.array([200, 3001, 3002], np.int32)]
+    plan = [[("R", ["x", "a"]), ("S", ["x"]), ("T", ["x"])], [("S", ["b"]), ("U", ["b"])], [("T", ["c"])]]
+    r = oracle.execute(q2, plan, cols + [U], backend="colt", dynamic_cover=False)
+    assert r["count"] == 1
+    assert not (r["atom_levels_forced"][1] >> 1) & 1
+
+
+def test_acceptance5_backend_ladder():
+    rng = np.random.default_rng(5)
+    n = 100_000
+    zipf = lambda: np.minimum(rng.zipf(1.3, n) - 1, 5000).astype(np.int32)
+    uni = lambda: rng.integers(0, 100_000_000, n).astype(np.int32)
+    # skewed triangle with a selective y join: COLT forces T's level-1 maps
+    # only under the few x that survive, simple/SLT build them all
+    q = [{"rel": "R", "vars": ["x", "y"]}, {"rel": "S", "vars": ["y", "z"]}, {"rel": "T", "vars": ["x", "z"]}]
+    cols = [[zipf(), uni()], [uni(), zipf()], [zipf(), zipf()]]
+    plan = P.compile_plan(q, "generic")
+    k = {b: oracle.execute(q, plan, cols, backend=b)["keys_inserted"] for b in ("colt", "slt", "simple")}
+    assert k["colt"] <= k["slt"] <= k["simple"]
+    assert k["colt"] < k["simple"]
+
+
+def test_acceptance6_batch_invariance():
+    rng = np.random.default_rng(6)
+    for _ in range(30):
+        q, cols = random_query(rng)
+        plan = P.compile_plan(q, "free")
+        rs = [oracle.execute(q, plan, cols, batch_size=b, output_mode="enumerate") for b in (1, 2, 7, 1000)]
+        for r in rs[1:]:
+            assert bag_equal(r["tuples"], rs[0]["tuples"])
+            assert r["probes"] == rs[0]["probes"]
+
+
+def test_acceptance8_factorized_count():
+    q, cols = clover(50)
+    gj = P.compile_plan(q, "generic")  # Eq. 3: Cartesian suffix [R(a)],[S(b)],[T(c)]
+    e = oracle.execute(q, gj, cols, output_mode="count")
+    f = oracle.execute(q, gj, cols, output_mode="factorized_count")
+    assert f["factorized"] and f["count"] == e["count"] == 1
+    rng = np.random.default_rng(8)
+    hit = 0
+    for _ in range(60):
+        qq, cc = random_query(rng)
+        for mode in ("free", "generic"):
+            plan = P.compile_plan(qq, mode)
+            a = oracle.execute(qq, plan, cc)
+            b = oracle.execute(qq, plan, cc, output_mode="factorized_count")
+            assert a["count"] == b["count"]
+            hit += b["factorized"]
+    assert hit > 0
+
+
+def test_checksum_is_sum_of_fmix_tuple_hash():
+    rng = np.random.default_rng(9)
+    q, cols = random_query(rng)
+    plan = P.compile_plan(q, "free")
+    r = oracle.execute(q, plan, cols, output_mode="enumerate")
+    assert r["checksum"] == oracle.checksum_of(r["tuples"])
+
+
+def test_partitioned_execution_sums_to_whole():
+    rng = np.random.default_rng(10)
+    for _ in range(10):
+        q, cols = random_query(rng)
+        plan = P.compile_plan(q, "generic")
+        whole = oracle.execute(q, plan, cols)
+        parts = [oracle.execute(q, plan, cols, part=p, nparts=3) for p in range(3)]
+        assert sum(p["count"] for p in parts) == whole["count"]
+        assert sum(p["checksum"] for p in parts) % 2 ** 64 == whole["checksum"]
+        assert oracle.execute(q, plan, cols, nthreads=3)["count"] == whole["count"]
