@@ -520,7 +520,7 @@ __device__ __forceinline__ void put2(uint32_t (&a)[W], uint32_t (&b)[W], int v, 
 template <int MODE, int W>
 __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64_t j, int32_t (&val)[W],
                                               uint32_t (&cp)[W], uint32_t (&cl)[W], uint64_t& mult,
-                                              uint64_t& probes, uint64_t& misses) {
+                                              uint64_t& probes, uint64_t& misses, uint64_t& body) {
 #pragma unroll
   for (int v = 0; v < W; ++v)
     if ((N.in_vars >> v) & 1u) val[v] = __ldg(N.in_var[v] + e);
@@ -562,6 +562,7 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
         }
       }
   }
+  ++body;  // the node body runs for this cover tuple (ExecStats.node_body_entries)
   // ---- probe every other subatom in node order (Fig 13 inner loop) ----
   for (int s = 0; s < N.nsub; ++s) {
     if (s == ci) continue;
@@ -616,8 +617,7 @@ __global__ void __launch_bounds__(TILE) k_expand(const __grid_constant__ KNode N
     if (alive) {
       const uint64_t e = upper_bound_u64(scan, lo, hi, i);
       const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
-      alive = run_candidate<MODE, W>(N, e, j, val, cp, cl, mult, probes, misses);
-      if (alive) ++body;
+      alive = run_candidate<MODE, W>(N, e, j, val, cp, cl, mult, probes, misses, body);
     }
     if (MODE == EXPAND_WRITE) {
       const unsigned bal = __ballot_sync(0xffffffffu, alive);

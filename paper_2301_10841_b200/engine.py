@@ -8,6 +8,7 @@ returns the OutputSink counters plus ExecStats/TrieStats.
 """
 import ctypes as C
 import json
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -53,9 +54,12 @@ class Engine:
         check(lib.fjg_engine_create(int(device), C.byref(h)))
         self._h = h
         self.device = device
+        self._children = weakref.WeakSet()  # relations / queries: closed before the engine
 
     def close(self):
         if self._h:
+            for c in list(self._children):
+                c.close()
             lib.fjg_engine_destroy(self._h)
             self._h = None
 
@@ -125,6 +129,7 @@ class Relation:
         self.engine = engine
         self._h = handle
         self._keep = keepalive
+        engine._children.add(self)
 
     @property
     def rows(self):
@@ -167,9 +172,9 @@ class Relation:
         return Relation(self.engine, h), [int(x) for x in counts]
 
     def close(self):
-        if self._h:
+        if self._h and self.engine._h:
             lib.fjg_relation_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -199,6 +204,7 @@ class Query:
         check(lib.fjg_query_create(engine._h, self.query_json.encode(), self.plan_json.encode(), arr,
                                    len(self.relations), C.byref(h)))
         self._h = h
+        engine._children.add(self)
         self.head = []
         for a in self.atoms:
             for v in a["vars"]:
@@ -225,9 +231,10 @@ class Query:
                           last_node_candidates=r.last_node_candidates,
                           kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
 
-    def enumerate(self, batch_size=0, dynamic_cover=True):
+    def enumerate(self, batch_size=0, dynamic_cover=True, min_var=None):
         """Enumerate mode: (tuples as an (n, |head|) int32 array in head-variable order, ExecResult)."""
-        r = self.execute(batch_size=batch_size, dynamic_cover=dynamic_cover, output_mode="enumerate")
+        r = self.execute(batch_size=batch_size, dynamic_cover=dynamic_cover, output_mode="enumerate",
+                         min_var=min_var)
         nv = len(self.head)
         buf = np.empty((max(r.output_rows, 1), nv), dtype=np.int32)
         rows = C.c_uint64(0)
@@ -235,9 +242,9 @@ class Query:
         return buf[: rows.value], r
 
     def close(self):
-        if self._h:
+        if self._h and self.engine._h:
             lib.fjg_query_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
