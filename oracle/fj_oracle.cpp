@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <map>
 #include <memory>
@@ -239,9 +240,10 @@ struct TrieStats {
 // NodeBody: Map | Vec (row offsets) | BaseScan.
 struct Node {
   enum Kind : uint8_t { BaseScan, Vec, Map } kind = Vec;
-  int level = 0;                    // schema level this node keys on
-  std::vector<uint32_t> offs;       // Vec
-  FlatMap map;                      // Map
+  int32_t level = 0;                // schema level this node keys on
+  uint32_t n = 0;                   // Vec: number of offsets
+  const uint32_t* offs = nullptr;   // Vec: offsets (slice of the trie's offset arena)
+  std::unique_ptr<FlatMap> map;     // Map
   uint64_t rows = 0;                // offsets under this node
 };
 
@@ -251,15 +253,16 @@ struct Colt {
   bool trailing_empty = false;
   Backend backend = COLT;
   Node root;
-  std::vector<std::unique_ptr<Node>> arena;
+  std::deque<Node> nodes;                              // stable child nodes
+  std::vector<std::unique_ptr<uint32_t[]>> offs_arena;  // child offset vectors, one block per force
   TrieStats stats;
 
   uint64_t length(const Node& nd) const {
-    return nd.kind == Node::BaseScan ? rel->n : nd.kind == Node::Vec ? nd.offs.size() : nd.rows;
+    return nd.kind == Node::BaseScan ? rel->n : nd.kind == Node::Vec ? nd.n : nd.rows;
   }
   // estimated_key_count: never forces.
   uint64_t estimated_key_count(const Node& nd) const {
-    if (nd.kind == Node::Map) return nd.map.size();
+    if (nd.kind == Node::Map) return nd.map->size();
     return length(nd);
   }
   Key key_at(int level, uint64_t row) const {
@@ -271,37 +274,50 @@ struct Colt {
   // force (Fig 12 `force`): group offsets by key; idempotent.
   void force(Node& nd) {
     if (nd.kind == Node::Map) return;
-    FlatMap m;
-    m.reserve(std::min<uint64_t>(length(nd), 1u << 16));
-    auto visit = [&](uint64_t i) {
-      Key k = key_at(nd.level, i);
+    const uint64_t len = length(nd);
+    auto off_at = [&](uint64_t i) -> uint32_t { return nd.kind == Node::BaseScan ? (uint32_t)i : nd.offs[i]; };
+    auto m = std::make_unique<FlatMap>();
+    m->reserve(std::min<uint64_t>(len, 1u << 16));
+    // pass 1: key -> child index, child sizes
+    std::vector<uint32_t> which(len);
+    std::vector<uint32_t> counts;
+    for (uint64_t i = 0; i < len; ++i) {
       bool ins;
-      Node*& slot = m.get_or_insert(k, ins);
+      Node*& slot = m->get_or_insert(key_at(nd.level, off_at(i)), ins);
       if (ins) {
-        arena.emplace_back(new Node());
-        slot = arena.back().get();
-        slot->kind = Node::Vec;
-        slot->level = nd.level + 1;
+        slot = reinterpret_cast<Node*>((uintptr_t)counts.size());
+        counts.push_back(0);
       }
-      slot->offs.push_back((uint32_t)i);
-    };
-    uint64_t rows = 0;
-    if (nd.kind == Node::BaseScan) {
-      for (uint64_t i = 0; i < rel->n; ++i) visit(i);
-      rows = rel->n;
-    } else {
-      for (uint32_t i : nd.offs) visit(i);
-      rows = nd.offs.size();
-      std::vector<uint32_t>().swap(nd.offs);
+      const uint32_t c = (uint32_t)(uintptr_t)slot;
+      which[i] = c;
+      ++counts[c];
     }
+    // pass 2: group offsets by child into one arena block
+    std::unique_ptr<uint32_t[]> block(new uint32_t[std::max<uint64_t>(len, 1)]);
+    std::vector<uint64_t> start(counts.size() + 1, 0);
+    for (size_t c = 0; c < counts.size(); ++c) start[c + 1] = start[c] + counts[c];
+    std::vector<uint64_t> cur(start.begin(), start.end() - 1);
+    for (uint64_t i = 0; i < len; ++i) block[cur[which[i]]++] = off_at(i);
+    for (size_t c = 0; c < counts.size(); ++c) {
+      nodes.emplace_back();
+      Node& ch = nodes.back();
+      ch.kind = Node::Vec;
+      ch.level = nd.level + 1;
+      ch.offs = block.get() + start[c];
+      ch.n = counts[c];
+      ch.rows = counts[c];
+      m->vals[c] = &ch;
+    }
+    offs_arena.push_back(std::move(block));
     nd.kind = Node::Map;
-    nd.map.swap(m);
-    nd.rows = rows;
-    for (Node* c : nd.map.vals) c->rows = c->offs.size();
+    nd.map = std::move(m);
+    nd.rows = len;
+    nd.offs = nullptr;
+    nd.n = 0;
     stats.maps_built += 1;
     stats.forces += 1;
     stats.level_mask |= 1u << nd.level;
-    stats.keys_inserted += nd.map.size();
+    stats.keys_inserted += nd.map->size();
   }
   // eager materialisation for simple (all map levels) / slt (level 0)
   void build(Backend b) {
@@ -313,7 +329,7 @@ struct Colt {
       std::function<void(Node&)> rec = [&](Node& nd) {
         if (nd.level >= map_levels) return;
         force(nd);
-        for (Node* c : nd.map.vals) rec(*c);
+        for (Node* c : nd.map->vals) rec(*c);
       };
       rec(root);
     } else if (b == SLT) {
@@ -410,7 +426,7 @@ struct Exec {
     }
     Colt& T = *tries[atom];
     T.force(*sub.node);
-    Node* c = sub.node->map.find(key);
+    Node* c = sub.node->map->find(key);
     if (!c) {
       ++res.misses;
       return false;
@@ -529,14 +545,15 @@ struct Exec {
           offer(t, r);
         }
       } else {
-        for (uint32_t i : csub.node->offs) {
+        for (uint32_t x = 0; x < csub.node->n; ++x) {
+          const uint32_t i = csub.node->offs[x];
           for (int q = 0; q < nc; ++q) t[q] = CT.rel->at(C.cols[q], i);
           offer(t, r);
         }
       }
     } else {
       CT.force(*csub.node);
-      const FlatMap& mp = csub.node->map;
+      const FlatMap& mp = *csub.node->map;
       for (size_t e = 0; e < mp.size(); ++e) {
         Sub r;
         r.node = mp.vals[e];

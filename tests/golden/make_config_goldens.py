@@ -28,11 +28,12 @@ def main(names):
         head = P.head_variables(w.query)
         mv = head.index(w.min_var) if w.min_var else -1
         t0 = time.time()
-        r = oracle.execute(w.query, plan, w.atom_columns(), min_var=mv, nthreads=os.cpu_count() or 1)
+        nt = int(os.environ.get("GOLDEN_THREADS", os.cpu_count() or 1))
+        r = oracle.execute(w.query, plan, w.atom_columns(), min_var=mv, nthreads=nt)
         dt = time.time() - t0
         res[name] = {"params": w.params, "plan": plan, "count": r["count"], "checksum": f"{r['checksum']:#018x}",
                      "min": r["min"], "probes": r["probes"], "input_tuples": w.input_tuples(),
-                     "oracle_seconds": round(dt, 1), "oracle_threads": os.cpu_count()}
+                     "oracle_seconds": round(dt, 1), "oracle_threads": nt}
         print(name, res[name]["count"], res[name]["checksum"], f"{dt:.1f}s", flush=True)
         with open(OUT, "w") as f:
             json.dump(res, f, indent=1, sort_keys=True)
