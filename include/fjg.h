@@ -158,6 +158,10 @@ void fjg_relation_destroy(fjg_relation* rel);
  * destination), counts[d] the rows for destination d. */
 int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_relation** out_rel,
                            uint64_t* counts);
+/* Same, into caller-provided device columns (nrows int32 each), e.g. the send
+ * buffers of an NCCL all-to-all. */
+int fjg_relation_partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_dev_cols,
+                                uint64_t* counts);
 
 /* ---- queries: build phase + join phase ----
  * query_json: {"query":[{"rel":..,"vars":[..]},..]}; plan_json: a Free Join

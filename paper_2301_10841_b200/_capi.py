@@ -88,6 +88,7 @@ def _load():
         "fjg_relation_download": (I, [P, I, P]),
         "fjg_relation_destroy": (None, [P]),
         "fjg_relation_partition": (I, [P, I, I, C.POINTER(P), C.POINTER(U64)]),
+        "fjg_relation_partition_into": (I, [P, I, I, C.POINTER(P), C.POINTER(U64)]),
         "fjg_query_create": (I, [P, C.c_char_p, C.c_char_p, C.POINTER(P), I, C.POINTER(P)]),
         "fjg_execute": (I, [P, C.POINTER(ExecOptions), C.POINTER(Result)]),
         "fjg_query_output": (I, [P, P, U64, C.POINTER(U64)]),
@@ -109,7 +110,8 @@ lib = _load()
 EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_op", "fjg_engine_create",
             "fjg_engine_destroy", "fjg_engine_sync", "fjg_engine_stream", "fjg_relation_create", "fjg_relation_from_device",
             "fjg_relation_filter", "fjg_relation_rows", "fjg_relation_cols", "fjg_relation_device_col",
-            "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition", "fjg_query_create",
+            "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition",
+            "fjg_relation_partition_into", "fjg_query_create",
             "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_destroy",
             "fjg_device_tuple_hash", "fjg_host_tuple_hash"]
 

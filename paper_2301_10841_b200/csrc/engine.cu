@@ -1590,43 +1590,63 @@ int fjg_relation_filter(const fjg_relation* in, const fjg_predicate* preds, int 
   });
 }
 
+// Stable hash-partition of `in` on column `col`: rows for destination d land in
+// out_cols[c][base_d ...) in their original order (flags -> scan -> compact per
+// destination).
+static void partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_cols, uint64_t* counts) {
+  fjg_engine* eng = in->eng;
+  if (col < 0 || col >= in->ncols) throw fj::ValidationError("partition column out of range");
+  if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
+  const uint64_t n = in->nrows;
+  uint32_t* flags = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
+  uint32_t* excl = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, excl, (int64_t)std::max<uint64_t>(n, 1)));
+  void* tmp = eng->pool->alloc(bytes);
+  uint64_t base = 0;
+  for (int d = 0; d < nparts; ++d) {
+    uint32_t total = 0;
+    if (n) {
+      LAUNCH(eng, k_partition_flags<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[col], n, nparts, d, flags));
+      size_t b = bytes;
+      CK(cub::DeviceScan::ExclusiveSum(tmp, b, flags, excl, (int64_t)n, eng->stream));
+      uint32_t last[2];
+      CK(cudaMemcpyAsync(&last[0], excl + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaMemcpyAsync(&last[1], flags + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      total = last[0] + last[1];
+      for (int c = 0; c < in->ncols; ++c)
+        LAUNCH(eng, k_compact_col<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[c], flags, excl, n,
+                                                                      out_cols[c] + base));
+    }
+    counts[d] = total;
+    base += total;
+  }
+  CK(cudaStreamSynchronize(eng->stream));
+  eng->pool->free(flags);
+  eng->pool->free(excl);
+  eng->pool->free(tmp);
+}
+
 int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_relation** out_rel, uint64_t* counts) {
   return guard([&] {
-    fjg_engine* eng = in->eng;
-    ScopedDevice sd(eng->device);
-    if (col < 0 || col >= in->ncols) throw fj::ValidationError("partition column out of range");
-    if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
-    const uint64_t n = in->nrows;
-    fjg_relation* r = new_relation(eng, in->ncols, n);
-    uint32_t* flags = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
-    uint32_t* excl = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
-    size_t bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, excl, (int64_t)std::max<uint64_t>(n, 1)));
-    void* tmp = eng->pool->alloc(bytes);
-    uint64_t base = 0;
-    for (int d = 0; d < nparts; ++d) {
-      uint32_t total = 0;
-      if (n) {
-        LAUNCH(eng, k_partition_flags<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[col], n, nparts, d, flags));
-        size_t b = bytes;
-        CK(cub::DeviceScan::ExclusiveSum(tmp, b, flags, excl, (int64_t)n, eng->stream));
-        uint32_t last[2];
-        CK(cudaMemcpyAsync(&last[0], excl + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
-        CK(cudaMemcpyAsync(&last[1], flags + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
-        CK(cudaStreamSynchronize(eng->stream));
-        total = last[0] + last[1];
-        for (int c = 0; c < in->ncols; ++c)
-          LAUNCH(eng, k_compact_col<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[c], flags, excl, n,
-                                                                        r->cols[c] + base));
-      }
-      counts[d] = total;
-      base += total;
+    ScopedDevice sd(in->eng->device);
+    fjg_relation* r = new_relation(in->eng, in->ncols, in->nrows);
+    try {
+      partition_into(in, col, nparts, r->cols.data(), counts);
+    } catch (...) {
+      fjg_relation_destroy(r);
+      throw;
     }
-    CK(cudaStreamSynchronize(eng->stream));
-    eng->pool->free(flags);
-    eng->pool->free(excl);
-    eng->pool->free(tmp);
     *out_rel = r;
+  });
+}
+
+int fjg_relation_partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_dev_cols,
+                                uint64_t* counts) {
+  return guard([&] {
+    ScopedDevice sd(in->eng->device);
+    partition_into(in, col, nparts, out_dev_cols, counts);
   });
 }
 

@@ -1,1 +1,160 @@
-"""Multi-GPU sharding (north_star (c)): placeholder, implemented in the next step."""
+"""Multi-GPU Free Join: hash-partitioning on the first plan variable
+(BASELINE.json north_star (c)).
+
+One process per GPU (torch.distributed, NCCL over NVLink). Every rank starts
+with a contiguous 1/G slice of each base relation (the distributed-load model).
+Per step:
+  1. views whose atom holds the plan's first variable v are hash-partitioned
+     on v's column (fjg_relation_partition_into, fj::partition_of = fmix64 mod
+     G) and exchanged with an all-to-all (uneven splits, counts exchanged
+     first);
+  2. every other view is all-gathered (padded to the largest slice, then
+     compacted);
+  3. each rank runs the single-GPU executor on (its shard of v) x (replicas);
+     outputs are disjoint by v, so count = sum, checksum = sum mod 2^64,
+     MIN = min, reduced with one all-reduce.
+The exchange primitives take an `ops` object (array allocation + the
+partition function) so the same exchange logic runs on CPU tensors under gloo
+in tests/test_dist.py; the product path uses `DeviceOps` (the CUDA partition
+kernel, NCCL).
+"""
+import torch
+import torch.distributed as dist
+
+MASK32 = (1 << 32) - 1
+
+
+def first_variable(plan):
+    node0 = plan[0]
+    for (_, vs) in node0:
+        if vs:
+            return vs[0]
+    raise ValueError("plan binds no variable in its first node")
+
+
+def atom_views(query, atom_rel, plan):
+    """Per atom: (base relation, column of the first variable or None)."""
+    fv = first_variable(plan)
+    views = []
+    for atom, base in zip(query, atom_rel):
+        views.append((base, atom["vars"].index(fv) if fv in atom["vars"] else None))
+    return fv, views
+
+
+def local_slice(n, world, rank):
+    lo = n * rank // world
+    hi = n * (rank + 1) // world
+    return lo, hi
+
+
+def all_to_all_partitioned(cols, col, world, ops, group=None):
+    """Send each row to rank partition_of(row[col]); returns this rank's rows."""
+    grouped, counts = ops.partition(cols, col, world)
+    send = torch.tensor(counts, dtype=torch.int64, device=ops.device)
+    recv = torch.empty(world, dtype=torch.int64, device=ops.device)
+    dist.all_to_all_single(recv, send, group=group)
+    rc = [int(x) for x in recv.tolist()]
+    out = []
+    for g in grouped:
+        o = ops.empty(sum(rc))
+        dist.all_to_all_single(o, g, output_split_sizes=rc, input_split_sizes=counts, group=group)
+        out.append(o)
+    return out
+
+
+def all_gather_rows(cols, world, ops, group=None):
+    n = cols[0].numel() if cols else 0
+    sizes = [torch.zeros(1, dtype=torch.int64, device=ops.device) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=ops.device), group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes) if sizes else 0
+    out = []
+    for c in cols:
+        pad = ops.empty(m)
+        if n:
+            pad[:n].copy_(c)
+        buf = ops.empty(m * world)
+        dist.all_gather_into_tensor(buf, pad, group=group)
+        out.append(torch.cat([buf[r * m: r * m + sizes[r]] for r in range(world)]) if world > 1 else buf[:n])
+    return out
+
+
+def reduce_results(count, checksum, minv, device, group=None):
+    """count (python int, < 2^127), checksum (u64), minv (int or None) -> global."""
+    INT64_MAX = (1 << 63) - 1
+    parts = [count & MASK32, (count >> 32) & MASK32, (count >> 64) & MASK32, count >> 96,
+             checksum & MASK32, checksum >> 32]
+    t = torch.tensor(parts, dtype=torch.int64, device=device)
+    dist.all_reduce(t, group=group)
+    v = [int(x) for x in t.tolist()]
+    total = v[0] + (v[1] << 32) + (v[2] << 64) + (v[3] << 96)
+    cs = (v[4] + (v[5] << 32)) & ((1 << 64) - 1)
+    m = torch.tensor([INT64_MAX if minv is None else int(minv)], dtype=torch.int64, device=device)
+    dist.all_reduce(m, op=dist.ReduceOp.MIN, group=group)
+    mv = int(m.item())
+    return total, cs, (None if mv == INT64_MAX else mv)
+
+
+def exchange(relations, views, world, rank, ops, group=None):
+    """relations: base -> list of local-slice column tensors. Returns
+    view -> list of column tensors held by this rank after the exchange."""
+    out = {}
+    for view in sorted(set(views), key=lambda v: (v[0], -1 if v[1] is None else v[1])):
+        base, col = view
+        cols = relations[base]
+        out[view] = all_gather_rows(cols, world, ops, group) if col is None else \
+            all_to_all_partitioned(cols, col, world, ops, group)
+    return out
+
+
+class DeviceOps:
+    """Product ops: CUDA tensors, the libfjg partition kernel."""
+
+    def __init__(self, engine):
+        self.engine = engine
+        self.device = torch.device("cuda", engine.device)
+
+    def empty(self, n):
+        return torch.empty(n, dtype=torch.int32, device=self.device)
+
+    def partition(self, cols, col, world):
+        rel = self.engine.relation_from_torch(cols)
+        grouped = [self.empty(cols[0].numel()) for _ in cols]
+        counts = rel.partition_into(col, world, [g.data_ptr() for g in grouped])
+        rel.close()
+        return grouped, counts
+
+
+class ShardedQuery:
+    """A workload executed across `world` ranks (one GPU each)."""
+
+    def __init__(self, engine, w, plan, world, rank, group=None):
+        from . import plan as P
+        self.engine, self.w, self.plan = engine, w, plan
+        self.world, self.rank, self.group = world, rank, group
+        self.ops = DeviceOps(engine)
+        self.fv, self.views = atom_views(w.query, w.atom_rel, plan)
+        self.head = P.head_variables(w.query)
+        # this rank's slice of every (filtered) base relation, resident on the device
+        self.local = {}
+        for base, cols in w.filtered().items():
+            lo, hi = local_slice(len(cols[0]), world, rank)
+            self.local[base] = [torch.from_numpy(c[lo:hi].copy()).to(self.ops.device) for c in cols]
+        self.input_tuples_local = sum(len(w.relations[b][0]) for b in w.atom_rel) / world
+        self._q = None
+
+    def _bind(self, held):
+        rels = {v: self.engine.relation_from_torch(cols) for v, cols in held.items()}
+        self._held = held
+        self._rels = rels
+        self._q = self.engine.query({"query": self.w.query}, self.plan, [rels[v] for v in self.views])
+
+    def execute(self, min_var=None, timing=False, **kw):
+        held = exchange(self.local, self.views, self.world, self.rank, self.ops, self.group)
+        torch.cuda.current_stream(self.ops.device).synchronize()
+        self._bind(held)  # zero-copy relations over the exchanged buffers
+        r = self._q.execute(min_var=min_var, timing=timing, **kw)
+        r.extra["local_count"] = r.count
+        r.count, r.checksum, r.min_value = reduce_results(r.count, r.checksum, r.min_value, self.ops.device,
+                                                          self.group)
+        return r

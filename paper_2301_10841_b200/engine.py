@@ -171,6 +171,13 @@ class Relation:
         check(lib.fjg_relation_partition(self._h, col, nparts, C.byref(h), counts))
         return Relation(self.engine, h), [int(x) for x in counts]
 
+    def partition_into(self, col, nparts, out_ptrs):
+        """Hash-partition into caller-provided device columns; returns per-destination counts."""
+        counts = (C.c_uint64 * nparts)()
+        arr = (C.c_void_p * len(out_ptrs))(*out_ptrs)
+        check(lib.fjg_relation_partition_into(self._h, col, nparts, arr, counts))
+        return [int(x) for x in counts]
+
     def close(self):
         if self._h and self.engine._h:
             lib.fjg_relation_destroy(self._h)
