@@ -349,7 +349,11 @@ def run_ours(args):
             "result": {"count": res.count, "checksum": f"{res.checksum:#018x}"},
             "phases_ms": {"build": statistics.mean(r.build_ms for r in results),
                           "join": statistics.mean(r.join_ms for r in results),
-                          "last_node": last_ms},
+                          "last_node_total": statistics.mean(r.last_node_ms for r in results),
+                          "last_node_per_launch": last_ms, "last_node_launches": r0.last_node_launches},
+            "counters": {"probes": r0.probes, "node_probes": r0.node_probes, "node_inputs": r0.node_inputs,
+                         "last_node_candidates": r0.last_node_candidates, "maps_built": r0.maps_built,
+                         "keys_inserted": r0.keys_inserted, "host_syncs": r0.host_syncs},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": "k_expand<EXPAND_COUNT> (fused last node)",

@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfjg.so")
+LIB_PATH = os.environ.get("FJG_LIB") or os.path.join(_HERE, "libfjg.so")
 
 FJG_OK, FJG_E_IO, FJG_E_PARSE, FJG_E_VALIDATION, FJG_E_RESOURCE, FJG_E_ENGINE = range(6)
 MAX_NODES = 32

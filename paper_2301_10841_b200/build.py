@@ -47,10 +47,10 @@ def build_product(force=False):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
               "-diag-suppress", "128",
               *_srcs("engine.cu", "capi.cpp", "fj_plan.cpp"), "-o", LIBFJG])
-    gdeps = _srcs("datagen.cpp")
+    gdeps = _srcs("datagen.cpp", "datagen_dev.cu", "rmat.hpp")
     if force or _stale(LIBFJGEN, gdeps):
-        _run(["g++", "-std=c++17", "-O3", "-march=x86-64-v2", "-fPIC", "-shared", "-pthread",
-              *gdeps, "-o", LIBFJGEN])
+        _run([NVCC, "-std=c++17", "-O3", *ARCH, "-Xcompiler", "-fPIC,-pthread,-march=x86-64-v2", "-shared",
+              *_srcs("datagen.cpp", "datagen_dev.cu"), "-o", LIBFJGEN])
 
 
 def build_oracle(force=False):

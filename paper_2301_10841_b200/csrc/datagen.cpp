@@ -14,19 +14,14 @@
 #include <thread>
 #include <vector>
 
+#include "rmat.hpp"
+
 namespace {
 
-inline uint64_t splitmix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-  return x ^ (x >> 31);
-}
-// counter-based stream: value i of stream (seed, stream)
-inline uint64_t rng(uint64_t seed, uint64_t stream, uint64_t i) {
-  return splitmix64(splitmix64(seed * 0x100000001b3ULL + stream) ^ (i * 0xd1b54a32d192ed03ULL));
-}
-inline double u01(uint64_t x) { return (double)(x >> 11) * (1.0 / 9007199254740992.0); }
+using fjgen::rmat_edge;
+using fjgen::rng;
+using fjgen::splitmix64;
+using fjgen::u01;
 
 template <class F>
 void parallel_for(uint64_t n, F&& f) {
@@ -39,26 +34,6 @@ void parallel_for(uint64_t n, F&& f) {
       for (uint64_t i = lo; i < hi; ++i) f(i);
     });
   for (auto& x : th) x.join();
-}
-
-// R-MAT edge i: `scale` quadrant draws with probabilities (a, b, c, 1-a-b-c).
-inline uint64_t rmat_edge(uint64_t seed, uint64_t i, int scale, double a, double b, double c) {
-  uint64_t s = 0, d = 0;
-  for (int l = 0; l < scale; ++l) {
-    const double r = u01(rng(seed, 1000 + l, i));
-    uint64_t sb = 0, db = 0;
-    if (r < a) {
-    } else if (r < a + b) {
-      db = 1;
-    } else if (r < a + b + c) {
-      sb = 1;
-    } else {
-      sb = db = 1;
-    }
-    s = (s << 1) | sb;
-    d = (d << 1) | db;
-  }
-  return (s << 32) | d;
 }
 
 std::string g_err;

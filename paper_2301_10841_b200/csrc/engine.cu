@@ -588,8 +588,11 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
   return true;
 }
 
+#ifndef FJG_EXPAND_MINBLOCKS
+#define FJG_EXPAND_MINBLOCKS 1
+#endif
 template <int MODE, int W>
-__global__ void __launch_bounds__(TILE) k_expand(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+__global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
                                                  uint64_t F, const uint64_t* __restrict__ bounds, int min_var,
                                                  int32_t* __restrict__ out_tuples, uint64_t out_cap,
                                                  DevCounters* ctr) {
@@ -830,11 +833,6 @@ inline unsigned grid_for(uint64_t n, int threads = 256, unsigned cap = 148u * 16
   return (unsigned)g;
 }
 
-uint64_t pow2_at_least(uint64_t x) {
-  uint64_t p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
 
 }  // namespace
 

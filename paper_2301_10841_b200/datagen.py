@@ -32,6 +32,9 @@ def lib():
         L.fjgen_orient.argtypes = [U64, P, P, U64, P, P]
         L.fjgen_orient.restype = C.c_int64
         L.fjgen_last_error.restype = C.c_char_p
+        L.fjgen_rmat_device.argtypes = [C.c_int, U64, C.c_int, U64, C.c_double, C.c_double, C.c_double, P, P]
+        L.fjgen_rmat_device.restype = C.c_int
+        L.fjgen_device_last_error.restype = C.c_char_p
         _lib = L
     return _lib
 
@@ -73,9 +76,32 @@ def zipf(seed, stream, n, k, s):
     return _cached(("zipf", seed, stream, n, k, s), gen, 1)[0]
 
 
+def rmat_device(seed, scale, m, a=0.57, b=0.19, c=0.19, device=0):
+    """Same edges as rmat(), generated on the GPU into int32 CUDA tensors."""
+    import torch
+    src = torch.empty(max(m, 1), dtype=torch.int32, device=f"cuda:{device}")
+    dst = torch.empty(max(m, 1), dtype=torch.int32, device=f"cuda:{device}")
+    torch.cuda.synchronize(device)
+    if lib().fjgen_rmat_device(device, seed, scale, m, a, b, c, src.data_ptr(), dst.data_ptr()) != 0:
+        raise RuntimeError(lib().fjgen_device_last_error().decode())
+    return src[:m], dst[:m]
+
+
+def _gpu_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
 def rmat(seed, scale, m, a=0.57, b=0.19, c=0.19):
-    """R-MAT edges: exactly m distinct directed non-loop edges, random row order."""
+    """R-MAT edges: exactly m distinct directed non-loop edges, random row order.
+    Large graphs are generated on the GPU when one is present (bit-identical)."""
     def gen():
+        if m >= (1 << 26) and _gpu_available():
+            s, d = rmat_device(seed, scale, m, a, b, c)
+            return [s.cpu().numpy(), d.cpu().numpy()]
         s = np.empty(max(m, 1), dtype=np.int32)
         d = np.empty(max(m, 1), dtype=np.int32)
         if lib().fjgen_rmat(seed, scale, m, a, b, c, s.ctypes.data, d.ctypes.data) != 0:

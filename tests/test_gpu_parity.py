@@ -191,3 +191,12 @@ def test_counters(engine):
     assert res.probe_misses == ref["probe_misses"]
     assert res.node_body_entries == ref["node_body_entries"][:len(plan)]
     assert res.maps_built >= 2  # S and T roots forced, R never (BaseScan)
+
+
+def test_device_rmat_matches_host():
+    from paper_2301_10841_b200 import datagen
+    import torch
+    s, d = datagen.rmat(21, 14, 200000)
+    ds, dd = datagen.rmat_device(21, 14, 200000)
+    assert (ds.cpu().numpy() == s).all() and (dd.cpu().numpy() == d).all()
+    torch.cuda.synchronize()
