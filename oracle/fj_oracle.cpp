@@ -417,6 +417,127 @@ struct Exec {
     return true;
   }
 
+  // ---- memoised factorised count over a chain suffix (extension of
+  // count_factorized): from node k* on, each
+  // node j has exactly one open atom C_j whose last subatom is in j and binds
+  // only fresh variables; every other subatom of j is the first subatom of a
+  // fresh atom keyed on C_j's variables; at most one of those continues and
+  // becomes C_{j+1}. Then count(j, subtrie s of C_j) depends only on s and is
+  // memoised per COLT node.
+  struct ChainNode {
+    int carrier = -1;             // subatom index of C_j in node j
+    std::vector<int> fresh;       // subatom indices of the fresh atoms
+    int next = -1;                // subatom index (in node j) of C_{j+1}, -1 at the end
+  };
+  int chain_start = -1;
+  std::vector<ChainNode> chain;
+  std::vector<int> atom_first, atom_last;  // node index of each atom's first / last subatom
+  std::map<std::pair<int, const Node*>, unsigned __int128> memo;
+
+  bool chain_node_ok(int j, ChainNode& cn) const {
+    const PNode& N = nodes[j];
+    const int A = (int)tries.size();
+    int carrier_atom = -1;
+    for (int a = 0; a < A; ++a)
+      if (atom_first[a] < j && atom_last[a] >= j) {
+        if (carrier_atom >= 0) return false;
+        carrier_atom = a;
+      }
+    if (carrier_atom < 0) return false;
+    uint32_t cvars = 0;
+    for (size_t i = 0; i < N.subs.size(); ++i)
+      if (N.subs[i].atom == carrier_atom) {
+        if (cn.carrier >= 0 || !N.subs[i].last) return false;
+        cn.carrier = (int)i;
+        for (int v : N.subs[i].vars) cvars |= 1u << v;
+      }
+    if (cn.carrier < 0 || (cvars & N.avs_mask)) return false;
+    for (size_t i = 0; i < N.subs.size(); ++i) {
+      if ((int)i == cn.carrier) continue;
+      const PSub& X = N.subs[i];
+      if (X.level != 0) return false;
+      for (int v : X.vars)
+        if (!((cvars >> v) & 1u)) return false;
+      if (!X.last) {
+        if (cn.next >= 0) return false;
+        cn.next = (int)i;
+      }
+      cn.fresh.push_back((int)i);
+    }
+    for (size_t i = j; i < nodes.size(); ++i)
+      for (const PSub& X : nodes[i].subs)
+        for (int v : X.vars)
+          if ((N.avs_mask >> v) & 1u) return false;
+    return (cn.next >= 0) == (j + 1 < (int)nodes.size());
+  }
+
+  void analyze_chain() {
+    for (int k = (int)nodes.size() - 1; k >= 1; --k) {
+      ChainNode cn;
+      if (!chain_node_ok(k, cn)) break;
+      chain.insert(chain.begin(), cn);
+      chain_start = k;
+    }
+  }
+
+  unsigned __int128 chain_count(int j, const Sub& s) {
+    std::pair<int, const Node*> mk{j, s.singleton ? nullptr : s.node};
+    if (!s.singleton) {
+      auto it = memo.find(mk);
+      if (it != memo.end()) return it->second;
+    }
+    const ChainNode& cn = chain[j - chain_start];
+    const PNode& N = nodes[j];
+    const PSub& C = N.subs[cn.carrier];
+    Colt& CT = *tries[C.atom];
+    unsigned __int128 total = 0;
+    auto visit = [&](const int64_t* t, uint64_t m) {
+      unsigned __int128 f = m;
+      for (int xi : cn.fresh) {
+        const PSub& X = N.subs[xi];
+        Key key;
+        key.n = (int)X.vars.size();
+        for (int q = 0; q < key.n; ++q) {
+          int at = 0;
+          while (C.vars[at] != X.vars[q]) ++at;
+          key.v[q] = t[at];
+        }
+        Sub root;
+        root.node = &tries[X.atom]->root;
+        Sub out;
+        if (!get(X.atom, root, key, out)) return;
+        if (xi == cn.next)
+          f *= chain_count(j + 1, out);
+        else
+          f *= out.singleton ? 1 : tries[X.atom]->length(*out.node);
+      }
+      total += f;
+    };
+    int64_t t[MAXK];
+    if (s.singleton) {
+      visit(t, 1);
+    } else if (s.node->kind == Node::Map) {
+      const FlatMap& mp = *s.node->map;
+      for (size_t e = 0; e < mp.size(); ++e) visit(mp.keys[e].v, CT.length(*mp.vals[e]));
+    } else {
+      const uint64_t n = CT.length(*s.node);
+      for (uint64_t x = 0; x < n; ++x) {
+        const uint64_t row = s.node->kind == Node::BaseScan ? x : s.node->offs[x];
+        for (size_t q = 0; q < C.cols.size(); ++q) t[q] = CT.rel->at(C.cols[q], row);
+        visit(t, 1);
+      }
+    }
+    if (!s.singleton) memo[mk] = total;
+    return total;
+  }
+
+  void add_count128(unsigned __int128 v) {
+    const uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
+    uint64_t old = res.count_lo;
+    res.count_lo += lo;
+    res.count_hi += hi + (res.count_lo < old ? 1 : 0);
+  }
+
   // get (Fig 12 `get`: force then lookup)
   bool get(int atom, const Sub& sub, const Key& key, Sub& out) {
     ++res.probes;
@@ -452,6 +573,19 @@ struct Exec {
       return;
     }
     const PNode& N = nodes[k];
+    if (output_mode == 2 && k > 0 && k == chain_start && !factorizable(k)) {
+      unsigned __int128 m = 1;
+      int carrier = -1;
+      for (int a = 0; a < A; ++a) {
+        if (atom_last[a] < k)
+          m *= subs[a].singleton ? 1 : tries[a]->length(*subs[a].node);
+        else if (atom_first[a] < k)
+          carrier = a;
+      }
+      add_count128(m * chain_count(k, subs[carrier]));
+      res.factorized = 1;
+      return;
+    }
     if (output_mode == 2 && k > 0 && factorizable(k)) {
       uint64_t mult = 1;
       std::set<int> suffix_atoms;
@@ -660,6 +794,13 @@ static Result run_one(const Prepared& P, const std::vector<Relation>& rels, int 
   ex.part_var = P.nodes[0].subs[0].vars.empty() ? 0 : P.nodes[0].subs[0].vars[0];
   ex.collect = collect;
   const int A = (int)rels.size();
+  ex.atom_first.assign(A, 1 << 30);
+  ex.atom_last.assign(A, -1);
+  for (size_t k = 0; k < P.nodes.size(); ++k)
+    for (const PSub& ps : P.nodes[k].subs) {
+      ex.atom_first[ps.atom] = std::min(ex.atom_first[ps.atom], (int)k);
+      ex.atom_last[ps.atom] = std::max(ex.atom_last[ps.atom], (int)k);
+    }
   std::vector<Sub> subs(A);
   for (int a = 0; a < A; ++a) {
     auto T = std::make_unique<Colt>();
@@ -670,6 +811,7 @@ static Result run_one(const Prepared& P, const std::vector<Relation>& rels, int 
     subs[a].node = &T->root;
     ex.tries.push_back(std::move(T));
   }
+  if (output_mode == 2) ex.analyze_chain();
   std::vector<int64_t> vals(ex.nvars, 0);
   ex.batches.resize(P.nodes.size() + 1);
   ex.join(0, vals.data(), subs.data());

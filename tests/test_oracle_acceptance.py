@@ -131,3 +131,22 @@ def test_partitioned_execution_sums_to_whole():
         assert sum(p["count"] for p in parts) == whole["count"]
         assert sum(p["checksum"] for p in parts) % 2 ** 64 == whole["checksum"]
         assert oracle.execute(q, plan, cols, nthreads=3)["count"] == whole["count"]
+
+
+def test_memoised_chain_count_matches_enumeration_and_spmv():
+    """Memoised factorised count on the 5-path (chain suffix) == enumeration
+    == 1^T A^5 1 computed independently with exact integers."""
+    from paper_2301_10841_b200 import configs
+    for sc, m in [(8, 1500), (10, 6000)]:
+        w = configs.path5(scale=sc, m=m, seed=5)
+        plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+        a = oracle.execute(w.query, plan, w.atom_columns(), nthreads=4)
+        b = oracle.execute(w.query, plan, w.atom_columns(), output_mode="factorized_count")
+        assert b["factorized"]
+        src, dst = w.relations["E"]
+        x = np.ones(1 << sc, dtype=object)
+        for _ in range(5):
+            y = np.zeros(1 << sc, dtype=object)
+            np.add.at(y, src, x[dst])
+            x = y
+        assert a["count"] == b["count"] == int(x.sum())
