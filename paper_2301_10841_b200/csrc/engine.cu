@@ -456,7 +456,7 @@ __global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, in
 // ============================================================================
 // k_expand: iterate cover, probe, compact / aggregate  (Fig 13)
 // ============================================================================
-enum ExpandMode { EXPAND_WRITE = 0, EXPAND_COUNT = 1, EXPAND_ENUM = 2 };
+enum ExpandMode { EXPAND_WRITE = 0, EXPAND_COUNT = 1, EXPAND_ENUM = 2, EXPAND_MEMO = 3 };
 
 __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ a, uint64_t lo, uint64_t hi,
                                                     uint64_t x) {
@@ -513,6 +513,14 @@ __device__ __forceinline__ void put2(uint32_t (&a)[W], uint32_t (&b)[W], int v, 
     a[u] = (x & m) | (a[u] & ~m);
     b[u] = (y & m) | (b[u] & ~m);
   }
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t selu_(const uint32_t (&a)[W], int v) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int u = 0; u < W; ++u) x |= a[u] & (0u - (uint32_t)(u == v));
+  return x;
 }
 
 // One candidate: iterate the chosen cover at position j of entry e, then probe
@@ -660,6 +668,14 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
         acc_lo += mult;
         if (acc_lo < mult) ++acc_hi;
         if (min_var >= 0) acc_min = min(acc_min, (long long)sel(val, min_var));
+      } else if (MODE == EXPAND_MEMO) {
+        // memoised chain suffix: this binding contributes mult * count(child of the carrier)
+        const uint32_t q = selu_(cp, N.memo_atom);
+        const unsigned __int128 mv =
+            ((unsigned __int128)N.memo[2ull * q + 1] << 64) | (unsigned __int128)N.memo[2ull * q];
+        const unsigned __int128 c = mv * mult + (((unsigned __int128)acc_hi << 64) | acc_lo);
+        acc_lo = (uint64_t)c;
+        acc_hi = (uint64_t)(c >> 64);
       } else {
         const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
         for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
@@ -681,7 +697,7 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
     if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
     if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
   }
-  if (MODE == EXPAND_COUNT) {
+  if (MODE == EXPAND_COUNT || MODE == EXPAND_MEMO) {
     // 128-bit count: carry out of the low word
     uint64_t lo = acc_lo, hi = acc_hi;
 #pragma unroll
@@ -705,6 +721,79 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
       if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
     }
   }
+}
+
+__device__ __forceinline__ void atomic_add_u128(unsigned long long* m, unsigned __int128 v) {
+  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  const unsigned long long old = atomicAdd(m, lo);
+  const unsigned long long carry = (old + lo < old) ? 1ull : 0ull;
+  if (hi + carry) atomicAdd(m + 1, hi + carry);
+}
+
+__global__ void __launch_bounds__(256) k_memo_pass(const __grid_constant__ MemoPass M) {
+  const unsigned FULL = 0xffffffffu;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t iters = (M.n + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t pos = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + it * stride;
+    const bool ok = pos < M.n;
+    uint32_t g = 0;
+    unsigned __int128 f = 0;
+    if (ok) {
+      g = M.owner[pos];
+      int32_t t[MAXK];
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k) t[k] = k < M.cnv ? __ldg(M.cvals[k] + pos) : 0;
+      f = 1;
+      for (int x = 0; x < M.nfresh; ++x) {
+        const KSub& X = M.fresh[x];
+        int32_t key[MAXK];
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) {
+          int32_t v = 0;
+#pragma unroll
+          for (int u = 0; u < MAXK; ++u) v |= t[u] & -(int32_t)(u == M.cpos[x][k]);
+          key[k] = k < X.nv ? v : 0;
+        }
+        uint32_t q, ql;
+        if (!colt_get(X, 0u, X.root_n, key, q, ql)) {
+          f = 0;
+          break;
+        }
+        if (M.cont[x])
+          f *= ((unsigned __int128)M.memo_next[2ull * q + 1] << 64) | (unsigned __int128)M.memo_next[2ull * q];
+        else
+          f *= ql;
+      }
+    }
+    // positions of one group are contiguous: aggregate per group inside the warp
+    const unsigned act = __ballot_sync(FULL, ok && f != 0);
+    if (ok && f != 0) {
+      const unsigned grp = __match_any_sync(act, g);
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(grp) - 1;
+      unsigned long long lo = (unsigned long long)f, hi = (unsigned long long)(f >> 64);
+      unsigned long long slo = 0, shi = 0;
+      unsigned m = grp;
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const unsigned long long a = __shfl_sync(grp, lo, l), b = __shfl_sync(grp, hi, l);
+        const unsigned long long s2 = slo + a;
+        shi += b + (s2 < slo ? 1ull : 0ull);
+        slo = s2;
+      }
+      if (lane == leader) atomic_add_u128(M.memo_out + 2ull * g, ((unsigned __int128)shi << 64) | slo);
+    }
+  }
+}
+
+struct MaxOp {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+__global__ void k_group_starts(const uint32_t* cnt, uint64_t n, uint32_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = cnt[i] ? (uint32_t)i : 0u;
 }
 
 // host-side dispatch on the query width (max(#vars, #atoms) -> 4 / 8 / 16)
@@ -932,6 +1021,14 @@ struct fjg_query {
   uint64_t batch = 0;
   int min_var = -1;
   int width = 16;  // max(#variables, #atoms): selects the register-resident kernel variant
+  // memoised chain count (FJG_OUT_FACTORIZED_COUNT over a chain suffix)
+  int chain_start = -1;                 // k*, or -1 if the plan has no device-memoisable chain suffix
+  std::vector<MemoPass> memo_passes;    // for nodes K-1 .. k* (index j - k*)
+  std::vector<unsigned long long*> memo;  // per chain node: 2n u64 (lo, hi)
+  std::vector<uint64_t> memo_n;
+  std::map<int, uint32_t*> owner;       // per carrier trie: group start of each level-0 position
+  KNode memo_top{};                     // node k*-1 aggregating mult * memo[child]
+  int stop_node = -1;
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   // non-blocking phase timer: event pairs resolved after the final sync
@@ -1221,6 +1318,109 @@ static void build_knodes(fjg_query* q) {
   }
 }
 
+// Chain-suffix analysis for the memoised factorised count (mirrors the
+// oracle's Exec::chain_node_ok). Device-specific extra
+// condition: the carrier's subatom at node j is its second one (depth 1), so
+// the memo is indexed by level-0 groups, which forcing the root builds whole.
+static bool device_chain_node(const fjg_query* q, int j, int& carrier, std::vector<int>& fresh, int& next) {
+  const auto& plan = q->plan;
+  const DevNode& N = q->nodes[j];
+  const int A = (int)q->atoms.size();
+  carrier = -1;
+  next = -1;
+  fresh.clear();
+  int catom = -1;
+  for (int a = 0; a < A; ++a) {
+    const auto& S = q->atoms[a].subs;
+    if (S.front().first < j && S.back().first >= j) {
+      if (catom >= 0) return false;
+      catom = a;
+    }
+  }
+  if (catom < 0) return false;
+  uint32_t cvars = 0;
+  for (int i = 0; i < N.nsub; ++i)
+    if (N.sub[i].atom == catom) {
+      if (carrier >= 0 || !N.sub[i].last || N.sub[i].depth != 1) return false;
+      carrier = i;
+      for (int t = 0; t < N.sub[i].nv; ++t) cvars |= 1u << N.sub[i].var[t];
+    }
+  if (carrier < 0 || (cvars & N.in_vars)) return false;
+  for (int i = 0; i < N.nsub; ++i) {
+    if (i == carrier) continue;
+    const DevSub& X = N.sub[i];
+    if (X.depth != 0) return false;
+    for (int t = 0; t < X.nv; ++t)
+      if (!((cvars >> X.var[t]) & 1u)) return false;
+    if (!X.last) {
+      if (next >= 0) return false;
+      next = i;
+    }
+    fresh.push_back(i);
+  }
+  for (size_t i = j; i < plan.nodes.size(); ++i)
+    for (int t = 0; t < q->nodes[i].nsub; ++t)
+      for (int u = 0; u < q->nodes[i].sub[t].nv; ++u)
+        if ((N.in_vars >> q->nodes[i].sub[t].var[u]) & 1u) return false;
+  return (next >= 0) == (j + 1 < (int)plan.nodes.size());
+}
+
+static void prepare_chain(fjg_query* q) {
+  const int K = (int)q->nodes.size();
+  int start = -1;
+  std::vector<MemoPass> passes;
+  for (int j = K - 1; j >= 1; --j) {
+    int carrier, next;
+    std::vector<int> fresh;
+    if (!device_chain_node(q, j, carrier, fresh, next)) break;
+    // the node before the chain must hand over the carrier's level-0 child
+    MemoPass M{};
+    const KNode& G = q->knodes[j];
+    const KSub& C = G.sub[carrier];
+    M.n = q->tries[C.trie].dev.n;
+    M.cnv = C.nv;
+    for (int t = 0; t < C.nv; ++t) M.cvals[t] = C.src[t];
+    M.nfresh = (int)fresh.size();
+    for (int x = 0; x < M.nfresh; ++x) {
+      const KSub& X = G.sub[fresh[x]];
+      M.fresh[x] = X;
+      M.cont[x] = fresh[x] == next ? 1 : 0;
+      for (int t = 0; t < X.nv; ++t) {
+        int at = 0;
+        while (C.var[at] != X.var[t]) ++at;
+        M.cpos[x][t] = (int8_t)at;
+      }
+    }
+    passes.insert(passes.begin(), M);
+    start = j;
+  }
+  if (start < 1) return;
+  q->chain_start = start;
+  q->memo_passes = passes;
+  q->memo.resize(passes.size());
+  q->memo_n.resize(passes.size());
+  for (size_t i = 0; i < passes.size(); ++i) {
+    const int j = start + (int)i;
+    int cidx, nx0;
+    std::vector<int> fr0;
+    device_chain_node(q, j, cidx, fr0, nx0);
+    const KSub& C = q->knodes[j].sub[cidx];
+    q->memo_n[i] = passes[i].n;
+    q->memo[i] = (unsigned long long*)q->alloc(std::max<uint64_t>(passes[i].n, 1) * 16);
+    if (!q->owner.count(C.trie)) q->owner[C.trie] = (uint32_t*)q->alloc(std::max<uint64_t>(passes[i].n, 1) * 4);
+    q->memo_passes[i].owner = q->owner[C.trie];
+    q->memo_passes[i].memo_out = q->memo[i];
+  }
+  for (size_t i = 0; i + 1 < passes.size(); ++i) q->memo_passes[i].memo_next = q->memo[i + 1];
+  // the aggregating top node
+  int c, nx;
+  std::vector<int> fr;
+  device_chain_node(q, start, c, fr, nx);
+  q->memo_top = q->knodes[start - 1];
+  q->memo_top.memo = q->memo[0];
+  q->memo_top.memo_atom = q->knodes[start].sub[c].atom;
+}
+
 // (Re)allocate per-node frontier buffers for a candidate capacity `cap`.
 static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   if (q->cap >= cap && q->cap) return;
@@ -1262,6 +1462,13 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
     q->cub_tmp_bytes = need;
   }
   build_knodes(q);
+  if (q->chain_start < 0 && q->memo_passes.empty()) prepare_chain(q);
+  else if (q->chain_start >= 1) {  // frontier pointers moved: refresh the top node
+    const int c = q->memo_top.memo_atom;
+    q->memo_top = q->knodes[q->chain_start - 1];
+    q->memo_top.memo = q->memo[0];
+    q->memo_top.memo_atom = c;
+  }
 }
 
 static void sync_counters(fjg_query* q) {
@@ -1360,7 +1567,9 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   q->node_inputs[k] += F;
   fjg_engine* eng = q->eng;
   const DevNode& N = q->nodes[k];
-  const KNode& KN = q->knodes[k];
+  const bool memo_top = mode == EXPAND_MEMO && k == q->stop_node;
+  const KNode& KN = memo_top ? q->memo_top : q->knodes[k];
+  const bool is_last = N.is_last || memo_top;
   LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(KN, q->d_tries, F,
                                                                                     q->dynamic ? 1 : 0, q->d_ctr));
   size_t bytes = q->cub_tmp_bytes;
@@ -1372,7 +1581,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   const uint64_t M = q->h_ctr->total_m;
   force_claims(q, k);
   if (M == 0) return;
-  if (N.is_last) {
+  if (is_last) {
     q->mark(eng->stream, -1);
     for (uint64_t c0 = 0; c0 < M; c0 += kLastChunk) {
       const uint64_t c1 = std::min(M, c0 + kLastChunk);
@@ -1382,6 +1591,9 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       if (mode == EXPAND_ENUM)
         LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1,
                                                q->out_tuples, q->out_cap, q->d_ctr));
+      else if (mode == EXPAND_MEMO)
+        LAUNCH(eng, launch_expand<EXPAND_MEMO>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
+                                               q->d_ctr));
       else
         LAUNCH(eng, launch_expand<EXPAND_COUNT>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, q->min_var,
                                                 nullptr, 0, q->d_ctr));
@@ -1432,8 +1644,45 @@ static void reset_query(fjg_query* q) {
   q->ev_used = 0;
 }
 
+// Memoised chain count: force the chain tries' roots, then the bottom-up passes.
+static void run_memo_passes(fjg_query* q) {
+  fjg_engine* eng = q->eng;
+  std::set<int> tries;
+  for (int j = q->chain_start; j < (int)q->nodes.size(); ++j)
+    for (int i = 0; i < q->nodes[j].nsub; ++i) tries.insert(q->nodes[j].sub[i].trie);
+  for (int t : tries)
+    if (!q->tries[t].root_forced) {
+      force_level(q, t, 0, true, 0, (uint32_t)q->tries[t].rel->nrows, 1);
+      LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
+      q->tries[t].root_forced = true;
+    }
+  for (auto& [t, own] : q->owner) {
+    const uint64_t n = q->tries[t].rel->nrows;
+    if (!n) continue;
+    LAUNCH(eng, k_group_starts<<<grid_for(n), 256, 0, eng->stream>>>(q->tries[t].dev.lev[0].cnt, n, own));
+    size_t bytes = 0;
+    CK(cub::DeviceScan::InclusiveScan(nullptr, bytes, own, own, MaxOp(), (int64_t)n));
+    void* tmp = eng->pool->alloc(bytes);
+    CK(cub::DeviceScan::InclusiveScan(tmp, bytes, own, own, MaxOp(), (int64_t)n, eng->stream));
+    ++eng->launches;
+    eng->pool->free(tmp);
+  }
+  q->mark(eng->stream, -1);
+  for (int i = (int)q->memo_passes.size() - 1; i >= 0; --i) {
+    const MemoPass& M = q->memo_passes[i];
+    CK(cudaMemsetAsync(q->memo[i], 0, std::max<uint64_t>(M.n, 1) * 16, eng->stream));
+    if (M.n) LAUNCH(eng, k_memo_pass<<<grid_for(M.n, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(M));
+  }
+  q->mark(eng->stream, 1);
+}
+
 static void execute_once(fjg_query* q, int mode) {
   reset_query(q);
+  q->stop_node = -1;
+  if (mode == EXPAND_MEMO) {
+    run_memo_passes(q);
+    q->stop_node = q->chain_start - 1;
+  }
   run_node(q, 0, 1, mode);
   sync_counters(q);
   q->resolve_marks();
@@ -1712,7 +1961,8 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     q->batch = batch;
     q->min_var = o.min_var;
     const uint32_t l0 = eng->launches, s0 = eng->syncs;
-    execute_once(q, EXPAND_COUNT);
+    const bool memo = o.output_mode == FJG_OUT_FACTORIZED_COUNT && q->chain_start >= 1;
+    execute_once(q, memo ? EXPAND_MEMO : EXPAND_COUNT);
     if (o.output_mode == FJG_OUT_ENUMERATE) {
       const uint64_t rows = q->h_ctr->count_lo;
       if (q->h_ctr->count_hi || rows > (1ull << 34) / std::max<uint64_t>(q->head.size(), 1))

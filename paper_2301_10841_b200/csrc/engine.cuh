@@ -153,7 +153,26 @@ struct KNode {
   uint8_t* chosen;
   uint64_t* m;
   uint64_t* scan;
+  const unsigned long long* memo;  // memoised chain count per child start (u128 as lo,hi), or null
+  int memo_atom;                   // atom whose child subtrie indexes `memo`
   KSub sub[MAXS];
+};
+
+// One bottom-up pass of the memoised chain count: for every
+// row of the carrier trie's level-0 domain, probe the fresh atoms' roots with
+// the row's values and add prod(leaf lengths) * memo_next[child] to the row's
+// group.
+struct MemoPass {
+  uint64_t n;
+  const uint32_t* owner;       // group start of every position (level 0)
+  const int32_t* cvals[MAXK];  // carrier's variables at level-0 positions
+  int cnv;
+  int nfresh;
+  int cont[MAXS];              // fresh atom continues the chain (uses memo_next)
+  int8_t cpos[MAXS][MAXK];     // key var t of fresh x = carrier var cpos[x][t]
+  KSub fresh[MAXS];
+  const unsigned long long* memo_next;
+  unsigned long long* memo_out;
 };
 
 struct DevCounters {

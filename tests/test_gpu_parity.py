@@ -222,3 +222,22 @@ def test_scale_triangle_partition(engine):
     full = engine.relation(cols[1])
     r = engine.query({"query": w.query}, plan, [part, full, part]).execute()
     assert r.count == g["count"] and f"{r.checksum:#018x}" == g["checksum"]
+
+
+@pytest.mark.parametrize("scale,m", [(8, 1500), (12, 30000), (16, 400000)])
+def test_path5_memoised_count(engine, scale, m):
+    """C5 5-path at reduced scale: the device memoised chain count equals the
+    oracle's memoised count and an independent exact 1^T A^5 1."""
+    w = configs.path5(scale=scale, m=m, seed=5)
+    res, q, plan, _ = fjg.run_workload(engine, w, output_mode="factorized_count")
+    ref = oracle.execute(w.query, plan, w.atom_columns(), output_mode="factorized_count")
+    assert ref["factorized"]
+    src, dst = w.relations["E"]
+    x = np.ones(1 << scale, dtype=object)
+    for _ in range(5):
+        y = np.zeros(1 << scale, dtype=object)
+        np.add.at(y, src, x[dst])
+        x = y
+    assert res.count == ref["count"] == int(x.sum())
+    if scale == 8:  # plain enumeration agrees too
+        assert fjg.run_workload(engine, w)[0].count == res.count
