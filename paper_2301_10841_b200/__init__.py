@@ -34,4 +34,6 @@ def run_workload(engine, w, **exec_kw):
     kw = dict(exec_kw)
     if w.min_var is not None and "min_var" not in kw:
         kw["min_var"] = w.min_var
+    if getattr(w, "output_mode", "count") != "count" and "output_mode" not in kw:
+        kw["output_mode"] = w.output_mode
     return q.execute(**kw), q, fj_plan, rels

@@ -24,6 +24,7 @@ class Workload:
     filters: dict = field(default_factory=dict)  # base relation -> [(col, op, const)]
     min_var: str = None
     params: dict = field(default_factory=dict)
+    output_mode: str = "count"     # factorized_count for the 5-path (memoised chain count)
 
     @property
     def query_json(self):
@@ -121,7 +122,7 @@ def path5(scale=27, m=512 * M, seed=5):
     vs = "abcdef"
     q = [{"rel": f"E{i + 1}", "vars": [vs[i], vs[i + 1]]} for i in range(5)]
     return Workload("path5", q, left_deep([f"E{i + 1}" for i in range(5)]), "free", {"E": [src, dst]}, ["E"] * 5,
-                    params={"scale": scale, "edges": m, "seed": seed})
+                    params={"scale": scale, "edges": m, "seed": seed}, output_mode="factorized_count")
 
 
 def scale_triangle(scale=27, m=512 * M, seed=5):
@@ -131,5 +132,12 @@ def scale_triangle(scale=27, m=512 * M, seed=5):
     return w
 
 
-CONFIGS = {"chain": chain, "triangle": triangle, "star": star, "clique4": clique4, "path5": path5,
+def scale_path5(scale=27, m=512 * M, seed=5):
+    """C5 5-path at R-MAT 2^27 / 512M edges (count only, memoised)."""
+    w = path5(scale, m, seed)
+    w.name = "scale_path5"
+    return w
+
+
+CONFIGS = {"scale_path5": scale_path5, "chain": chain, "triangle": triangle, "star": star, "clique4": clique4, "path5": path5,
            "scale_triangle": scale_triangle}

@@ -241,3 +241,30 @@ def test_path5_memoised_count(engine, scale, m):
     assert res.count == ref["count"] == int(x.sum())
     if scale == 8:  # plain enumeration agrees too
         assert fjg.run_workload(engine, w)[0].count == res.count
+
+
+def test_scale_path5_residues(engine):
+    """C5 5-path at full size (~4.9e21 walks, > 2^64): the device memoised count
+    agrees with 1^T A^5 1 computed independently by torch index_add SpMV,
+    modulo 2^64 and modulo two primes (exact integer residues)."""
+    import torch
+    w = configs.scale_path5()
+    res, q, plan, rels = fjg.run_workload(engine, w)
+    assert res.count > 2 ** 64
+    q.close()
+    for r in rels.values():
+        r.close()
+    src = torch.from_numpy(w.relations["E"][0]).cuda().long()
+    dst = torch.from_numpy(w.relations["E"][1]).cuda().long()
+    n = 1 << w.params["scale"]
+    for mod in (None, 2_147_483_647, 1_000_000_007):
+        x = torch.ones(n, dtype=torch.int64, device="cuda")
+        for _ in range(5):
+            y = torch.zeros(n, dtype=torch.int64, device="cuda")
+            y.index_add_(0, src, x[dst])  # wraps mod 2^64 when mod is None
+            x = y if mod is None else y % mod
+        tot = int(x.sum().item()) if mod is not None else int(x.sum().item()) & (2 ** 64 - 1)
+        if mod is None:
+            assert tot == res.count % 2 ** 64
+        else:
+            assert tot % mod == res.count % mod
