@@ -32,6 +32,7 @@
 #include <memory>
 #include <set>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -523,22 +524,77 @@ __device__ __forceinline__ uint32_t selu_(const uint32_t (&a)[W], int v) {
   return x;
 }
 
+// Per-candidate binding state. Narrow queries (W = 4) keep it in registers
+// with arithmetic-blend selects; wider ones (W >= 8, where a blend costs W
+// instructions per access) keep it in shared memory, variable-major so the
+// lanes of a warp hit distinct banks.
+template <int W>
+struct RegState {
+  int32_t val[W];
+  uint32_t cp[W], cl[W];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int u = 0; u < W; ++u) val[u] = cp[u] = cl[u] = 0;
+  }
+  __device__ __forceinline__ int32_t get(int v) const { return sel(val, v); }
+  __device__ __forceinline__ void set(int v, int32_t x) { put(val, v, x); }
+  __device__ __forceinline__ int32_t at(int u) const { return val[u]; }
+  __device__ __forceinline__ void seta(int u, int32_t x) { val[u] = x; }
+  __device__ __forceinline__ void setc(int a, uint32_t p, uint32_t l) { put2(cp, cl, a, p, l); }
+  __device__ __forceinline__ void setca(int a, uint32_t p, uint32_t l) {
+    cp[a] = p;
+    cl[a] = l;
+  }
+  __device__ __forceinline__ uint32_t cpa(int a) const { return cp[a]; }
+  __device__ __forceinline__ uint32_t cla(int a) const { return cl[a]; }
+  __device__ __forceinline__ uint32_t cpd(int a) const { return selu_(cp, a); }
+};
+
+template <int W>
+struct SmemState {
+  int32_t* val;
+  uint32_t *cp, *cl;
+  __device__ __forceinline__ SmemState(int32_t* sv, uint32_t* sp, uint32_t* sl)
+      : val(sv + threadIdx.x), cp(sp + threadIdx.x), cl(sl + threadIdx.x) {}
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int u = 0; u < W; ++u) val[u * TILE] = cp[u * TILE] = cl[u * TILE] = 0;
+  }
+  __device__ __forceinline__ int32_t get(int v) const { return val[v * TILE]; }
+  __device__ __forceinline__ void set(int v, int32_t x) { val[v * TILE] = x; }
+  __device__ __forceinline__ int32_t at(int u) const { return val[u * TILE]; }
+  __device__ __forceinline__ void seta(int u, int32_t x) { val[u * TILE] = x; }
+  __device__ __forceinline__ void setc(int a, uint32_t p, uint32_t l) {
+    cp[a * TILE] = p;
+    cl[a * TILE] = l;
+  }
+  __device__ __forceinline__ void setca(int a, uint32_t p, uint32_t l) { setc(a, p, l); }
+  __device__ __forceinline__ uint32_t cpa(int a) const { return cp[a * TILE]; }
+  __device__ __forceinline__ uint32_t cla(int a) const { return cl[a * TILE]; }
+  __device__ __forceinline__ uint32_t cpd(int a) const { return cp[a * TILE]; }
+};
+
+template <class St, int W>
+__device__ __forceinline__ St make_state(uint32_t* smem) {
+  if constexpr (W >= 8) {
+    return St(reinterpret_cast<int32_t*>(smem), smem + W * TILE, smem + 2 * W * TILE);
+  } else {
+    return St();
+  }
+}
+
 // One candidate: iterate the chosen cover at position j of entry e, then probe
 // every other subatom of the node in order. Returns false if the candidate dies.
-template <int MODE, int W>
-__device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64_t j, int32_t (&val)[W],
-                                              uint32_t (&cp)[W], uint32_t (&cl)[W], uint64_t& mult,
+template <int MODE, int W, class St>
+__device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64_t j, St& st, uint64_t& mult,
                                               uint64_t& probes, uint64_t& misses, uint64_t& body) {
 #pragma unroll
   for (int v = 0; v < W; ++v)
-    if ((N.in_vars >> v) & 1u) val[v] = __ldg(N.in_var[v] + e);
+    if ((N.in_vars >> v) & 1u) st.seta(v, __ldg(N.in_var[v] + e));
   if (MODE == EXPAND_WRITE) {
 #pragma unroll
     for (int a = 0; a < W; ++a)
-      if ((N.in_atoms >> a) & 1u) {
-        cp[a] = __ldg(N.in_p[a] + e);
-        cl[a] = __ldg(N.in_len[a] + e);
-      }
+      if ((N.in_atoms >> a) & 1u) st.setca(a, __ldg(N.in_p[a] + e), __ldg(N.in_len[a] + e));
   }
   if (N.in_mult) mult = __ldg(N.in_mult + e);
   // ---- iterate the chosen cover (Fig 12 iter) ----
@@ -547,16 +603,16 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
   uint32_t p, len;
   subtrie_of(S, e, p, len);
   if (p == kSingleton) {
-    put2(cp, cl, S.atom, kSingleton, 1u);
+    st.setc(S.atom, kSingleton, 1u);
   } else {
     const uint32_t pos = p + (uint32_t)j;
     if (!S.stream) {
       // forced map: distinct keys are the child starts
       const uint32_t c = __ldg(S.cnt + pos);
       if (c == 0) return false;
-      put2(cp, cl, S.atom, pos, c);
+      st.setc(S.atom, pos, c);
     } else {
-      put2(cp, cl, S.atom, kSingleton, 1u);  // suffix: stream values at the offsets
+      st.setc(S.atom, kSingleton, 1u);  // suffix: stream values at the offsets
     }
 #pragma unroll
     for (int t = 0; t < MAXK; ++t)
@@ -564,9 +620,9 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
         const int32_t x = __ldg(S.src[t] + pos);
         const int v = S.var[t];
         if ((S.bound_mask >> t) & 1) {
-          if (sel(val, v) != x) return false;  // cover re-binds a bound variable
+          if (st.get(v) != x) return false;  // cover re-binds a bound variable
         } else {
-          put(val, v, x);
+          st.set(v, x);
         }
       }
   }
@@ -581,7 +637,7 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
     if (pp != kSingleton) {
       int32_t key[MAXK];
 #pragma unroll
-      for (int t = 0; t < MAXK; ++t) key[t] = t < P.nv ? sel(val, P.var[t]) : 0;
+      for (int t = 0; t < MAXK; ++t) key[t] = t < P.nv ? st.get(P.var[t]) : 0;
       ++probes;
       if (!colt_get(P, pp, pl, key, q, ql)) {
         ++misses;
@@ -591,7 +647,7 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
     if (P.last)
       mult *= ql;  // residual leaf vector: its offsets are the multiplicity
     else
-      put2(cp, cl, P.atom, q, ql);
+      st.setc(P.atom, q, ql);
   }
   return true;
 }
@@ -600,35 +656,32 @@ __device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64
 #define FJG_EXPAND_MINBLOCKS 1
 #endif
 template <int MODE, int W>
-__global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                 uint64_t F, const uint64_t* __restrict__ bounds, int min_var,
-                                                 int32_t* __restrict__ out_tuples, uint64_t out_cap,
-                                                 DevCounters* ctr) {
+__global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __grid_constant__ KNode N, uint64_t c0,
+                                                                       uint64_t c1, uint64_t F,
+                                                                       const uint64_t* __restrict__ bounds,
+                                                                       int min_var, int32_t* __restrict__ out_tuples,
+                                                                       uint64_t out_cap, DevCounters* ctr) {
   __shared__ uint32_t s_warp[TILE / 32];
   __shared__ uint32_t s_base;
+  extern __shared__ uint32_t s_state[];  // W >= 8: 3 * W * TILE words
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
   long long acc_min = LLONG_MAX;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t* __restrict__ scan = N.scan;
+  using St = typename std::conditional<(W >= 8), SmemState<W>, RegState<W>>::type;
 
   for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
     const uint64_t t = (base - c0) / TILE;
     const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
     const uint64_t i = base + threadIdx.x;
     bool alive = i < c1;
-    int32_t val[W];
-    uint32_t cp[W], cl[W];
+    St st = make_state<St, W>(s_state);
+    st.init();
     uint64_t mult = 1;
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      val[u] = 0;
-      cp[u] = 0;
-      cl[u] = 0;
-    }
     if (alive) {
       const uint64_t e = upper_bound_u64(scan, lo, hi, i);
       const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
-      alive = run_candidate<MODE, W>(N, e, j, val, cp, cl, mult, probes, misses, body);
+      alive = run_candidate<MODE, W>(N, e, j, st, mult, probes, misses, body);
     }
     if (MODE == EXPAND_WRITE) {
       const unsigned bal = __ballot_sync(0xffffffffu, alive);
@@ -648,12 +701,12 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
         const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
 #pragma unroll
         for (int v = 0; v < W; ++v)
-          if ((N.out_vars >> v) & 1u) N.out_var[v][o] = val[v];
+          if ((N.out_vars >> v) & 1u) N.out_var[v][o] = st.at(v);
 #pragma unroll
         for (int a = 0; a < W; ++a)
           if ((N.out_atoms >> a) & 1u) {
-            N.out_p[a][o] = cp[a];
-            N.out_len[a][o] = cl[a];
+            N.out_p[a][o] = st.cpa(a);
+            N.out_len[a][o] = st.cla(a);
           }
         if (N.out_mult) N.out_mult[o] = mult;
       }
@@ -663,14 +716,14 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
         uint64_t h = fj::kTupleHashSeed;
 #pragma unroll
         for (int v = 0; v < W; ++v)
-          if (v < N.nhead) h = fj::tuple_hash_step(h, (int64_t)val[v]);
+          if (v < N.nhead) h = fj::tuple_hash_step(h, (int64_t)st.at(v));
         acc_sum += mult * fj::checksum_word(h);
         acc_lo += mult;
         if (acc_lo < mult) ++acc_hi;
-        if (min_var >= 0) acc_min = min(acc_min, (long long)sel(val, min_var));
+        if (min_var >= 0) acc_min = min(acc_min, (long long)st.get(min_var));
       } else if (MODE == EXPAND_MEMO) {
         // memoised chain suffix: this binding contributes mult * count(child of the carrier)
-        const uint32_t q = selu_(cp, N.memo_atom);
+        const uint32_t q = st.cpd(N.memo_atom);
         const unsigned __int128 mv =
             ((unsigned __int128)N.memo[2ull * q + 1] << 64) | (unsigned __int128)N.memo[2ull * q];
         const unsigned __int128 c = mv * mult + (((unsigned __int128)acc_hi << 64) | acc_lo);
@@ -681,7 +734,7 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
         for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
 #pragma unroll
           for (int v = 0; v < W; ++v)
-            if (v < N.nhead) out_tuples[(o + r) * N.nhead + v] = val[v];
+            if (v < N.nhead) out_tuples[(o + r) * N.nhead + v] = st.at(v);
       }
     }
   }
@@ -801,12 +854,18 @@ template <int MODE>
 static void launch_expand(int width, unsigned grid, cudaStream_t st, const KNode& nd, uint64_t c0, uint64_t c1,
                           uint64_t F, const uint64_t* bounds, int min_var, int32_t* out, uint64_t cap,
                           DevCounters* ctr) {
+  static bool attr_set = false;
+  if (!attr_set) {  // the W >= 8 variants keep per-candidate state in (>48 KB) dynamic shared memory
+    cudaFuncSetAttribute(k_expand<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 8 * TILE * 4);
+    cudaFuncSetAttribute(k_expand<MODE, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16 * TILE * 4);
+    attr_set = true;
+  }
   if (width <= 4)
     k_expand<MODE, 4><<<grid, TILE, 0, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
   else if (width <= 8)
-    k_expand<MODE, 8><<<grid, TILE, 0, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
+    k_expand<MODE, 8><<<grid, TILE, 3 * 8 * TILE * 4, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
   else
-    k_expand<MODE, 16><<<grid, TILE, 0, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
+    k_expand<MODE, 16><<<grid, TILE, 3 * 16 * TILE * 4, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
 }
 
 // ============================================================================
