@@ -849,6 +849,143 @@ __global__ void k_group_starts(const uint32_t* cnt, uint64_t n, uint32_t* out) {
     out[i] = cnt[i] ? (uint32_t)i : 0u;
 }
 
+// Fast path for the Generic-Join-shaped aggregating last node: every subatom
+// is a cover over the same single new variable x (triangle C2/C5, 4-clique
+// C4). Per candidate: binding lookup, one coalesced cover read, NS-1 bucket
+// probes, fold into count / checksum -- no generic state machinery.
+template <int NS, int W>
+__global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                  uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
+                                                  int min_var, DevCounters* ctr) {
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const uint64_t* __restrict__ scan = N.scan;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    const uint64_t i = base + threadIdx.x;
+    if (i >= c1) continue;
+    const uint64_t e = upper_bound_u64(scan, lo, hi, i);
+    const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+    const int ci = N.chosen[e];
+    uint32_t sp[NS], sl[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const KSub& P = N.sub[s];
+      if (P.in_p) {
+        sp[s] = __ldg(P.in_p + e);
+        sl[s] = __ldg(P.in_len + e);
+      } else {
+        sp[s] = 0;
+        sl[s] = P.root_n;
+      }
+    }
+    uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+    uint32_t cpos = 0;
+    const int32_t* csrc = nullptr;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == ci) {
+        cpos = sp[s] + (uint32_t)j;
+        csrc = N.sub[s].src[0];
+      }
+    const int32_t x = __ldg(csrc + cpos);
+    ++body;
+    bool alive = true;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s == ci || !alive) continue;
+      const KSub& P = N.sub[s];
+      ++probes;
+      const uint32_t kw = (uint32_t)x;
+      uint64_t b = region_bucket(sp[s], sl[s], kw);
+      const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+      const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+      uint32_t q = kEmpty;
+      while (true) {
+        const uint4 h0 = __ldg(tb + 2 * b);
+        if (h0.y == kEmpty) break;
+        if (h0.x == kw) { q = h0.y; break; }
+        if (h0.w == kEmpty) break;
+        if (h0.z == kw) { q = h0.w; break; }
+        const uint4 h1 = __ldg(tb + 2 * b + 1);
+        if (h1.y == kEmpty) break;
+        if (h1.x == kw) { q = h1.y; break; }
+        if (h1.w == kEmpty) break;
+        if (h1.z == kw) { q = h1.w; break; }
+        if (++b == bhi) b = blo;
+      }
+      if (q == kEmpty) {
+        ++misses;
+        alive = false;
+      } else if (P.last) {
+        mult *= __ldg(P.cnt + q);
+      }
+    }
+    if (!alive) continue;
+    uint64_t h = fj::kTupleHashSeed;
+#pragma unroll
+    for (int v = 0; v < W; ++v)
+      if (v < N.nhead) {
+        const int32_t val = (v == xvar) ? x : __ldg(N.in_var[v] + e);
+        h = fj::tuple_hash_step(h, (int64_t)val);
+        if (v == min_var) acc_min = min(acc_min, (long long)val);
+      }
+    acc_sum += mult * fj::checksum_word(h);
+    acc_lo += mult;
+    if (acc_lo < mult) ++acc_hi;
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  uint64_t lo2 = acc_lo, hi2 = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
+    const uint64_t sm = lo2 + l2;
+    hi2 += h2 + (sm < lo2 ? 1 : 0);
+    lo2 = sm;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (lo2) {
+      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
+      if (old + lo2 < old) ++hi2;
+    }
+    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
+    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+  }
+}
+
+// The GJ fast path applies when every subatom of the node is a one-variable
+// cover of the same new, unbound variable, and no subtrie can be a streamed
+// singleton (all subatoms keys-or-stream levels of depth >= 0 with nv == 1).
+static int gj_last_var(const KNode& G, const DevNode& N) {
+  if (N.nsub < 2 || N.nsub > 3 || N.ncov != N.nsub || N.nhead > 8) return -1;
+  int x = -1;
+  for (int s = 0; s < N.nsub; ++s) {
+    const DevSub& D = N.sub[s];
+    if (D.nv != 1 || D.bound_mask || !D.stream) return -1;
+    if (x >= 0 && D.var[0] != x) return -1;
+    x = D.var[0];
+  }
+  // every earlier subatom of these atoms bound variables (no singleton residuals)
+  for (int s = 0; s < N.nsub; ++s)
+    if (G.sub[s].in_p == nullptr && N.sub[s].depth != 0) return -1;
+  return x;
+}
+
 // host-side dispatch on the query width (max(#vars, #atoms) -> 4 / 8 / 16)
 template <int MODE>
 static void launch_expand(int width, unsigned grid, cudaStream_t st, const KNode& nd, uint64_t c0, uint64_t c1,
@@ -1088,6 +1225,7 @@ struct fjg_query {
   std::map<int, uint32_t*> owner;       // per carrier trie: group start of each level-0 position
   KNode memo_top{};                     // node k*-1 aggregating mult * memo[child]
   int stop_node = -1;
+  int gj_x[MAXN];  // per node: the GJ fast-path variable, or -1
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   // non-blocking phase timer: event pairs resolved after the final sync
@@ -1315,6 +1453,8 @@ static void prepare_query(fjg_query* q) {
 }
 
 // Resolve each node's descriptor into the constant-bank kernel plan.
+static int gj_last_var(const KNode& G, const DevNode& N);
+
 static void build_knodes(fjg_query* q) {
   const size_t K = q->nodes.size();
   q->knodes.assign(K, KNode{});
@@ -1375,6 +1515,7 @@ static void build_knodes(fjg_query* q) {
       S.depth = (uint8_t)D.depth;
     }
   }
+  for (size_t k = 0; k < K && k < (size_t)MAXN; ++k) q->gj_x[k] = gj_last_var(q->knodes[k], q->nodes[k]);
 }
 
 // Chain-suffix analysis for the memoised factorised count (mirrors the
@@ -1653,7 +1794,22 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       else if (mode == EXPAND_MEMO)
         LAUNCH(eng, launch_expand<EXPAND_MEMO>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
                                                q->d_ctr));
-      else
+      else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT) {
+        const int W8 = q->head.size() <= 4 ? 4 : 8;
+        const int ns = N.nsub;
+        if (ns == 2 && W8 == 4)
+          LAUNCH(eng, (k_last_gj<2, 4><<<g, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_x[k], q->min_var,
+                                                                     q->d_ctr)));
+        else if (ns == 2)
+          LAUNCH(eng, (k_last_gj<2, 8><<<g, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_x[k], q->min_var,
+                                                                     q->d_ctr)));
+        else if (W8 == 4)
+          LAUNCH(eng, (k_last_gj<3, 4><<<g, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_x[k], q->min_var,
+                                                                     q->d_ctr)));
+        else
+          LAUNCH(eng, (k_last_gj<3, 8><<<g, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_x[k], q->min_var,
+                                                                     q->d_ctr)));
+      } else
         LAUNCH(eng, launch_expand<EXPAND_COUNT>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, q->min_var,
                                                 nullptr, 0, q->d_ctr));
     }
