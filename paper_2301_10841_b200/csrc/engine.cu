@@ -849,6 +849,12 @@ __global__ void k_group_starts(const uint32_t* cnt, uint64_t n, uint32_t* out) {
     out[i] = cnt[i] ? (uint32_t)i : 0u;
 }
 
+#ifndef FJG_GJ_WARPSEARCH
+#define FJG_GJ_WARPSEARCH 0
+#endif
+#ifndef FJG_GJ_PREFETCH
+#define FJG_GJ_PREFETCH 1
+#endif
 // Fast path for the Generic-Join-shaped aggregating last node: every subatom
 // is a cover over the same single new variable x (triangle C2/C5, 4-clique
 // C4). Per candidate: binding lookup, one coalesced cover read, NS-1 bucket
@@ -865,9 +871,23 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
     const uint64_t t = (base - c0) / TILE;
     const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
     const uint64_t i = base + threadIdx.x;
+    // binding of candidate i: the tile's bindings [lo, hi] are usually few, so
+    // the warp loads their scan values in one coalesced load and each lane
+    // counts the ones <= i with shuffles; long spans fall back to a search.
+    uint64_t e, j;
+    if (FJG_GJ_WARPSEARCH && hi - lo < 32) {
+      const uint32_t span = (uint32_t)(hi - lo) + 1;
+      const uint64_t sv = lane < (int)span ? __ldg(scan + lo + lane) : ~0ull;
+      uint32_t k = 0;
+      for (uint32_t u = 0; u < span; ++u) k += __shfl_sync(0xffffffffu, sv, u) <= i ? 1u : 0u;
+      const uint64_t prev = __shfl_sync(0xffffffffu, sv, k > 0 ? k - 1 : 0);
+      e = lo + k;
+      j = i - (k > 0 ? prev : (lo ? __ldg(scan + lo - 1) : 0ull));
+    } else {
+      e = i < c1 ? upper_bound_u64(scan, lo, hi, i) : lo;
+      j = i - (e ? __ldg(scan + e - 1) : 0ull);
+    }
     if (i >= c1) continue;
-    const uint64_t e = upper_bound_u64(scan, lo, hi, i);
-    const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
     const int ci = N.chosen[e];
     uint32_t sp[NS], sl[NS];
 #pragma unroll
@@ -882,6 +902,9 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
       }
     }
     uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+    int32_t hv[W];  // bound head variables, prefetched off the critical path
+#pragma unroll
+    for (int v = 0; v < W; ++v) hv[v] = (FJG_GJ_PREFETCH && v < N.nhead && v != xvar) ? __ldg(N.in_var[v] + e) : 0;
     uint32_t cpos = 0;
     const int32_t* csrc = nullptr;
 #pragma unroll
@@ -928,7 +951,7 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
 #pragma unroll
     for (int v = 0; v < W; ++v)
       if (v < N.nhead) {
-        const int32_t val = (v == xvar) ? x : __ldg(N.in_var[v] + e);
+        const int32_t val = (v == xvar) ? x : (FJG_GJ_PREFETCH ? hv[v] : __ldg(N.in_var[v] + e));
         h = fj::tuple_hash_step(h, (int64_t)val);
         if (v == min_var) acc_min = min(acc_min, (long long)val);
       }
