@@ -991,6 +991,177 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
   }
 }
 
+// ILP variant of k_last_gj for the common case where the new variable x is the
+// last head variable (so the tuple hash is step(prefix(binding), x)): each
+// thread owns a run of R consecutive candidates, split at binding
+// boundaries; inside a run the binding state is loaded once and the R cover
+// reads and R first-bucket probes are issued back to back.
+template <int NS, int R, int W>
+__global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                      uint64_t F, const uint64_t* __restrict__ bounds,
+                                                      int min_var, DevCounters* ctr) {
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const uint64_t* __restrict__ scan = N.scan;
+  const int nhead = N.nhead;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * R; base < c1; base += (uint64_t)gridDim.x * TILE * R) {
+    uint64_t i = base + (uint64_t)threadIdx.x * R;
+    const uint64_t iend = min(i + R, c1);
+    if (i >= iend) continue;
+    const uint64_t t = (i - c0) / TILE;
+    uint64_t e = upper_bound_u64(scan, __ldg(bounds + t), __ldg(bounds + t + 1), i);
+    while (i < iend) {
+      const uint64_t se = __ldg(scan + e);
+      const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
+      const uint64_t bend = min(iend, se);  // this batch: candidates [i, bend) of binding e
+      // binding state
+      const int ci = N.chosen[e];
+      uint32_t sp[NS], sl[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const KSub& P = N.sub[s];
+        if (P.in_p) {
+          sp[s] = __ldg(P.in_p + e);
+          sl[s] = __ldg(P.in_len + e);
+        } else {
+          sp[s] = 0;
+          sl[s] = P.root_n;
+        }
+      }
+      const uint64_t mult0 = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+      uint64_t pre = fj::kTupleHashSeed;
+      long long bmin = LLONG_MAX;
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if (v < nhead - 1) {
+          const int32_t hvv = __ldg(N.in_var[v] + e);
+          pre = fj::tuple_hash_step(pre, (int64_t)hvv);
+          if (v == min_var) bmin = hvv;
+        }
+      uint32_t cbase = 0;
+      const int32_t* csrc = nullptr;
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (s == ci) {
+          cbase = sp[s] + (uint32_t)(i - prev);
+          csrc = N.sub[s].src[0];
+        }
+      // R cover reads
+      int32_t x[R];
+      bool live[R];
+      uint64_t mu[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        live[r] = i + r < bend;
+        x[r] = live[r] ? __ldg(csrc + cbase + r) : 0;
+        mu[r] = mult0;
+        if (live[r]) ++body;
+      }
+      // probes, R first buckets in flight per subatom
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s == ci) continue;
+        const KSub& P = N.sub[s];
+        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+        uint4 h0[R];
+        uint64_t b0[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          b0[r] = region_bucket(sp[s], sl[s], (uint32_t)x[r]);
+          h0[r] = live[r] ? __ldg(tb + 2 * b0[r]) : make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!live[r]) continue;
+          ++probes;
+          const uint32_t kw = (uint32_t)x[r];
+          uint32_t q = kEmpty;
+          bool more = false;
+          if (h0[r].y == kEmpty) {
+          } else if (h0[r].x == kw) {
+            q = h0[r].y;
+          } else if (h0[r].w == kEmpty) {
+          } else if (h0[r].z == kw) {
+            q = h0[r].w;
+          } else {
+            more = true;
+          }
+          if (more) {  // rest of the bucket, then the following buckets
+            uint64_t b = b0[r];
+            uint4 h1 = __ldg(tb + 2 * b + 1);
+            while (true) {
+              if (h1.y == kEmpty) break;
+              if (h1.x == kw) { q = h1.y; break; }
+              if (h1.w == kEmpty) break;
+              if (h1.z == kw) { q = h1.w; break; }
+              if (++b == bhi) b = blo;
+              const uint4 a0 = __ldg(tb + 2 * b);
+              if (a0.y == kEmpty) break;
+              if (a0.x == kw) { q = a0.y; break; }
+              if (a0.w == kEmpty) break;
+              if (a0.z == kw) { q = a0.w; break; }
+              h1 = __ldg(tb + 2 * b + 1);
+            }
+          }
+          if (q == kEmpty) {
+            ++misses;
+            live[r] = false;
+          } else if (P.last) {
+            mu[r] *= __ldg(P.cnt + q);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!live[r]) continue;
+        const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x[r]);
+        acc_sum += mu[r] * fj::checksum_word(h);
+        acc_lo += mu[r];
+        if (acc_lo < mu[r]) ++acc_hi;
+        if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x[r] : bmin);
+      }
+      i = bend;
+      ++e;
+    }
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  uint64_t lo2 = acc_lo, hi2 = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
+    const uint64_t sm = lo2 + l2;
+    hi2 += h2 + (sm < lo2 ? 1 : 0);
+    lo2 = sm;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (lo2) {
+      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
+      if (old + lo2 < old) ++hi2;
+    }
+    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
+    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+  }
+}
+
+#ifndef FJG_GJ_R
+#define FJG_GJ_R 2
+#endif
+
 // The GJ fast path applies when every subatom of the node is a one-variable
 // cover of the same new, unbound variable, and no subtrie can be a streamed
 // singleton (all subatoms keys-or-stream levels of depth >= 0 with nv == 1).
@@ -1817,7 +1988,23 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       else if (mode == EXPAND_MEMO)
         LAUNCH(eng, launch_expand<EXPAND_MEMO>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
                                                q->d_ctr));
-      else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT) {
+      else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
+               FJG_GJ_R > 1) {
+        const int W8 = q->head.size() <= 4 ? 4 : 8;
+        const unsigned gi = grid_for(c1 - c0, TILE * FJG_GJ_R, eng->num_sms * 8);
+        if (N.nsub == 2 && W8 == 4)
+          LAUNCH(eng, (k_last_gj_ilp<2, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
+                                                                                 q->min_var, q->d_ctr)));
+        else if (N.nsub == 2)
+          LAUNCH(eng, (k_last_gj_ilp<2, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
+                                                                                 q->min_var, q->d_ctr)));
+        else if (W8 == 4)
+          LAUNCH(eng, (k_last_gj_ilp<3, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
+                                                                                 q->min_var, q->d_ctr)));
+        else
+          LAUNCH(eng, (k_last_gj_ilp<3, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
+                                                                                 q->min_var, q->d_ctr)));
+      } else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT) {
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const int ns = N.nsub;
         if (ns == 2 && W8 == 4)
