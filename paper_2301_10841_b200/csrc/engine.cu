@@ -1161,6 +1161,171 @@ __global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KN
 #ifndef FJG_GJ_R
 #define FJG_GJ_R 2
 #endif
+#ifndef FJG_GJ_WRITE
+#define FJG_GJ_WRITE 1
+#endif
+
+// GJ-shaped frontier-writing node: every subatom is a one-variable cover of the
+// new variable x; atoms whose subatom is not their last continue with the
+// child of their cover (keys mode) or probe (q, cnt[q]). Survivors are
+// block-compacted into the next frontier.
+template <int NS, int W>
+__global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                   uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
+                                                   DevCounters* ctr) {
+  __shared__ uint32_t s_warp[TILE / 32];
+  __shared__ uint32_t s_base;
+  uint64_t probes = 0, misses = 0, body = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t* __restrict__ scan = N.scan;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    const uint64_t i = base + threadIdx.x;
+    bool alive = i < c1;
+    uint64_t e = 0, mult = 1;
+    int32_t x = 0;
+    uint32_t chp[NS], chl[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) chp[s] = chl[s] = 0;
+    if (alive) {
+      e = upper_bound_u64(scan, lo, hi, i);
+      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+      const int ci = N.chosen[e];
+      uint32_t sp[NS], sl[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const KSub& P = N.sub[s];
+        if (P.in_p) {
+          sp[s] = __ldg(P.in_p + e);
+          sl[s] = __ldg(P.in_len + e);
+        } else {
+          sp[s] = 0;
+          sl[s] = P.root_n;
+        }
+      }
+      if (N.in_mult) mult = __ldg(N.in_mult + e);
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (s == ci) {
+          const KSub& S = N.sub[s];
+          const uint32_t pos = sp[s] + (uint32_t)j;
+          if (!S.stream) {  // forced map: distinct keys are the child starts
+            const uint32_t c = __ldg(S.cnt + pos);
+            if (c == 0) alive = false;
+            chp[s] = pos;
+            chl[s] = c;
+          } else {
+            chp[s] = kSingleton;
+            chl[s] = 1;
+          }
+          if (alive) x = __ldg(S.src[0] + pos);
+        }
+      if (alive) ++body;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s == ci || !alive) continue;
+        const KSub& P = N.sub[s];
+        ++probes;
+        const uint32_t kw = (uint32_t)x;
+        uint64_t b = region_bucket(sp[s], sl[s], kw);
+        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+        uint32_t q = kEmpty;
+        while (true) {
+          const uint4 h0 = __ldg(tb + 2 * b);
+          if (h0.y == kEmpty) break;
+          if (h0.x == kw) { q = h0.y; break; }
+          if (h0.w == kEmpty) break;
+          if (h0.z == kw) { q = h0.w; break; }
+          const uint4 h1 = __ldg(tb + 2 * b + 1);
+          if (h1.y == kEmpty) break;
+          if (h1.x == kw) { q = h1.y; break; }
+          if (h1.w == kEmpty) break;
+          if (h1.z == kw) { q = h1.w; break; }
+          if (++b == bhi) b = blo;
+        }
+        if (q == kEmpty) {
+          ++misses;
+          alive = false;
+        } else {
+          const uint32_t ql = __ldg(P.cnt + q);
+          if (P.last)
+            mult *= ql;
+          else {
+            chp[s] = q;
+            chl[s] = ql;
+          }
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, alive);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < TILE / 32; ++w) {
+        const uint32_t c = s_warp[w];
+        s_warp[w] = tot;
+        tot += c;
+      }
+      s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
+    }
+    __syncthreads();
+    if (alive) {
+      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if ((N.out_vars >> v) & 1u) N.out_var[v][o] = (v == xvar) ? x : __ldg(N.in_var[v] + e);
+#pragma unroll
+      for (int a = 0; a < W; ++a)
+        if ((N.out_atoms >> a) & 1u) {
+          uint32_t pa = 0, la = 0;
+          bool here = false;
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            if (N.sub[s].atom == a) {
+              pa = chp[s];
+              la = chl[s];
+              here = true;
+            }
+          if (!here) {
+            pa = __ldg(N.in_p[a] + e);
+            la = __ldg(N.in_len[a] + e);
+          }
+          N.out_p[a][o] = pa;
+          N.out_len[a][o] = la;
+        }
+      if (N.out_mult) N.out_mult[o] = mult;
+    }
+    __syncthreads();
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+  }
+}
+
+// A frontier-writing node is GJ-shaped when every subatom is a one-variable
+// cover of the same fresh variable (levels of depth >= 0, no bound check).
+static int gj_write_var(const DevNode& N, int width) {
+  if (N.nsub < 2 || N.nsub > 3 || N.ncov != N.nsub || width > 8) return -1;
+  int x = -1;
+  for (int s = 0; s < N.nsub; ++s) {
+    const DevSub& D = N.sub[s];
+    if (D.nv != 1 || D.bound_mask) return -1;
+    if (x >= 0 && D.var[0] != x) return -1;
+    x = D.var[0];
+  }
+  return x;
+}
 
 // The GJ fast path applies when every subatom of the node is a one-variable
 // cover of the same new, unbound variable, and no subtrie can be a streamed
@@ -1420,6 +1585,7 @@ struct fjg_query {
   KNode memo_top{};                     // node k*-1 aggregating mult * memo[child]
   int stop_node = -1;
   int gj_x[MAXN];  // per node: the GJ fast-path variable, or -1
+  int gj_w[MAXN];  // per node: the GJ frontier-writing fast-path variable, or -1
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   // non-blocking phase timer: event pairs resolved after the final sync
@@ -1648,6 +1814,7 @@ static void prepare_query(fjg_query* q) {
 
 // Resolve each node's descriptor into the constant-bank kernel plan.
 static int gj_last_var(const KNode& G, const DevNode& N);
+static int gj_write_var(const DevNode& N, int width);
 
 static void build_knodes(fjg_query* q) {
   const size_t K = q->nodes.size();
@@ -1709,7 +1876,10 @@ static void build_knodes(fjg_query* q) {
       S.depth = (uint8_t)D.depth;
     }
   }
-  for (size_t k = 0; k < K && k < (size_t)MAXN; ++k) q->gj_x[k] = gj_last_var(q->knodes[k], q->nodes[k]);
+  for (size_t k = 0; k < K && k < (size_t)MAXN; ++k) {
+    q->gj_x[k] = gj_last_var(q->knodes[k], q->nodes[k]);
+    q->gj_w[k] = gj_write_var(q->nodes[k], q->width);
+  }
 }
 
 // Chain-suffix analysis for the memoised factorised count (mirrors the
@@ -2034,8 +2204,21 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     q->mark(eng->stream, -1);
     const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
     LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
-    LAUNCH(eng, launch_expand<EXPAND_WRITE>(q->width, grid_for(c1 - c0, TILE, eng->num_sms * 8), eng->stream, KN,
-                                            c0, c1, F, q->bounds, -1, nullptr, 0, q->d_ctr));
+    const unsigned gw = grid_for(c1 - c0, TILE, eng->num_sms * 8);
+    if (q->gj_w[k] >= 0 && FJG_GJ_WRITE) {
+      const int w8 = q->width <= 4 ? 4 : 8;
+      if (N.nsub == 2 && w8 == 4)
+        LAUNCH(eng, (k_write_gj<2, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+      else if (N.nsub == 2)
+        LAUNCH(eng, (k_write_gj<2, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+      else if (w8 == 4)
+        LAUNCH(eng, (k_write_gj<3, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+      else
+        LAUNCH(eng, (k_write_gj<3, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+    } else {
+      LAUNCH(eng, launch_expand<EXPAND_WRITE>(q->width, gw, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
+                                              q->d_ctr));
+    }
     q->mark(eng->stream, 1);
     sync_counters(q);
     run_node(q, k + 1, q->h_ctr->survivors, mode);
