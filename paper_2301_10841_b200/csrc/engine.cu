@@ -240,6 +240,7 @@ struct ForceRange {
   const uint32_t* list_len;
   const uint32_t* list_scan;   // inclusive
   const uint32_t* list_count;  // device count
+  const uint32_t* owner;       // list entry of every forced offset index (max-scan of start markers)
   uint32_t p0, len0;
   int single;
 };
@@ -258,18 +259,19 @@ __device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, ui
     pos = R.p0 + i;
     return;
   }
-  uint32_t lo = 0, hi = *R.list_count - 1;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (R.list_scan[mid] > i)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
+  const uint32_t lo = __ldg(R.owner + i);
   const uint32_t before = lo ? R.list_scan[lo - 1] : 0u;
   p = R.list_p[lo];
   len = R.list_len[lo];
   pos = p + (i - before);
+}
+
+// owner map, pass 1: mark the first offset index of every listed subtrie
+__global__ void k_force_marks(const uint32_t* __restrict__ list_scan, const uint32_t* __restrict__ list_count,
+                              uint32_t* __restrict__ marks) {
+  const uint32_t c = *list_count;
+  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < c; li += gridDim.x * blockDim.x)
+    marks[li ? list_scan[li - 1] : 0u] = li;
 }
 
 // clear the slot regions (one 4-slot bucket per position) and child counts of
@@ -1565,6 +1567,7 @@ struct fjg_query {
   uint32_t* tmp_rank = nullptr;
   uint32_t* newslots = nullptr;
   uint32_t* newslot_p = nullptr;
+  uint32_t* owner_scratch = nullptr;  // force: offset index -> claimed subtrie
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
   int32_t* out_tuples = nullptr;
@@ -1747,6 +1750,7 @@ static void prepare_query(fjg_query* q) {
   q->tmp_rank = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->newslots = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->newslot_p = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  q->owner_scratch = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   if (q->max_n >= (1ull << 31)) throw ValidationError("relations must have fewer than 2^31 rows");
   // static node descriptors
   const size_t K = plan.nodes.size();
@@ -2020,7 +2024,10 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   CK(cub::DeviceScan::InclusiveSum(nullptr, b1, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)cap));
   CK(cub::DeviceScan::InclusiveSum(nullptr, b2, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                    (int64_t)std::max<uint64_t>(q->max_n, 1)));
-  size_t need = std::max(b1, b2);
+  size_t b3 = 0;
+  CK(cub::DeviceScan::InclusiveScan(nullptr, b3, (uint32_t*)nullptr, (uint32_t*)nullptr, MaxOp(),
+                                    (int64_t)std::max<uint64_t>(q->max_n, 1)));
+  size_t need = std::max(std::max(b1, b2), b3);
   if (need > q->cub_tmp_bytes) {
     q->cub_tmp = q->alloc(need);
     q->cub_tmp_bytes = need;
@@ -2062,6 +2069,15 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, L.list_len, L.list_scan, (int64_t)count, eng->stream));
     ++eng->launches;
     upper = T.rel->nrows;
+    // offset index -> list entry: marks at each entry's first index, then a max-scan
+    CK(cudaMemsetAsync(q->owner_scratch, 0, std::max<uint64_t>(upper, 1) * 4, eng->stream));
+    LAUNCH(eng, k_force_marks<<<grid_for(count), 256, 0, eng->stream>>>(L.list_scan, R.list_count,
+                                                                         q->owner_scratch));
+    bytes = q->cub_tmp_bytes;
+    CK(cub::DeviceScan::InclusiveScan(q->cub_tmp, bytes, q->owner_scratch, q->owner_scratch, MaxOp(),
+                                      (int64_t)upper, eng->stream));
+    ++eng->launches;
+    R.owner = q->owner_scratch;
   }
   q->mark(eng->stream, -1);
   if (single) {
