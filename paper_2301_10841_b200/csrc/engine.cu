@@ -1166,6 +1166,9 @@ __global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KN
 #ifndef FJG_GJ_WRITE
 #define FJG_GJ_WRITE 1
 #endif
+#ifndef FJG_STREAM_WRITE
+#define FJG_STREAM_WRITE 1
+#endif
 
 // GJ-shaped frontier-writing node: every subatom is a one-variable cover of the
 // new variable x; atoms whose subatom is not their last continue with the
@@ -1313,6 +1316,191 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
     if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
     if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
   }
+}
+
+// Binary-join-pipeline node (frontier-writing): one cover iterated in stream
+// mode, every other subatom a single-variable probe keyed on a variable the
+// cover binds (C1 chain, C3 star node 0). Cover columns are loaded lazily, in
+// probe order, so a candidate that dies at its first probe reads one column.
+template <int W>
+__global__ void __launch_bounds__(TILE) k_write_stream(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                       uint64_t F, const uint64_t* __restrict__ bounds,
+                                                       DevCounters* ctr) {
+  __shared__ uint32_t s_warp[TILE / 32];
+  __shared__ uint32_t s_base;
+  uint64_t probes = 0, misses = 0, body = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t* __restrict__ scan = N.scan;
+  const int ci = N.cov[0];
+  const KSub& S = N.sub[ci];
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    const uint64_t i = base + threadIdx.x;
+    bool alive = i < c1;
+    uint64_t e = 0, mult = 1;
+    uint32_t pos = 0;
+    int32_t xv[MAXK];
+    uint32_t have = 0;  // bit t: cover column t loaded
+    uint32_t chp[MAXS], chl[MAXS];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) xv[k] = 0;
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) chp[s] = chl[s] = 0;
+    if (alive) {
+      e = upper_bound_u64(scan, lo, hi, i);
+      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+      uint32_t p;
+      if (S.in_p) {
+        p = __ldg(S.in_p + e);
+      } else {
+        p = 0;
+      }
+      pos = p + (uint32_t)j;
+      if (N.in_mult) mult = __ldg(N.in_mult + e);
+      ++body;
+#pragma unroll
+      for (int s = 0; s < MAXS; ++s) {
+        if (s >= N.nsub || s == ci || !alive) continue;
+        const KSub& P = N.sub[s];
+        // key: the cover column bound to P's variable (loaded on first use)
+        int tk = 0;
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k < S.nv && S.var[k] == P.var[0]) tk = k;
+        int32_t key = 0;
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k == tk) {
+            if (!((have >> k) & 1u)) {
+              xv[k] = __ldg(S.src[k] + pos);
+              have |= 1u << k;
+            }
+            key = xv[k];
+          }
+        uint32_t pp, pl;
+        if (P.in_p) {
+          pp = __ldg(P.in_p + e);
+          pl = __ldg(P.in_len + e);
+        } else {
+          pp = 0;
+          pl = P.root_n;
+        }
+        ++probes;
+        const uint32_t kw = (uint32_t)key;
+        uint64_t b = region_bucket(pp, pl, kw);
+        const uint64_t blo = pp, bhi = (uint64_t)pp + pl;
+        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+        uint32_t q = kEmpty;
+        while (true) {
+          const uint4 h0 = __ldg(tb + 2 * b);
+          if (h0.y == kEmpty) break;
+          if (h0.x == kw) { q = h0.y; break; }
+          if (h0.w == kEmpty) break;
+          if (h0.z == kw) { q = h0.w; break; }
+          const uint4 h1 = __ldg(tb + 2 * b + 1);
+          if (h1.y == kEmpty) break;
+          if (h1.x == kw) { q = h1.y; break; }
+          if (h1.w == kEmpty) break;
+          if (h1.z == kw) { q = h1.w; break; }
+          if (++b == bhi) b = blo;
+        }
+        if (q == kEmpty) {
+          ++misses;
+          alive = false;
+        } else {
+          const uint32_t ql = __ldg(P.cnt + q);
+          if (P.last)
+            mult *= ql;
+          else {
+            chp[s] = q;
+            chl[s] = ql;
+          }
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, alive);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < TILE / 32; ++w) {
+        const uint32_t c = s_warp[w];
+        s_warp[w] = tot;
+        tot += c;
+      }
+      s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
+    }
+    __syncthreads();
+    if (alive) {
+      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if ((N.out_vars >> v) & 1u) {
+          int32_t val = 0;
+          bool cov = false;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            if (k < S.nv && S.var[k] == v) {
+              val = ((have >> k) & 1u) ? xv[k] : __ldg(S.src[k] + pos);
+              cov = true;
+            }
+          N.out_var[v][o] = cov ? val : __ldg(N.in_var[v] + e);
+        }
+#pragma unroll
+      for (int a = 0; a < W; ++a)
+        if ((N.out_atoms >> a) & 1u) {
+          uint32_t pa = 0, la = 0;
+          bool here = false;
+#pragma unroll
+          for (int s = 0; s < MAXS; ++s)
+            if (s < N.nsub && N.sub[s].atom == a) {
+              pa = s == ci ? kSingleton : chp[s];
+              la = s == ci ? 1u : chl[s];
+              here = true;
+            }
+          if (!here) {
+            pa = __ldg(N.in_p[a] + e);
+            la = __ldg(N.in_len[a] + e);
+          }
+          N.out_p[a][o] = pa;
+          N.out_len[a][o] = la;
+        }
+      if (N.out_mult) N.out_mult[o] = mult;
+    }
+    __syncthreads();
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+  }
+}
+
+// The stream fast path: a single cover in stream mode whose subtrie is never a
+// singleton, all its variables fresh; every other subatom probes one variable
+// the cover binds.
+static bool stream_write_ok(const DevNode& N, const KNode& G) {
+  if (N.ncov != 1 || N.nsub < 2) return false;
+  const DevSub& C = N.sub[N.cov[0]];
+  if (!C.stream || C.bound_mask || C.nv < 1) return false;
+  if (G.sub[N.cov[0]].in_p == nullptr && C.depth != 0) return false;
+  for (int s = 0; s < N.nsub; ++s) {
+    if (s == N.cov[0]) continue;
+    const DevSub& P = N.sub[s];
+    if (P.nv != 1) return false;
+    bool found = false;
+    for (int t = 0; t < C.nv; ++t)
+      if (C.var[t] == P.var[0]) found = true;
+    if (!found) return false;
+  }
+  return true;
 }
 
 // A frontier-writing node is GJ-shaped when every subatom is a one-variable
@@ -1589,6 +1777,7 @@ struct fjg_query {
   int stop_node = -1;
   int gj_x[MAXN];  // per node: the GJ fast-path variable, or -1
   int gj_w[MAXN];  // per node: the GJ frontier-writing fast-path variable, or -1
+  bool sw[MAXN];   // per node: the stream-cover frontier-writing fast path applies
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   // non-blocking phase timer: event pairs resolved after the final sync
@@ -1819,6 +2008,7 @@ static void prepare_query(fjg_query* q) {
 // Resolve each node's descriptor into the constant-bank kernel plan.
 static int gj_last_var(const KNode& G, const DevNode& N);
 static int gj_write_var(const DevNode& N, int width);
+static bool stream_write_ok(const DevNode& N, const KNode& G);
 
 static void build_knodes(fjg_query* q) {
   const size_t K = q->nodes.size();
@@ -1883,6 +2073,7 @@ static void build_knodes(fjg_query* q) {
   for (size_t k = 0; k < K && k < (size_t)MAXN; ++k) {
     q->gj_x[k] = gj_last_var(q->knodes[k], q->nodes[k]);
     q->gj_w[k] = gj_write_var(q->nodes[k], q->width);
+    q->sw[k] = stream_write_ok(q->nodes[k], q->knodes[k]);
   }
 }
 
@@ -2231,6 +2422,13 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
         LAUNCH(eng, (k_write_gj<3, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
       else
         LAUNCH(eng, (k_write_gj<3, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+    } else if (q->sw[k] && FJG_STREAM_WRITE) {
+      if (q->width <= 4)
+        LAUNCH(eng, (k_write_stream<4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->d_ctr)));
+      else if (q->width <= 8)
+        LAUNCH(eng, (k_write_stream<8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->d_ctr)));
+      else
+        LAUNCH(eng, (k_write_stream<16><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->d_ctr)));
     } else {
       LAUNCH(eng, launch_expand<EXPAND_WRITE>(q->width, gw, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
                                               q->d_ctr));
@@ -2578,7 +2776,7 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     o.min_var = -1;
     if (opts) o = *opts;
     if (o.min_var >= (int)q->head.size()) throw fj::ValidationError("min_var out of range");
-    uint64_t batch = o.batch_size ? o.batch_size : (1ull << 24);
+    uint64_t batch = o.batch_size ? o.batch_size : (1ull << 25);
     ensure_frontiers(q, batch);
     q->dynamic = o.dynamic_cover != 0;
     q->timing = o.collect_timing != 0;
