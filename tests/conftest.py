@@ -9,7 +9,10 @@ if ROOT not in sys.path:
 
 
 def _ensure_built():
-    from paper_2301_10841_b200 import build as B
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fjg_build", os.path.join(ROOT, "paper_2301_10841_b200", "build.py"))
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
     need = [B.LIBFJG, B.LIBFJGEN, B.LIBORACLE]
     if not all(os.path.exists(p) for p in need):
         B.build_all()
