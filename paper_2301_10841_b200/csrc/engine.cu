@@ -62,1478 +62,12 @@ static void throw_cuda(cudaError_t e, const char* what, int line) {
     if (_e != cudaSuccess) throw_cuda(_e, #x, __LINE__); \
   } while (0)
 
-// ============================================================================
-// device helpers
-// ============================================================================
-__device__ __forceinline__ const int32_t* level_src(const DevTrie& T, int depth, int col) {
-  return depth == 0 ? T.base[col] : T.lev[depth - 1].cval[col];
-}
-
-template <int N>
-__device__ __forceinline__ uint32_t key_word_r(int nk, const int32_t (&vals)[N]) {
-  if (nk == 0) return 0u;
-  if (nk == 1) return static_cast<uint32_t>(vals[0]);
-  uint64_t h = fj::kTupleHashSeed;
-#pragma unroll
-  for (int t = 0; t < N; ++t)
-    if (t < nk) h = fj::tuple_hash_step(h, vals[t]);
-  return static_cast<uint32_t>(fj::fmix64(h));
-}
-
-// first bucket (4 slots) of key word kw inside the region of subtrie (p, len)
-__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
-  h ^= h >> 16;
-  h *= 0x85ebca6bu;
-  h ^= h >> 13;
-  h *= 0xc2b2ae35u;
-  h ^= h >> 16;
-  return h;
-}
-__device__ __forceinline__ uint64_t region_bucket(uint32_t p, uint32_t len, uint32_t kw) {
-  return (uint64_t)p + (((uint64_t)fmix32(kw ^ 0x9e3779b9u) * len) >> 32);
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// COLT get (Fig 12 `get` = force, then lookup): the subtrie was forced by an
-// earlier kernel of this node, so this is a pure lookup in its slot region:
-// read a bucket (one sector, as two 16-byte halves), stop at a match or at the
-// first free slot.
-__device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len, const int32_t (&key)[MAXK],
-                                         uint32_t& q, uint32_t& ql) {
-  const int nk = P.nv;
-  const uint32_t kw = key_word_r(nk, key);
-  uint64_t b = region_bucket(p, len, kw);
-  const uint64_t blo = p, bhi = (uint64_t)p + len;
-  const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-  while (true) {
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint4 s = __ldg(tb + 2 * b + half);
-      // slot (s.x, s.y) then (s.z, s.w)
-#pragma unroll
-      for (int w = 0; w < 2; ++w) {
-        const uint32_t sk = w ? s.z : s.x, sq = w ? s.w : s.y;
-        if (sq == kEmpty) return false;
-        if (sk == kw) {
-          bool eq = true;
-          if (nk >= 2) {
-#pragma unroll
-            for (int t = 0; t < MAXK; ++t)
-              if (t < nk && __ldg(P.kcmp[t] + sq) != key[t]) eq = false;
-          }
-          if (eq) {
-            q = sq;
-            ql = __ldg(P.cnt + sq);
-            return true;
-          }
-        }
-      }
-    }
-    if (++b == bhi) b = blo;
-  }
-}
-
-__device__ __forceinline__ void subtrie_of(const KSub& S, uint64_t e, uint32_t& p, uint32_t& len) {
-  if (S.in_p) {
-    p = __ldg(S.in_p + e);
-    len = __ldg(S.in_len + e);
-  } else {
-    p = 0;
-    len = S.root_n;
-  }
-}
-
-// estimated_key_count: forced map -> #keys, vector -> its
-// length, BaseScan -> cardinality. Never forces.
-__device__ __forceinline__ uint64_t estimate(const KSub& S, uint32_t p, uint32_t len) {
-  if (p == kSingleton) return 1;
-  const uint32_t id = S.depth == 0 ? 0u : p;
-  if (*((volatile const uint32_t*)(S.state + id)) == 2u) return S.nkeys[id];
-  return len;
-}
-
-// ============================================================================
-// k_select: cover choice, candidate counts, force claims
-// ============================================================================
-__device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters* ctr, const KSub& S, uint32_t p,
-                                              uint32_t len, bool need) {
-  // Warp-level dedup of identical subtries (bindings of one parent are
-  // adjacent in the frontier), then a CAS on the state word.
-  const unsigned act = __activemask();
-  const unsigned want = __ballot_sync(act, need);
-  if (!need) return;
-  const unsigned grp = __match_any_sync(want, p);
-  const int leader = __ffs(grp) - 1;
-  if ((int)(threadIdx.x & 31) != leader) return;
-  if (S.depth == 0) {
-    ctr->root_need[S.trie] = 1;
-    return;
-  }
-  const DevLevel& L = tries[S.trie].lev[S.depth];
-  if (atomicCAS(L.state + p, 0u, 1u) == 0u) {
-    L.cursor[p] = 0;
-    L.nkeys[p] = 0;
-    const uint32_t idx = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], 1u);
-    L.list_p[idx] = p;
-    L.list_len[idx] = len;
-  }
-}
-
-__global__ void k_select(const __grid_constant__ KNode N, const DevTrie* __restrict__ tries, uint64_t F,
-                         int dynamic, DevCounters* ctr) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t iters = (F + stride - 1) / stride;
-  for (uint64_t it = 0; it < iters; ++it) {
-    const uint64_t e = start + it * stride;
-    const bool ok = e < F;
-    int best = N.cov[0];
-    uint32_t bp = 0, bl = 0;
-    if (ok) {
-      subtrie_of(N.sub[best], e, bp, bl);
-      if (dynamic && N.ncov > 1) {
-        uint64_t best_est = estimate(N.sub[best], bp, bl);
-        for (int ci = 1; ci < N.ncov; ++ci) {
-          const int s = N.cov[ci];
-          uint32_t p, l;
-          subtrie_of(N.sub[s], e, p, l);
-          const uint64_t est = estimate(N.sub[s], p, l);
-          if (est < best_est) {  // ties keep the lowest position
-            best_est = est;
-            best = s;
-            bp = p;
-            bl = l;
-          }
-        }
-      }
-      N.chosen[e] = (uint8_t)best;
-      N.m[e] = (bp == kSingleton) ? 1ull : (uint64_t)bl;
-    }
-    // claims: the keys-iterated cover and every probed subatom must be forced
-    for (int s = 0; s < N.nsub; ++s) {
-      const KSub& S = N.sub[s];
-      uint32_t p = 0, l = 0;
-      bool need = false;
-      if (ok) {
-        subtrie_of(S, e, p, l);
-        need = (p != kSingleton) && (s != best || !S.stream);
-        if (need) need = *((volatile const uint32_t*)(S.state + (S.depth == 0 ? 0u : p))) == 0u;
-      }
-      claim_subtrie(tries, ctr, S, p, l, need);
-    }
-  }
-}
-
-// ============================================================================
-// force: clear -> insert -> assign -> scatter -> finalize  (Fig 12 `force`)
-// ============================================================================
-// Position iteration over the union of claimed ranges. single: one subtrie
-// (p0, len0) given by value (the root BaseScan).
-struct ForceRange {
-  const uint32_t* list_p;
-  const uint32_t* list_len;
-  const uint32_t* list_scan;   // inclusive
-  const uint32_t* list_count;  // device count
-  const uint32_t* owner;       // list entry of every forced offset index (max-scan of start markers)
-  uint32_t p0, len0;
-  int single;
-};
-
-__device__ __forceinline__ uint32_t force_total(const ForceRange& R) {
-  if (R.single) return R.len0;
-  const uint32_t c = *R.list_count;
-  return c ? R.list_scan[c - 1] : 0u;
-}
-
-__device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, uint32_t& p, uint32_t& len,
-                                             uint32_t& pos) {
-  if (R.single) {
-    p = R.p0;
-    len = R.len0;
-    pos = R.p0 + i;
-    return;
-  }
-  const uint32_t lo = __ldg(R.owner + i);
-  const uint32_t before = lo ? R.list_scan[lo - 1] : 0u;
-  p = R.list_p[lo];
-  len = R.list_len[lo];
-  pos = p + (i - before);
-}
-
-// owner map, pass 1: mark the first offset index of every listed subtrie
-__global__ void k_force_marks(const uint32_t* __restrict__ list_scan, const uint32_t* __restrict__ list_count,
-                              uint32_t* __restrict__ marks) {
-  const uint32_t c = *list_count;
-  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < c; li += gridDim.x * blockDim.x)
-    marks[li ? list_scan[li - 1] : 0u] = li;
-}
-
-// clear the slot regions (one 4-slot bucket per position) and child counts of
-// the claimed subtries
-__global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
-  const DevLevel& L = tries[trie].lev[lev];
-  const uint32_t total = force_total(R);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t p, len, pos;
-    force_locate(R, i, p, len, pos);
-    uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * pos;
-    t[0] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    t[1] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    L.cnt[pos] = 0;
-    if (L.srep) reinterpret_cast<uint4*>(L.srep)[pos] = make_uint4(0u, 0u, 0u, 0u);
-  }
-}
-
-// Insert every offset of the claimed subtries: claim a slot for its key (CAS
-// on the 8-byte slot), then count it (the pending slot's q word is the group
-// counter; the returned value is the offset's rank inside its child group).
-template <bool MULTI>
-__global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
-                               uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
-                               uint32_t* __restrict__ newslots, uint32_t* __restrict__ newslot_p,
-                               DevCounters* ctr) {
-  const DevTrie& T = tries[trie];
-  const DevLevel& L = T.lev[lev];
-  const uint32_t total = force_total(R);
-  const int nk = L.nk;
-  const int32_t* src[MAXK];
-#pragma unroll
-  for (int t = 0; t < MAXK; ++t) src[t] = t < nk ? level_src(T, lev, L.keycol[t]) : nullptr;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t p, len, pos;
-    force_locate(R, i, p, len, pos);
-    int32_t vals[MAXK];
-#pragma unroll
-    for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
-    const uint32_t kw = key_word_r(nk, vals);
-    const unsigned long long mine = ((unsigned long long)kPendBit << 32) | kw;
-    const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
-    uint64_t h = 4ull * region_bucket(p, len, kw);
-    bool won = false;
-    while (true) {
-      unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
-      unsigned long long cur = *((volatile unsigned long long*)addr);
-      if ((uint32_t)(cur >> 32) == kEmpty) {
-        const unsigned long long old = atomicCAS(addr, cur, mine);
-        if (old == cur) {
-          won = true;
-          if (MULTI) {
-            *((volatile uint32_t*)(L.srep + h)) = pos + 1;
-            __threadfence();
-          }
-          break;
-        }
-        cur = old;
-      }
-      if ((uint32_t)cur == kw) {
-        if (!MULTI) break;
-        uint32_t r;
-        while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
-        }
-        bool eq = true;
-#pragma unroll
-        for (int t = 0; t < MAXK; ++t)
-          if (t < nk && src[t][r - 1] != vals[t]) eq = false;
-        if (eq) break;
-      }
-      if (++h == hi) h = lo;
-    }
-    const uint32_t rank = atomicAdd(&L.table[h].q, 1u) & ~kPendBit;
-    tmp_slot[pos] = (uint32_t)h;
-    tmp_rank[pos] = rank;
-    // warp-aggregated append of new slots
-    const unsigned act = __activemask();
-    const unsigned wmask = __ballot_sync(act, won);
-    if (won) {
-      const int lane = threadIdx.x & 31;
-      const int leader = __ffs(wmask) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&ctr->newslots, (uint32_t)__popc(wmask));
-      base = __shfl_sync(wmask, base, leader);
-      const uint32_t o = base + __popc(wmask & ((1u << lane) - 1));
-      newslots[o] = (uint32_t)h;
-      newslot_p[o] = p;
-    }
-  }
-}
-
-// Child-range allocation: q = p + (running sum of child sizes of p).
-template <bool SINGLE>
-__global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0,
-                               const uint32_t* __restrict__ newslots, const uint32_t* __restrict__ newslot_p,
-                               DevCounters* ctr) {
-  const DevLevel& L = tries[trie].lev[lev];
-  const uint32_t total = ctr->newslots;
-  typedef cub::BlockScan<uint32_t, 256> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ uint32_t s_base;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  const uint32_t iters = (total + stride - 1) / stride;
-  for (uint32_t it = 0; it < iters; ++it) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
-    const bool ok = i < total;
-    uint32_t h = 0, c = 0, p = 0;
-    if (ok) {
-      h = newslots[i];
-      p = newslot_p[i];
-      c = L.table[h].q & ~kPendBit;
-    }
-    uint32_t q = 0;
-    if (SINGLE) {
-      uint32_t excl, blk_total;
-      BS(tmp).ExclusiveSum(c, excl, blk_total);
-      if (threadIdx.x == 0) {
-        const uint32_t first = blockIdx.x * blockDim.x + it * stride;
-        if (first < total) {
-          const uint32_t nb = min((uint32_t)blockDim.x, total - first);
-          s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);
-          atomicAdd(&L.nkeys[p0], nb);
-        }
-      }
-      __syncthreads();
-      q = s_base + excl;
-      __syncthreads();
-    } else if (ok) {
-      const unsigned act = __activemask();
-      const unsigned grp = __match_any_sync(act, p);
-      const int lane = threadIdx.x & 31;
-      const int leader = __ffs(grp) - 1;
-      uint32_t pre = 0, tot = 0;
-      unsigned m = grp;
-      while (m) {
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t cl = __shfl_sync(grp, c, l);
-        if (l < lane) pre += cl;
-        tot += cl;
-      }
-      uint32_t base = 0;
-      if (lane == leader) {
-        base = atomicAdd(&L.cursor[p], tot);
-        atomicAdd(&L.nkeys[p], (uint32_t)__popc(grp));
-      }
-      base = __shfl_sync(grp, base, leader);
-      q = p + base + pre;
-    }
-    if (ok) {
-      L.table[h].q = q;
-      L.cnt[q] = c;
-    }
-  }
-}
-
-__global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
-                                const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank) {
-  const DevTrie& T = tries[trie];
-  const DevLevel& L = T.lev[lev];
-  const uint32_t total = force_total(R);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t p, len, pos;
-    force_locate(R, i, p, len, pos);
-    const uint32_t h = tmp_slot[pos];
-    const uint32_t dst = L.table[h].q + tmp_rank[pos];
-    for (int c = 0; c < T.ncols; ++c) {
-      int32_t* out = L.cval[c];
-      if (out) out[dst] = level_src(T, lev, c)[pos];
-    }
-  }
-}
-
-__global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
-  const DevLevel& L = tries[trie].lev[lev];
-  if (R.single) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
-    return;
-  }
-  const uint32_t c = *R.list_count;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
-    L.state[R.list_p[i]] = 2u;
-}
-
-// ============================================================================
-// k_expand: iterate cover, probe, compact / aggregate  (Fig 13)
-// ============================================================================
-enum ExpandMode { EXPAND_WRITE = 0, EXPAND_COUNT = 1, EXPAND_ENUM = 2, EXPAND_MEMO = 3 };
-
-__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ a, uint64_t lo, uint64_t hi,
-                                                    uint64_t x) {
-  // first index in [lo, hi] with a[idx] > x (a[hi] > x guaranteed)
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) > x)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  return lo;
-}
-
-// Load-balanced search, pass 1: bounds[t] = entry owning candidate c0 + t*TILE
-// (bounds[ntiles] = F-1). Each k_expand tile then searches only
-// [bounds[t], bounds[t+1]] instead of the whole scan.
-constexpr int TILE = 256;
-constexpr uint64_t kLastChunk = 1ull << 28;  // last-node candidates per launch
-__global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1,
-                              uint64_t* __restrict__ bounds) {
-  const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles;
-       t += (uint64_t)gridDim.x * blockDim.x)
-    bounds[t] = (t == ntiles) ? F - 1 : upper_bound_u64(scan, 0, F - 1, c0 + t * TILE);
-}
-
-// Register-resident helpers: W bounds the variables / atoms of the query at
-// compile time so every per-candidate array stays in registers.
-// (arithmetic blends: a plain `if (u == v) a[u] = x` is pattern-matched back
-// into an indexed local-memory store)
-template <int W>
-__device__ __forceinline__ int32_t sel(const int32_t (&a)[W], int v) {
-  int32_t x = 0;
-#pragma unroll
-  for (int u = 0; u < W; ++u) x |= a[u] & -(int32_t)(u == v);
-  return x;
-}
-
-template <int W>
-__device__ __forceinline__ void put(int32_t (&a)[W], int v, int32_t x) {
-#pragma unroll
-  for (int u = 0; u < W; ++u) {
-    const int32_t m = -(int32_t)(u == v);
-    a[u] = (x & m) | (a[u] & ~m);
-  }
-}
-
-template <int W>
-__device__ __forceinline__ void put2(uint32_t (&a)[W], uint32_t (&b)[W], int v, uint32_t x, uint32_t y) {
-#pragma unroll
-  for (int u = 0; u < W; ++u) {
-    const uint32_t m = 0u - (uint32_t)(u == v);
-    a[u] = (x & m) | (a[u] & ~m);
-    b[u] = (y & m) | (b[u] & ~m);
-  }
-}
-
-template <int W>
-__device__ __forceinline__ uint32_t selu_(const uint32_t (&a)[W], int v) {
-  uint32_t x = 0;
-#pragma unroll
-  for (int u = 0; u < W; ++u) x |= a[u] & (0u - (uint32_t)(u == v));
-  return x;
-}
-
-// Per-candidate binding state. Narrow queries (W = 4) keep it in registers
-// with arithmetic-blend selects; wider ones (W >= 8, where a blend costs W
-// instructions per access) keep it in shared memory, variable-major so the
-// lanes of a warp hit distinct banks.
-template <int W>
-struct RegState {
-  int32_t val[W];
-  uint32_t cp[W], cl[W];
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int u = 0; u < W; ++u) val[u] = cp[u] = cl[u] = 0;
-  }
-  __device__ __forceinline__ int32_t get(int v) const { return sel(val, v); }
-  __device__ __forceinline__ void set(int v, int32_t x) { put(val, v, x); }
-  __device__ __forceinline__ int32_t at(int u) const { return val[u]; }
-  __device__ __forceinline__ void seta(int u, int32_t x) { val[u] = x; }
-  __device__ __forceinline__ void setc(int a, uint32_t p, uint32_t l) { put2(cp, cl, a, p, l); }
-  __device__ __forceinline__ void setca(int a, uint32_t p, uint32_t l) {
-    cp[a] = p;
-    cl[a] = l;
-  }
-  __device__ __forceinline__ uint32_t cpa(int a) const { return cp[a]; }
-  __device__ __forceinline__ uint32_t cla(int a) const { return cl[a]; }
-  __device__ __forceinline__ uint32_t cpd(int a) const { return selu_(cp, a); }
-};
-
-template <int W>
-struct SmemState {
-  int32_t* val;
-  uint32_t *cp, *cl;
-  __device__ __forceinline__ SmemState(int32_t* sv, uint32_t* sp, uint32_t* sl)
-      : val(sv + threadIdx.x), cp(sp + threadIdx.x), cl(sl + threadIdx.x) {}
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int u = 0; u < W; ++u) val[u * TILE] = cp[u * TILE] = cl[u * TILE] = 0;
-  }
-  __device__ __forceinline__ int32_t get(int v) const { return val[v * TILE]; }
-  __device__ __forceinline__ void set(int v, int32_t x) { val[v * TILE] = x; }
-  __device__ __forceinline__ int32_t at(int u) const { return val[u * TILE]; }
-  __device__ __forceinline__ void seta(int u, int32_t x) { val[u * TILE] = x; }
-  __device__ __forceinline__ void setc(int a, uint32_t p, uint32_t l) {
-    cp[a * TILE] = p;
-    cl[a * TILE] = l;
-  }
-  __device__ __forceinline__ void setca(int a, uint32_t p, uint32_t l) { setc(a, p, l); }
-  __device__ __forceinline__ uint32_t cpa(int a) const { return cp[a * TILE]; }
-  __device__ __forceinline__ uint32_t cla(int a) const { return cl[a * TILE]; }
-  __device__ __forceinline__ uint32_t cpd(int a) const { return cp[a * TILE]; }
-};
-
-template <class St, int W>
-__device__ __forceinline__ St make_state(uint32_t* smem) {
-  if constexpr (W >= 8) {
-    return St(reinterpret_cast<int32_t*>(smem), smem + W * TILE, smem + 2 * W * TILE);
-  } else {
-    return St();
-  }
-}
-
-// One candidate: iterate the chosen cover at position j of entry e, then probe
-// every other subatom of the node in order. Returns false if the candidate dies.
-template <int MODE, int W, class St>
-__device__ __forceinline__ bool run_candidate(const KNode& N, uint64_t e, uint64_t j, St& st, uint64_t& mult,
-                                              uint64_t& probes, uint64_t& misses, uint64_t& body) {
-#pragma unroll
-  for (int v = 0; v < W; ++v)
-    if ((N.in_vars >> v) & 1u) st.seta(v, __ldg(N.in_var[v] + e));
-  if (MODE == EXPAND_WRITE) {
-#pragma unroll
-    for (int a = 0; a < W; ++a)
-      if ((N.in_atoms >> a) & 1u) st.setca(a, __ldg(N.in_p[a] + e), __ldg(N.in_len[a] + e));
-  }
-  if (N.in_mult) mult = __ldg(N.in_mult + e);
-  // ---- iterate the chosen cover (Fig 12 iter) ----
-  const int ci = N.chosen[e];
-  const KSub& S = N.sub[ci];
-  uint32_t p, len;
-  subtrie_of(S, e, p, len);
-  if (p == kSingleton) {
-    st.setc(S.atom, kSingleton, 1u);
-  } else {
-    const uint32_t pos = p + (uint32_t)j;
-    if (!S.stream) {
-      // forced map: distinct keys are the child starts
-      const uint32_t c = __ldg(S.cnt + pos);
-      if (c == 0) return false;
-      st.setc(S.atom, pos, c);
-    } else {
-      st.setc(S.atom, kSingleton, 1u);  // suffix: stream values at the offsets
-    }
-#pragma unroll
-    for (int t = 0; t < MAXK; ++t)
-      if (t < S.nv) {
-        const int32_t x = __ldg(S.src[t] + pos);
-        const int v = S.var[t];
-        if ((S.bound_mask >> t) & 1) {
-          if (st.get(v) != x) return false;  // cover re-binds a bound variable
-        } else {
-          st.set(v, x);
-        }
-      }
-  }
-  ++body;  // the node body runs for this cover tuple (ExecStats.node_body_entries)
-  // ---- probe every other subatom in node order (Fig 13 inner loop) ----
-  for (int s = 0; s < N.nsub; ++s) {
-    if (s == ci) continue;
-    const KSub& P = N.sub[s];
-    uint32_t pp, pl;
-    subtrie_of(P, e, pp, pl);
-    uint32_t q = kSingleton, ql = 1;
-    if (pp != kSingleton) {
-      int32_t key[MAXK];
-#pragma unroll
-      for (int t = 0; t < MAXK; ++t) key[t] = t < P.nv ? st.get(P.var[t]) : 0;
-      ++probes;
-      if (!colt_get(P, pp, pl, key, q, ql)) {
-        ++misses;
-        return false;
-      }
-    }
-    if (P.last)
-      mult *= ql;  // residual leaf vector: its offsets are the multiplicity
-    else
-      st.setc(P.atom, q, ql);
-  }
-  return true;
-}
-
-#ifndef FJG_EXPAND_MINBLOCKS
-#define FJG_EXPAND_MINBLOCKS 1
-#endif
-template <int MODE, int W>
-__global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __grid_constant__ KNode N, uint64_t c0,
-                                                                       uint64_t c1, uint64_t F,
-                                                                       const uint64_t* __restrict__ bounds,
-                                                                       int min_var, int32_t* __restrict__ out_tuples,
-                                                                       uint64_t out_cap, DevCounters* ctr) {
-  __shared__ uint32_t s_warp[TILE / 32];
-  __shared__ uint32_t s_base;
-  extern __shared__ uint32_t s_state[];  // W >= 8: 3 * W * TILE words
-  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
-  long long acc_min = LLONG_MAX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t* __restrict__ scan = N.scan;
-  using St = typename std::conditional<(W >= 8), SmemState<W>, RegState<W>>::type;
-
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
-    const uint64_t t = (base - c0) / TILE;
-    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
-    const uint64_t i = base + threadIdx.x;
-    bool alive = i < c1;
-    St st = make_state<St, W>(s_state);
-    st.init();
-    uint64_t mult = 1;
-    if (alive) {
-      const uint64_t e = upper_bound_u64(scan, lo, hi, i);
-      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
-      alive = run_candidate<MODE, W>(N, e, j, st, mult, probes, misses, body);
-    }
-    if (MODE == EXPAND_WRITE) {
-      const unsigned bal = __ballot_sync(0xffffffffu, alive);
-      if (lane == 0) s_warp[warp] = __popc(bal);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        for (int w = 0; w < TILE / 32; ++w) {
-          const uint32_t c = s_warp[w];
-          s_warp[w] = tot;
-          tot += c;
-        }
-        s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
-      }
-      __syncthreads();
-      if (alive) {
-        const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
-#pragma unroll
-        for (int v = 0; v < W; ++v)
-          if ((N.out_vars >> v) & 1u) N.out_var[v][o] = st.at(v);
-#pragma unroll
-        for (int a = 0; a < W; ++a)
-          if ((N.out_atoms >> a) & 1u) {
-            N.out_p[a][o] = st.cpa(a);
-            N.out_len[a][o] = st.cla(a);
-          }
-        if (N.out_mult) N.out_mult[o] = mult;
-      }
-      __syncthreads();
-    } else if (alive) {
-      if (MODE == EXPAND_COUNT) {
-        uint64_t h = fj::kTupleHashSeed;
-#pragma unroll
-        for (int v = 0; v < W; ++v)
-          if (v < N.nhead) h = fj::tuple_hash_step(h, (int64_t)st.at(v));
-        acc_sum += mult * fj::checksum_word(h);
-        acc_lo += mult;
-        if (acc_lo < mult) ++acc_hi;
-        if (min_var >= 0) acc_min = min(acc_min, (long long)st.get(min_var));
-      } else if (MODE == EXPAND_MEMO) {
-        // memoised chain suffix: this binding contributes mult * count(child of the carrier)
-        const uint32_t q = st.cpd(N.memo_atom);
-        const unsigned __int128 mv =
-            ((unsigned __int128)N.memo[2ull * q + 1] << 64) | (unsigned __int128)N.memo[2ull * q];
-        const unsigned __int128 c = mv * mult + (((unsigned __int128)acc_hi << 64) | acc_lo);
-        acc_lo = (uint64_t)c;
-        acc_hi = (uint64_t)(c >> 64);
-      } else {
-        const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
-        for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
-#pragma unroll
-          for (int v = 0; v < W; ++v)
-            if (v < N.nhead) out_tuples[(o + r) * N.nhead + v] = st.at(v);
-      }
-    }
-  }
-  // ---- flush per-thread accumulators: one atomic per warp ----
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
-  if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
-    }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
-  }
-  if (MODE == EXPAND_COUNT || MODE == EXPAND_MEMO) {
-    // 128-bit count: carry out of the low word
-    uint64_t lo = acc_lo, hi = acc_hi;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o);
-      const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi, o);
-      const uint64_t s = lo + l2;
-      hi += h2 + (s < lo ? 1 : 0);
-      lo = s;
-    }
-    acc_sum = warp_sum(acc_sum);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
-    if (lane == 0) {
-      if (lo) {
-        const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo);
-        if (old + lo < old) ++hi;
-      }
-      if (hi) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi);
-      if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
-      if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
-    }
-  }
-}
-
-__device__ __forceinline__ void atomic_add_u128(unsigned long long* m, unsigned __int128 v) {
-  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
-  const unsigned long long old = atomicAdd(m, lo);
-  const unsigned long long carry = (old + lo < old) ? 1ull : 0ull;
-  if (hi + carry) atomicAdd(m + 1, hi + carry);
-}
-
-__global__ void __launch_bounds__(256) k_memo_pass(const __grid_constant__ MemoPass M) {
-  const unsigned FULL = 0xffffffffu;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t iters = (M.n + stride - 1) / stride;
-  for (uint64_t it = 0; it < iters; ++it) {
-    const uint64_t pos = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + it * stride;
-    const bool ok = pos < M.n;
-    uint32_t g = 0;
-    unsigned __int128 f = 0;
-    if (ok) {
-      g = M.owner[pos];
-      int32_t t[MAXK];
-#pragma unroll
-      for (int k = 0; k < MAXK; ++k) t[k] = k < M.cnv ? __ldg(M.cvals[k] + pos) : 0;
-      f = 1;
-      for (int x = 0; x < M.nfresh; ++x) {
-        const KSub& X = M.fresh[x];
-        int32_t key[MAXK];
-#pragma unroll
-        for (int k = 0; k < MAXK; ++k) {
-          int32_t v = 0;
-#pragma unroll
-          for (int u = 0; u < MAXK; ++u) v |= t[u] & -(int32_t)(u == M.cpos[x][k]);
-          key[k] = k < X.nv ? v : 0;
-        }
-        uint32_t q, ql;
-        if (!colt_get(X, 0u, X.root_n, key, q, ql)) {
-          f = 0;
-          break;
-        }
-        if (M.cont[x])
-          f *= ((unsigned __int128)M.memo_next[2ull * q + 1] << 64) | (unsigned __int128)M.memo_next[2ull * q];
-        else
-          f *= ql;
-      }
-    }
-    // positions of one group are contiguous: aggregate per group inside the warp
-    const unsigned act = __ballot_sync(FULL, ok && f != 0);
-    if (ok && f != 0) {
-      const unsigned grp = __match_any_sync(act, g);
-      const int lane = threadIdx.x & 31;
-      const int leader = __ffs(grp) - 1;
-      unsigned long long lo = (unsigned long long)f, hi = (unsigned long long)(f >> 64);
-      unsigned long long slo = 0, shi = 0;
-      unsigned m = grp;
-      while (m) {
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        const unsigned long long a = __shfl_sync(grp, lo, l), b = __shfl_sync(grp, hi, l);
-        const unsigned long long s2 = slo + a;
-        shi += b + (s2 < slo ? 1ull : 0ull);
-        slo = s2;
-      }
-      if (lane == leader) atomic_add_u128(M.memo_out + 2ull * g, ((unsigned __int128)shi << 64) | slo);
-    }
-  }
-}
-
-struct MaxOp {
-  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
-};
-__global__ void k_group_starts(const uint32_t* cnt, uint64_t n, uint32_t* out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = cnt[i] ? (uint32_t)i : 0u;
-}
-
-#ifndef FJG_GJ_WARPSEARCH
-#define FJG_GJ_WARPSEARCH 0
-#endif
-#ifndef FJG_GJ_PREFETCH
-#define FJG_GJ_PREFETCH 1
-#endif
-// Fast path for the Generic-Join-shaped aggregating last node: every subatom
-// is a cover over the same single new variable x (triangle C2/C5, 4-clique
-// C4). Per candidate: binding lookup, one coalesced cover read, NS-1 bucket
-// probes, fold into count / checksum -- no generic state machinery.
-template <int NS, int W>
-__global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                  uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
-                                                  int min_var, DevCounters* ctr) {
-  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
-  long long acc_min = LLONG_MAX;
-  const int lane = threadIdx.x & 31;
-  const uint64_t* __restrict__ scan = N.scan;
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
-    const uint64_t t = (base - c0) / TILE;
-    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
-    const uint64_t i = base + threadIdx.x;
-    // binding of candidate i: the tile's bindings [lo, hi] are usually few, so
-    // the warp loads their scan values in one coalesced load and each lane
-    // counts the ones <= i with shuffles; long spans fall back to a search.
-    uint64_t e, j;
-    if (FJG_GJ_WARPSEARCH && hi - lo < 32) {
-      const uint32_t span = (uint32_t)(hi - lo) + 1;
-      const uint64_t sv = lane < (int)span ? __ldg(scan + lo + lane) : ~0ull;
-      uint32_t k = 0;
-      for (uint32_t u = 0; u < span; ++u) k += __shfl_sync(0xffffffffu, sv, u) <= i ? 1u : 0u;
-      const uint64_t prev = __shfl_sync(0xffffffffu, sv, k > 0 ? k - 1 : 0);
-      e = lo + k;
-      j = i - (k > 0 ? prev : (lo ? __ldg(scan + lo - 1) : 0ull));
-    } else {
-      e = i < c1 ? upper_bound_u64(scan, lo, hi, i) : lo;
-      j = i - (e ? __ldg(scan + e - 1) : 0ull);
-    }
-    if (i >= c1) continue;
-    const int ci = N.chosen[e];
-    uint32_t sp[NS], sl[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const KSub& P = N.sub[s];
-      if (P.in_p) {
-        sp[s] = __ldg(P.in_p + e);
-        sl[s] = __ldg(P.in_len + e);
-      } else {
-        sp[s] = 0;
-        sl[s] = P.root_n;
-      }
-    }
-    uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
-    int32_t hv[W];  // bound head variables, prefetched off the critical path
-#pragma unroll
-    for (int v = 0; v < W; ++v) hv[v] = (FJG_GJ_PREFETCH && v < N.nhead && v != xvar) ? __ldg(N.in_var[v] + e) : 0;
-    uint32_t cpos = 0;
-    const int32_t* csrc = nullptr;
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-      if (s == ci) {
-        cpos = sp[s] + (uint32_t)j;
-        csrc = N.sub[s].src[0];
-      }
-    const int32_t x = __ldg(csrc + cpos);
-    ++body;
-    bool alive = true;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s == ci || !alive) continue;
-      const KSub& P = N.sub[s];
-      ++probes;
-      const uint32_t kw = (uint32_t)x;
-      uint64_t b = region_bucket(sp[s], sl[s], kw);
-      const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
-      const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-      uint32_t q = kEmpty;
-      while (true) {
-        const uint4 h0 = __ldg(tb + 2 * b);
-        if (h0.y == kEmpty) break;
-        if (h0.x == kw) { q = h0.y; break; }
-        if (h0.w == kEmpty) break;
-        if (h0.z == kw) { q = h0.w; break; }
-        const uint4 h1 = __ldg(tb + 2 * b + 1);
-        if (h1.y == kEmpty) break;
-        if (h1.x == kw) { q = h1.y; break; }
-        if (h1.w == kEmpty) break;
-        if (h1.z == kw) { q = h1.w; break; }
-        if (++b == bhi) b = blo;
-      }
-      if (q == kEmpty) {
-        ++misses;
-        alive = false;
-      } else if (P.last) {
-        mult *= __ldg(P.cnt + q);
-      }
-    }
-    if (!alive) continue;
-    uint64_t h = fj::kTupleHashSeed;
-#pragma unroll
-    for (int v = 0; v < W; ++v)
-      if (v < N.nhead) {
-        const int32_t val = (v == xvar) ? x : (FJG_GJ_PREFETCH ? hv[v] : __ldg(N.in_var[v] + e));
-        h = fj::tuple_hash_step(h, (int64_t)val);
-        if (v == min_var) acc_min = min(acc_min, (long long)val);
-      }
-    acc_sum += mult * fj::checksum_word(h);
-    acc_lo += mult;
-    if (acc_lo < mult) ++acc_hi;
-  }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
-  uint64_t lo2 = acc_lo, hi2 = acc_hi;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
-    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
-    const uint64_t sm = lo2 + l2;
-    hi2 += h2 + (sm < lo2 ? 1 : 0);
-    lo2 = sm;
-  }
-  acc_sum = warp_sum(acc_sum);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
-  if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
-    }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
-    if (lo2) {
-      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
-      if (old + lo2 < old) ++hi2;
-    }
-    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
-    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
-    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
-  }
-}
-
-// ILP variant of k_last_gj for the common case where the new variable x is the
-// last head variable (so the tuple hash is step(prefix(binding), x)): each
-// thread owns a run of R consecutive candidates, split at binding
-// boundaries; inside a run the binding state is loaded once and the R cover
-// reads and R first-bucket probes are issued back to back.
-template <int NS, int R, int W>
-__global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                      uint64_t F, const uint64_t* __restrict__ bounds,
-                                                      int min_var, DevCounters* ctr) {
-  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
-  long long acc_min = LLONG_MAX;
-  const int lane = threadIdx.x & 31;
-  const uint64_t* __restrict__ scan = N.scan;
-  const int nhead = N.nhead;
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * R; base < c1; base += (uint64_t)gridDim.x * TILE * R) {
-    uint64_t i = base + (uint64_t)threadIdx.x * R;
-    const uint64_t iend = min(i + R, c1);
-    if (i >= iend) continue;
-    const uint64_t t = (i - c0) / TILE;
-    uint64_t e = upper_bound_u64(scan, __ldg(bounds + t), __ldg(bounds + t + 1), i);
-    while (i < iend) {
-      const uint64_t se = __ldg(scan + e);
-      const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
-      const uint64_t bend = min(iend, se);  // this batch: candidates [i, bend) of binding e
-      // binding state
-      const int ci = N.chosen[e];
-      uint32_t sp[NS], sl[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const KSub& P = N.sub[s];
-        if (P.in_p) {
-          sp[s] = __ldg(P.in_p + e);
-          sl[s] = __ldg(P.in_len + e);
-        } else {
-          sp[s] = 0;
-          sl[s] = P.root_n;
-        }
-      }
-      const uint64_t mult0 = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
-      uint64_t pre = fj::kTupleHashSeed;
-      long long bmin = LLONG_MAX;
-#pragma unroll
-      for (int v = 0; v < W; ++v)
-        if (v < nhead - 1) {
-          const int32_t hvv = __ldg(N.in_var[v] + e);
-          pre = fj::tuple_hash_step(pre, (int64_t)hvv);
-          if (v == min_var) bmin = hvv;
-        }
-      uint32_t cbase = 0;
-      const int32_t* csrc = nullptr;
-#pragma unroll
-      for (int s = 0; s < NS; ++s)
-        if (s == ci) {
-          cbase = sp[s] + (uint32_t)(i - prev);
-          csrc = N.sub[s].src[0];
-        }
-      // R cover reads
-      int32_t x[R];
-      bool live[R];
-      uint64_t mu[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        live[r] = i + r < bend;
-        x[r] = live[r] ? __ldg(csrc + cbase + r) : 0;
-        mu[r] = mult0;
-        if (live[r]) ++body;
-      }
-      // probes, R first buckets in flight per subatom
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s == ci) continue;
-        const KSub& P = N.sub[s];
-        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
-        uint4 h0[R];
-        uint64_t b0[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          b0[r] = region_bucket(sp[s], sl[s], (uint32_t)x[r]);
-          h0[r] = live[r] ? __ldg(tb + 2 * b0[r]) : make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!live[r]) continue;
-          ++probes;
-          const uint32_t kw = (uint32_t)x[r];
-          uint32_t q = kEmpty;
-          bool more = false;
-          if (h0[r].y == kEmpty) {
-          } else if (h0[r].x == kw) {
-            q = h0[r].y;
-          } else if (h0[r].w == kEmpty) {
-          } else if (h0[r].z == kw) {
-            q = h0[r].w;
-          } else {
-            more = true;
-          }
-          if (more) {  // rest of the bucket, then the following buckets
-            uint64_t b = b0[r];
-            uint4 h1 = __ldg(tb + 2 * b + 1);
-            while (true) {
-              if (h1.y == kEmpty) break;
-              if (h1.x == kw) { q = h1.y; break; }
-              if (h1.w == kEmpty) break;
-              if (h1.z == kw) { q = h1.w; break; }
-              if (++b == bhi) b = blo;
-              const uint4 a0 = __ldg(tb + 2 * b);
-              if (a0.y == kEmpty) break;
-              if (a0.x == kw) { q = a0.y; break; }
-              if (a0.w == kEmpty) break;
-              if (a0.z == kw) { q = a0.w; break; }
-              h1 = __ldg(tb + 2 * b + 1);
-            }
-          }
-          if (q == kEmpty) {
-            ++misses;
-            live[r] = false;
-          } else if (P.last) {
-            mu[r] *= __ldg(P.cnt + q);
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!live[r]) continue;
-        const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x[r]);
-        acc_sum += mu[r] * fj::checksum_word(h);
-        acc_lo += mu[r];
-        if (acc_lo < mu[r]) ++acc_hi;
-        if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x[r] : bmin);
-      }
-      i = bend;
-      ++e;
-    }
-  }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
-  uint64_t lo2 = acc_lo, hi2 = acc_hi;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
-    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
-    const uint64_t sm = lo2 + l2;
-    hi2 += h2 + (sm < lo2 ? 1 : 0);
-    lo2 = sm;
-  }
-  acc_sum = warp_sum(acc_sum);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
-  if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
-    }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
-    if (lo2) {
-      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
-      if (old + lo2 < old) ++hi2;
-    }
-    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
-    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
-    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
-  }
-}
-
-#ifndef FJG_GJ_R
-#define FJG_GJ_R 2
-#endif
-#ifndef FJG_GJ_WRITE
-#define FJG_GJ_WRITE 1
-#endif
-#ifndef FJG_STREAM_WRITE
-#define FJG_STREAM_WRITE 1
-#endif
-
-// GJ-shaped frontier-writing node: every subatom is a one-variable cover of the
-// new variable x; atoms whose subatom is not their last continue with the
-// child of their cover (keys mode) or probe (q, cnt[q]). Survivors are
-// block-compacted into the next frontier.
-template <int NS, int W>
-__global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                   uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
-                                                   DevCounters* ctr) {
-  __shared__ uint32_t s_warp[TILE / 32];
-  __shared__ uint32_t s_base;
-  uint64_t probes = 0, misses = 0, body = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t* __restrict__ scan = N.scan;
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
-    const uint64_t t = (base - c0) / TILE;
-    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
-    const uint64_t i = base + threadIdx.x;
-    bool alive = i < c1;
-    uint64_t e = 0, mult = 1;
-    int32_t x = 0;
-    uint32_t chp[NS], chl[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) chp[s] = chl[s] = 0;
-    if (alive) {
-      e = upper_bound_u64(scan, lo, hi, i);
-      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
-      const int ci = N.chosen[e];
-      uint32_t sp[NS], sl[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const KSub& P = N.sub[s];
-        if (P.in_p) {
-          sp[s] = __ldg(P.in_p + e);
-          sl[s] = __ldg(P.in_len + e);
-        } else {
-          sp[s] = 0;
-          sl[s] = P.root_n;
-        }
-      }
-      if (N.in_mult) mult = __ldg(N.in_mult + e);
-#pragma unroll
-      for (int s = 0; s < NS; ++s)
-        if (s == ci) {
-          const KSub& S = N.sub[s];
-          const uint32_t pos = sp[s] + (uint32_t)j;
-          if (!S.stream) {  // forced map: distinct keys are the child starts
-            const uint32_t c = __ldg(S.cnt + pos);
-            if (c == 0) alive = false;
-            chp[s] = pos;
-            chl[s] = c;
-          } else {
-            chp[s] = kSingleton;
-            chl[s] = 1;
-          }
-          if (alive) x = __ldg(S.src[0] + pos);
-        }
-      if (alive) ++body;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s == ci || !alive) continue;
-        const KSub& P = N.sub[s];
-        ++probes;
-        const uint32_t kw = (uint32_t)x;
-        uint64_t b = region_bucket(sp[s], sl[s], kw);
-        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
-        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-        uint32_t q = kEmpty;
-        while (true) {
-          const uint4 h0 = __ldg(tb + 2 * b);
-          if (h0.y == kEmpty) break;
-          if (h0.x == kw) { q = h0.y; break; }
-          if (h0.w == kEmpty) break;
-          if (h0.z == kw) { q = h0.w; break; }
-          const uint4 h1 = __ldg(tb + 2 * b + 1);
-          if (h1.y == kEmpty) break;
-          if (h1.x == kw) { q = h1.y; break; }
-          if (h1.w == kEmpty) break;
-          if (h1.z == kw) { q = h1.w; break; }
-          if (++b == bhi) b = blo;
-        }
-        if (q == kEmpty) {
-          ++misses;
-          alive = false;
-        } else {
-          const uint32_t ql = __ldg(P.cnt + q);
-          if (P.last)
-            mult *= ql;
-          else {
-            chp[s] = q;
-            chl[s] = ql;
-          }
-        }
-      }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, alive);
-    if (lane == 0) s_warp[warp] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tot = 0;
-      for (int w = 0; w < TILE / 32; ++w) {
-        const uint32_t c = s_warp[w];
-        s_warp[w] = tot;
-        tot += c;
-      }
-      s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
-    }
-    __syncthreads();
-    if (alive) {
-      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
-#pragma unroll
-      for (int v = 0; v < W; ++v)
-        if ((N.out_vars >> v) & 1u) N.out_var[v][o] = (v == xvar) ? x : __ldg(N.in_var[v] + e);
-#pragma unroll
-      for (int a = 0; a < W; ++a)
-        if ((N.out_atoms >> a) & 1u) {
-          uint32_t pa = 0, la = 0;
-          bool here = false;
-#pragma unroll
-          for (int s = 0; s < NS; ++s)
-            if (N.sub[s].atom == a) {
-              pa = chp[s];
-              la = chl[s];
-              here = true;
-            }
-          if (!here) {
-            pa = __ldg(N.in_p[a] + e);
-            la = __ldg(N.in_len[a] + e);
-          }
-          N.out_p[a][o] = pa;
-          N.out_len[a][o] = la;
-        }
-      if (N.out_mult) N.out_mult[o] = mult;
-    }
-    __syncthreads();
-  }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
-  if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
-    }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
-  }
-}
-
-// Binary-join-pipeline node (frontier-writing): one cover iterated in stream
-// mode, every other subatom a single-variable probe keyed on a variable the
-// cover binds (C1 chain, C3 star node 0). Cover columns are loaded lazily, in
-// probe order, so a candidate that dies at its first probe reads one column.
-template <int W>
-__global__ void __launch_bounds__(TILE) k_write_stream(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                       uint64_t F, const uint64_t* __restrict__ bounds,
-                                                       DevCounters* ctr) {
-  __shared__ uint32_t s_warp[TILE / 32];
-  __shared__ uint32_t s_base;
-  uint64_t probes = 0, misses = 0, body = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t* __restrict__ scan = N.scan;
-  const int ci = N.cov[0];
-  const KSub& S = N.sub[ci];
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
-    const uint64_t t = (base - c0) / TILE;
-    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
-    const uint64_t i = base + threadIdx.x;
-    bool alive = i < c1;
-    uint64_t e = 0, mult = 1;
-    uint32_t pos = 0;
-    int32_t xv[MAXK];
-    uint32_t have = 0;  // bit t: cover column t loaded
-    uint32_t chp[MAXS], chl[MAXS];
-#pragma unroll
-    for (int k = 0; k < MAXK; ++k) xv[k] = 0;
-#pragma unroll
-    for (int s = 0; s < MAXS; ++s) chp[s] = chl[s] = 0;
-    if (alive) {
-      e = upper_bound_u64(scan, lo, hi, i);
-      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
-      uint32_t p;
-      if (S.in_p) {
-        p = __ldg(S.in_p + e);
-      } else {
-        p = 0;
-      }
-      pos = p + (uint32_t)j;
-      if (N.in_mult) mult = __ldg(N.in_mult + e);
-      ++body;
-#pragma unroll
-      for (int s = 0; s < MAXS; ++s) {
-        if (s >= N.nsub || s == ci || !alive) continue;
-        const KSub& P = N.sub[s];
-        // key: the cover column bound to P's variable (loaded on first use)
-        int tk = 0;
-#pragma unroll
-        for (int k = 0; k < MAXK; ++k)
-          if (k < S.nv && S.var[k] == P.var[0]) tk = k;
-        int32_t key = 0;
-#pragma unroll
-        for (int k = 0; k < MAXK; ++k)
-          if (k == tk) {
-            if (!((have >> k) & 1u)) {
-              xv[k] = __ldg(S.src[k] + pos);
-              have |= 1u << k;
-            }
-            key = xv[k];
-          }
-        uint32_t pp, pl;
-        if (P.in_p) {
-          pp = __ldg(P.in_p + e);
-          pl = __ldg(P.in_len + e);
-        } else {
-          pp = 0;
-          pl = P.root_n;
-        }
-        ++probes;
-        const uint32_t kw = (uint32_t)key;
-        uint64_t b = region_bucket(pp, pl, kw);
-        const uint64_t blo = pp, bhi = (uint64_t)pp + pl;
-        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-        uint32_t q = kEmpty;
-        while (true) {
-          const uint4 h0 = __ldg(tb + 2 * b);
-          if (h0.y == kEmpty) break;
-          if (h0.x == kw) { q = h0.y; break; }
-          if (h0.w == kEmpty) break;
-          if (h0.z == kw) { q = h0.w; break; }
-          const uint4 h1 = __ldg(tb + 2 * b + 1);
-          if (h1.y == kEmpty) break;
-          if (h1.x == kw) { q = h1.y; break; }
-          if (h1.w == kEmpty) break;
-          if (h1.z == kw) { q = h1.w; break; }
-          if (++b == bhi) b = blo;
-        }
-        if (q == kEmpty) {
-          ++misses;
-          alive = false;
-        } else {
-          const uint32_t ql = __ldg(P.cnt + q);
-          if (P.last)
-            mult *= ql;
-          else {
-            chp[s] = q;
-            chl[s] = ql;
-          }
-        }
-      }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, alive);
-    if (lane == 0) s_warp[warp] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tot = 0;
-      for (int w = 0; w < TILE / 32; ++w) {
-        const uint32_t c = s_warp[w];
-        s_warp[w] = tot;
-        tot += c;
-      }
-      s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
-    }
-    __syncthreads();
-    if (alive) {
-      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
-#pragma unroll
-      for (int v = 0; v < W; ++v)
-        if ((N.out_vars >> v) & 1u) {
-          int32_t val = 0;
-          bool cov = false;
-#pragma unroll
-          for (int k = 0; k < MAXK; ++k)
-            if (k < S.nv && S.var[k] == v) {
-              val = ((have >> k) & 1u) ? xv[k] : __ldg(S.src[k] + pos);
-              cov = true;
-            }
-          N.out_var[v][o] = cov ? val : __ldg(N.in_var[v] + e);
-        }
-#pragma unroll
-      for (int a = 0; a < W; ++a)
-        if ((N.out_atoms >> a) & 1u) {
-          uint32_t pa = 0, la = 0;
-          bool here = false;
-#pragma unroll
-          for (int s = 0; s < MAXS; ++s)
-            if (s < N.nsub && N.sub[s].atom == a) {
-              pa = s == ci ? kSingleton : chp[s];
-              la = s == ci ? 1u : chl[s];
-              here = true;
-            }
-          if (!here) {
-            pa = __ldg(N.in_p[a] + e);
-            la = __ldg(N.in_len[a] + e);
-          }
-          N.out_p[a][o] = pa;
-          N.out_len[a][o] = la;
-        }
-      if (N.out_mult) N.out_mult[o] = mult;
-    }
-    __syncthreads();
-  }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
-  if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
-    }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
-  }
-}
-
-// The stream fast path: a single cover in stream mode whose subtrie is never a
-// singleton, all its variables fresh; every other subatom probes one variable
-// the cover binds.
-static bool stream_write_ok(const DevNode& N, const KNode& G) {
-  if (N.ncov != 1 || N.nsub < 2) return false;
-  const DevSub& C = N.sub[N.cov[0]];
-  if (!C.stream || C.bound_mask || C.nv < 1) return false;
-  if (G.sub[N.cov[0]].in_p == nullptr && C.depth != 0) return false;
-  for (int s = 0; s < N.nsub; ++s) {
-    if (s == N.cov[0]) continue;
-    const DevSub& P = N.sub[s];
-    if (P.nv != 1) return false;
-    bool found = false;
-    for (int t = 0; t < C.nv; ++t)
-      if (C.var[t] == P.var[0]) found = true;
-    if (!found) return false;
-  }
-  return true;
-}
-
-// A frontier-writing node is GJ-shaped when every subatom is a one-variable
-// cover of the same fresh variable (levels of depth >= 0, no bound check).
-static int gj_write_var(const DevNode& N, int width) {
-  if (N.nsub < 2 || N.nsub > 3 || N.ncov != N.nsub || width > 8) return -1;
-  int x = -1;
-  for (int s = 0; s < N.nsub; ++s) {
-    const DevSub& D = N.sub[s];
-    if (D.nv != 1 || D.bound_mask) return -1;
-    if (x >= 0 && D.var[0] != x) return -1;
-    x = D.var[0];
-  }
-  return x;
-}
-
-// The GJ fast path applies when every subatom of the node is a one-variable
-// cover of the same new, unbound variable, and no subtrie can be a streamed
-// singleton (all subatoms keys-or-stream levels of depth >= 0 with nv == 1).
-static int gj_last_var(const KNode& G, const DevNode& N) {
-  if (N.nsub < 2 || N.nsub > 3 || N.ncov != N.nsub || N.nhead > 8) return -1;
-  int x = -1;
-  for (int s = 0; s < N.nsub; ++s) {
-    const DevSub& D = N.sub[s];
-    if (D.nv != 1 || D.bound_mask || !D.stream) return -1;
-    if (x >= 0 && D.var[0] != x) return -1;
-    x = D.var[0];
-  }
-  // every earlier subatom of these atoms bound variables (no singleton residuals)
-  for (int s = 0; s < N.nsub; ++s)
-    if (G.sub[s].in_p == nullptr && N.sub[s].depth != 0) return -1;
-  return x;
-}
+#include "kernels/common.cuh"
+#include "kernels/select.cuh"
+#include "kernels/force.cuh"
+#include "kernels/node_generic.cuh"
+#include "kernels/memo.cuh"
+#include "kernels/node_fastpaths.cuh"
 
 // host-side dispatch on the query width (max(#vars, #atoms) -> 4 / 8 / 16)
 template <int MODE>
@@ -1554,55 +88,7 @@ static void launch_expand(int width, unsigned grid, cudaStream_t st, const KNode
     k_expand<MODE, 16><<<grid, TILE, 3 * 16 * TILE * 4, st>>>(nd, c0, c1, F, bounds, min_var, out, cap, ctr);
 }
 
-// ============================================================================
-// misc kernels
-// ============================================================================
-__global__ void k_tuple_hash(const int64_t* vals, int arity, uint64_t n, uint64_t* out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t h = fj::kTupleHashSeed;
-    for (int t = 0; t < arity; ++t) h = fj::tuple_hash_step(h, vals[i * arity + t]);
-    out[i] = h;
-  }
-}
-
-__device__ __forceinline__ bool cmp_eval(int cmp, int64_t a, int64_t b) {
-  switch (cmp) {
-    case FJG_CMP_EQ: return a == b;
-    case FJG_CMP_NE: return a != b;
-    case FJG_CMP_LT: return a < b;
-    case FJG_CMP_LE: return a <= b;
-    case FJG_CMP_GT: return a > b;
-    default: return a >= b;
-  }
-}
-
-struct DevPreds {
-  int n;
-  fjg_predicate p[8];
-  const int32_t* cols[MAXC];
-};
-
-__global__ void k_filter_flags(DevPreds P, uint64_t n, uint32_t* flags) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    bool ok = true;
-    for (int k = 0; k < P.n; ++k) {
-      const int64_t a = P.cols[P.p[k].column][i];
-      const int64_t b = P.p[k].is_column ? (int64_t)P.cols[P.p[k].rhs_column][i] : P.p[k].constant;
-      ok = ok && cmp_eval(P.p[k].cmp, a, b);
-    }
-    flags[i] = ok ? 1u : 0u;
-  }
-}
-
-__global__ void k_compact_col(const int32_t* in, const uint32_t* flags, const uint32_t* excl, uint64_t n, int32_t* out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    if (flags[i]) out[excl[i]] = in[i];
-}
-
-__global__ void k_partition_flags(const int32_t* col, uint64_t n, int nparts, int part, uint32_t* flags) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    flags[i] = fj::partition_of(col[i], (uint32_t)nparts) == (uint32_t)part ? 1u : 0u;
-}
+#include "kernels/misc.cuh"
 
 // ============================================================================
 // host: memory pool

@@ -1,0 +1,100 @@
+// common: device helpers: hashing, COLT get, estimated_key_count
+// Included by engine.cu (one translation unit: the kernels share templates and helpers).
+#pragma once
+
+// ============================================================================
+// device helpers
+// ============================================================================
+__device__ __forceinline__ const int32_t* level_src(const DevTrie& T, int depth, int col) {
+  return depth == 0 ? T.base[col] : T.lev[depth - 1].cval[col];
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t key_word_r(int nk, const int32_t (&vals)[N]) {
+  if (nk == 0) return 0u;
+  if (nk == 1) return static_cast<uint32_t>(vals[0]);
+  uint64_t h = fj::kTupleHashSeed;
+#pragma unroll
+  for (int t = 0; t < N; ++t)
+    if (t < nk) h = fj::tuple_hash_step(h, vals[t]);
+  return static_cast<uint32_t>(fj::fmix64(h));
+}
+
+// first bucket (4 slots) of key word kw inside the region of subtrie (p, len)
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+__device__ __forceinline__ uint64_t region_bucket(uint32_t p, uint32_t len, uint32_t kw) {
+  return (uint64_t)p + (((uint64_t)fmix32(kw ^ 0x9e3779b9u) * len) >> 32);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// COLT get (Fig 12 `get` = force, then lookup): the subtrie was forced by an
+// earlier kernel of this node, so this is a pure lookup in its slot region:
+// read a bucket (one sector, as two 16-byte halves), stop at a match or at the
+// first free slot.
+__device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len, const int32_t (&key)[MAXK],
+                                         uint32_t& q, uint32_t& ql) {
+  const int nk = P.nv;
+  const uint32_t kw = key_word_r(nk, key);
+  uint64_t b = region_bucket(p, len, kw);
+  const uint64_t blo = p, bhi = (uint64_t)p + len;
+  const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+  while (true) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const uint4 s = __ldg(tb + 2 * b + half);
+      // slot (s.x, s.y) then (s.z, s.w)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const uint32_t sk = w ? s.z : s.x, sq = w ? s.w : s.y;
+        if (sq == kEmpty) return false;
+        if (sk == kw) {
+          bool eq = true;
+          if (nk >= 2) {
+#pragma unroll
+            for (int t = 0; t < MAXK; ++t)
+              if (t < nk && __ldg(P.kcmp[t] + sq) != key[t]) eq = false;
+          }
+          if (eq) {
+            q = sq;
+            ql = __ldg(P.cnt + sq);
+            return true;
+          }
+        }
+      }
+    }
+    if (++b == bhi) b = blo;
+  }
+}
+
+__device__ __forceinline__ void subtrie_of(const KSub& S, uint64_t e, uint32_t& p, uint32_t& len) {
+  if (S.in_p) {
+    p = __ldg(S.in_p + e);
+    len = __ldg(S.in_len + e);
+  } else {
+    p = 0;
+    len = S.root_n;
+  }
+}
+
+// estimated_key_count: forced map -> #keys, vector -> its
+// length, BaseScan -> cardinality. Never forces.
+__device__ __forceinline__ uint64_t estimate(const KSub& S, uint32_t p, uint32_t len) {
+  if (p == kSingleton) return 1;
+  const uint32_t id = S.depth == 0 ? 0u : p;
+  if (*((volatile const uint32_t*)(S.state + id)) == 2u) return S.nkeys[id];
+  return len;
+}
+

@@ -1,0 +1,230 @@
+// force: batched lazy COLT forcing (Fig 12 force)
+// Included by engine.cu (one translation unit: the kernels share templates and helpers).
+#pragma once
+
+// ============================================================================
+// force: clear -> insert -> assign -> scatter -> finalize  (Fig 12 `force`)
+// ============================================================================
+// Position iteration over the union of claimed ranges. single: one subtrie
+// (p0, len0) given by value (the root BaseScan).
+struct ForceRange {
+  const uint32_t* list_p;
+  const uint32_t* list_len;
+  const uint32_t* list_scan;   // inclusive
+  const uint32_t* list_count;  // device count
+  const uint32_t* owner;       // list entry of every forced offset index (max-scan of start markers)
+  uint32_t p0, len0;
+  int single;
+};
+
+__device__ __forceinline__ uint32_t force_total(const ForceRange& R) {
+  if (R.single) return R.len0;
+  const uint32_t c = *R.list_count;
+  return c ? R.list_scan[c - 1] : 0u;
+}
+
+__device__ __forceinline__ void force_locate(const ForceRange& R, uint32_t i, uint32_t& p, uint32_t& len,
+                                             uint32_t& pos) {
+  if (R.single) {
+    p = R.p0;
+    len = R.len0;
+    pos = R.p0 + i;
+    return;
+  }
+  const uint32_t lo = __ldg(R.owner + i);
+  const uint32_t before = lo ? R.list_scan[lo - 1] : 0u;
+  p = R.list_p[lo];
+  len = R.list_len[lo];
+  pos = p + (i - before);
+}
+
+// owner map, pass 1: mark the first offset index of every listed subtrie
+__global__ void k_force_marks(const uint32_t* __restrict__ list_scan, const uint32_t* __restrict__ list_count,
+                              uint32_t* __restrict__ marks) {
+  const uint32_t c = *list_count;
+  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < c; li += gridDim.x * blockDim.x)
+    marks[li ? list_scan[li - 1] : 0u] = li;
+}
+
+// clear the slot regions (one 4-slot bucket per position) and child counts of
+// the claimed subtries
+__global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
+  const DevLevel& L = tries[trie].lev[lev];
+  const uint32_t total = force_total(R);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
+    uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * pos;
+    t[0] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    t[1] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    L.cnt[pos] = 0;
+    if (L.srep) reinterpret_cast<uint4*>(L.srep)[pos] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// Insert every offset of the claimed subtries: claim a slot for its key (CAS
+// on the 8-byte slot), then count it (the pending slot's q word is the group
+// counter; the returned value is the offset's rank inside its child group).
+template <bool MULTI>
+__global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                               uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
+                               uint32_t* __restrict__ newslots, uint32_t* __restrict__ newslot_p,
+                               DevCounters* ctr) {
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[lev];
+  const uint32_t total = force_total(R);
+  const int nk = L.nk;
+  const int32_t* src[MAXK];
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) src[t] = t < nk ? level_src(T, lev, L.keycol[t]) : nullptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
+    int32_t vals[MAXK];
+#pragma unroll
+    for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
+    const uint32_t kw = key_word_r(nk, vals);
+    const unsigned long long mine = ((unsigned long long)kPendBit << 32) | kw;
+    const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
+    uint64_t h = 4ull * region_bucket(p, len, kw);
+    bool won = false;
+    while (true) {
+      unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
+      unsigned long long cur = *((volatile unsigned long long*)addr);
+      if ((uint32_t)(cur >> 32) == kEmpty) {
+        const unsigned long long old = atomicCAS(addr, cur, mine);
+        if (old == cur) {
+          won = true;
+          if (MULTI) {
+            *((volatile uint32_t*)(L.srep + h)) = pos + 1;
+            __threadfence();
+          }
+          break;
+        }
+        cur = old;
+      }
+      if ((uint32_t)cur == kw) {
+        if (!MULTI) break;
+        uint32_t r;
+        while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
+        }
+        bool eq = true;
+#pragma unroll
+        for (int t = 0; t < MAXK; ++t)
+          if (t < nk && src[t][r - 1] != vals[t]) eq = false;
+        if (eq) break;
+      }
+      if (++h == hi) h = lo;
+    }
+    const uint32_t rank = atomicAdd(&L.table[h].q, 1u) & ~kPendBit;
+    tmp_slot[pos] = (uint32_t)h;
+    tmp_rank[pos] = rank;
+    // warp-aggregated append of new slots
+    const unsigned act = __activemask();
+    const unsigned wmask = __ballot_sync(act, won);
+    if (won) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(wmask) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&ctr->newslots, (uint32_t)__popc(wmask));
+      base = __shfl_sync(wmask, base, leader);
+      const uint32_t o = base + __popc(wmask & ((1u << lane) - 1));
+      newslots[o] = (uint32_t)h;
+      newslot_p[o] = p;
+    }
+  }
+}
+
+// Child-range allocation: q = p + (running sum of child sizes of p).
+template <bool SINGLE>
+__global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0,
+                               const uint32_t* __restrict__ newslots, const uint32_t* __restrict__ newslot_p,
+                               DevCounters* ctr) {
+  const DevLevel& L = tries[trie].lev[lev];
+  const uint32_t total = ctr->newslots;
+  typedef cub::BlockScan<uint32_t, 256> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t s_base;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t iters = (total + stride - 1) / stride;
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
+    const bool ok = i < total;
+    uint32_t h = 0, c = 0, p = 0;
+    if (ok) {
+      h = newslots[i];
+      p = newslot_p[i];
+      c = L.table[h].q & ~kPendBit;
+    }
+    uint32_t q = 0;
+    if (SINGLE) {
+      uint32_t excl, blk_total;
+      BS(tmp).ExclusiveSum(c, excl, blk_total);
+      if (threadIdx.x == 0) {
+        const uint32_t first = blockIdx.x * blockDim.x + it * stride;
+        if (first < total) {
+          const uint32_t nb = min((uint32_t)blockDim.x, total - first);
+          s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);
+          atomicAdd(&L.nkeys[p0], nb);
+        }
+      }
+      __syncthreads();
+      q = s_base + excl;
+      __syncthreads();
+    } else if (ok) {
+      const unsigned act = __activemask();
+      const unsigned grp = __match_any_sync(act, p);
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(grp) - 1;
+      uint32_t pre = 0, tot = 0;
+      unsigned m = grp;
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t cl = __shfl_sync(grp, c, l);
+        if (l < lane) pre += cl;
+        tot += cl;
+      }
+      uint32_t base = 0;
+      if (lane == leader) {
+        base = atomicAdd(&L.cursor[p], tot);
+        atomicAdd(&L.nkeys[p], (uint32_t)__popc(grp));
+      }
+      base = __shfl_sync(grp, base, leader);
+      q = p + base + pre;
+    }
+    if (ok) {
+      L.table[h].q = q;
+      L.cnt[q] = c;
+    }
+  }
+}
+
+__global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                                const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank) {
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[lev];
+  const uint32_t total = force_total(R);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
+    const uint32_t h = tmp_slot[pos];
+    const uint32_t dst = L.table[h].q + tmp_rank[pos];
+    for (int c = 0; c < T.ncols; ++c) {
+      int32_t* out = L.cval[c];
+      if (out) out[dst] = level_src(T, lev, c)[pos];
+    }
+  }
+}
+
+__global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
+  const DevLevel& L = tries[trie].lev[lev];
+  if (R.single) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
+    return;
+  }
+  const uint32_t c = *R.list_count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+    L.state[R.list_p[i]] = 2u;
+}
+

@@ -1,0 +1,688 @@
+// node_fastpaths: shape-specialised node kernels: GJ last / frontier nodes, stream-cover pipeline
+// Included by engine.cu (one translation unit: the kernels share templates and helpers).
+#pragma once
+
+#ifndef FJG_GJ_WARPSEARCH
+#define FJG_GJ_WARPSEARCH 0
+#endif
+#ifndef FJG_GJ_PREFETCH
+#define FJG_GJ_PREFETCH 1
+#endif
+// Fast path for the Generic-Join-shaped aggregating last node: every subatom
+// is a cover over the same single new variable x (triangle C2/C5, 4-clique
+// C4). Per candidate: binding lookup, one coalesced cover read, NS-1 bucket
+// probes, fold into count / checksum -- no generic state machinery.
+template <int NS, int W>
+__global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                  uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
+                                                  int min_var, DevCounters* ctr) {
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const uint64_t* __restrict__ scan = N.scan;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    const uint64_t i = base + threadIdx.x;
+    // binding of candidate i: the tile's bindings [lo, hi] are usually few, so
+    // the warp loads their scan values in one coalesced load and each lane
+    // counts the ones <= i with shuffles; long spans fall back to a search.
+    uint64_t e, j;
+    if (FJG_GJ_WARPSEARCH && hi - lo < 32) {
+      const uint32_t span = (uint32_t)(hi - lo) + 1;
+      const uint64_t sv = lane < (int)span ? __ldg(scan + lo + lane) : ~0ull;
+      uint32_t k = 0;
+      for (uint32_t u = 0; u < span; ++u) k += __shfl_sync(0xffffffffu, sv, u) <= i ? 1u : 0u;
+      const uint64_t prev = __shfl_sync(0xffffffffu, sv, k > 0 ? k - 1 : 0);
+      e = lo + k;
+      j = i - (k > 0 ? prev : (lo ? __ldg(scan + lo - 1) : 0ull));
+    } else {
+      e = i < c1 ? upper_bound_u64(scan, lo, hi, i) : lo;
+      j = i - (e ? __ldg(scan + e - 1) : 0ull);
+    }
+    if (i >= c1) continue;
+    const int ci = N.chosen[e];
+    uint32_t sp[NS], sl[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const KSub& P = N.sub[s];
+      if (P.in_p) {
+        sp[s] = __ldg(P.in_p + e);
+        sl[s] = __ldg(P.in_len + e);
+      } else {
+        sp[s] = 0;
+        sl[s] = P.root_n;
+      }
+    }
+    uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+    int32_t hv[W];  // bound head variables, prefetched off the critical path
+#pragma unroll
+    for (int v = 0; v < W; ++v) hv[v] = (FJG_GJ_PREFETCH && v < N.nhead && v != xvar) ? __ldg(N.in_var[v] + e) : 0;
+    uint32_t cpos = 0;
+    const int32_t* csrc = nullptr;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == ci) {
+        cpos = sp[s] + (uint32_t)j;
+        csrc = N.sub[s].src[0];
+      }
+    const int32_t x = __ldg(csrc + cpos);
+    ++body;
+    bool alive = true;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s == ci || !alive) continue;
+      const KSub& P = N.sub[s];
+      ++probes;
+      const uint32_t kw = (uint32_t)x;
+      uint64_t b = region_bucket(sp[s], sl[s], kw);
+      const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+      const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+      uint32_t q = kEmpty;
+      while (true) {
+        const uint4 h0 = __ldg(tb + 2 * b);
+        if (h0.y == kEmpty) break;
+        if (h0.x == kw) { q = h0.y; break; }
+        if (h0.w == kEmpty) break;
+        if (h0.z == kw) { q = h0.w; break; }
+        const uint4 h1 = __ldg(tb + 2 * b + 1);
+        if (h1.y == kEmpty) break;
+        if (h1.x == kw) { q = h1.y; break; }
+        if (h1.w == kEmpty) break;
+        if (h1.z == kw) { q = h1.w; break; }
+        if (++b == bhi) b = blo;
+      }
+      if (q == kEmpty) {
+        ++misses;
+        alive = false;
+      } else if (P.last) {
+        mult *= __ldg(P.cnt + q);
+      }
+    }
+    if (!alive) continue;
+    uint64_t h = fj::kTupleHashSeed;
+#pragma unroll
+    for (int v = 0; v < W; ++v)
+      if (v < N.nhead) {
+        const int32_t val = (v == xvar) ? x : (FJG_GJ_PREFETCH ? hv[v] : __ldg(N.in_var[v] + e));
+        h = fj::tuple_hash_step(h, (int64_t)val);
+        if (v == min_var) acc_min = min(acc_min, (long long)val);
+      }
+    acc_sum += mult * fj::checksum_word(h);
+    acc_lo += mult;
+    if (acc_lo < mult) ++acc_hi;
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  uint64_t lo2 = acc_lo, hi2 = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
+    const uint64_t sm = lo2 + l2;
+    hi2 += h2 + (sm < lo2 ? 1 : 0);
+    lo2 = sm;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (lo2) {
+      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
+      if (old + lo2 < old) ++hi2;
+    }
+    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
+    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+  }
+}
+
+// ILP variant of k_last_gj for the common case where the new variable x is the
+// last head variable (so the tuple hash is step(prefix(binding), x)): each
+// thread owns a run of R consecutive candidates, split at binding
+// boundaries; inside a run the binding state is loaded once and the R cover
+// reads and R first-bucket probes are issued back to back.
+template <int NS, int R, int W>
+__global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                      uint64_t F, const uint64_t* __restrict__ bounds,
+                                                      int min_var, DevCounters* ctr) {
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const uint64_t* __restrict__ scan = N.scan;
+  const int nhead = N.nhead;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * R; base < c1; base += (uint64_t)gridDim.x * TILE * R) {
+    uint64_t i = base + (uint64_t)threadIdx.x * R;
+    const uint64_t iend = min(i + R, c1);
+    if (i >= iend) continue;
+    const uint64_t t = (i - c0) / TILE;
+    uint64_t e = upper_bound_u64(scan, __ldg(bounds + t), __ldg(bounds + t + 1), i);
+    while (i < iend) {
+      const uint64_t se = __ldg(scan + e);
+      const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
+      const uint64_t bend = min(iend, se);  // this batch: candidates [i, bend) of binding e
+      // binding state
+      const int ci = N.chosen[e];
+      uint32_t sp[NS], sl[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const KSub& P = N.sub[s];
+        if (P.in_p) {
+          sp[s] = __ldg(P.in_p + e);
+          sl[s] = __ldg(P.in_len + e);
+        } else {
+          sp[s] = 0;
+          sl[s] = P.root_n;
+        }
+      }
+      const uint64_t mult0 = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+      uint64_t pre = fj::kTupleHashSeed;
+      long long bmin = LLONG_MAX;
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if (v < nhead - 1) {
+          const int32_t hvv = __ldg(N.in_var[v] + e);
+          pre = fj::tuple_hash_step(pre, (int64_t)hvv);
+          if (v == min_var) bmin = hvv;
+        }
+      uint32_t cbase = 0;
+      const int32_t* csrc = nullptr;
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (s == ci) {
+          cbase = sp[s] + (uint32_t)(i - prev);
+          csrc = N.sub[s].src[0];
+        }
+      // R cover reads
+      int32_t x[R];
+      bool live[R];
+      uint64_t mu[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        live[r] = i + r < bend;
+        x[r] = live[r] ? __ldg(csrc + cbase + r) : 0;
+        mu[r] = mult0;
+        if (live[r]) ++body;
+      }
+      // probes, R first buckets in flight per subatom
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s == ci) continue;
+        const KSub& P = N.sub[s];
+        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+        uint4 h0[R];
+        uint64_t b0[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          b0[r] = region_bucket(sp[s], sl[s], (uint32_t)x[r]);
+          h0[r] = live[r] ? __ldg(tb + 2 * b0[r]) : make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!live[r]) continue;
+          ++probes;
+          const uint32_t kw = (uint32_t)x[r];
+          uint32_t q = kEmpty;
+          bool more = false;
+          if (h0[r].y == kEmpty) {
+          } else if (h0[r].x == kw) {
+            q = h0[r].y;
+          } else if (h0[r].w == kEmpty) {
+          } else if (h0[r].z == kw) {
+            q = h0[r].w;
+          } else {
+            more = true;
+          }
+          if (more) {  // rest of the bucket, then the following buckets
+            uint64_t b = b0[r];
+            uint4 h1 = __ldg(tb + 2 * b + 1);
+            while (true) {
+              if (h1.y == kEmpty) break;
+              if (h1.x == kw) { q = h1.y; break; }
+              if (h1.w == kEmpty) break;
+              if (h1.z == kw) { q = h1.w; break; }
+              if (++b == bhi) b = blo;
+              const uint4 a0 = __ldg(tb + 2 * b);
+              if (a0.y == kEmpty) break;
+              if (a0.x == kw) { q = a0.y; break; }
+              if (a0.w == kEmpty) break;
+              if (a0.z == kw) { q = a0.w; break; }
+              h1 = __ldg(tb + 2 * b + 1);
+            }
+          }
+          if (q == kEmpty) {
+            ++misses;
+            live[r] = false;
+          } else if (P.last) {
+            mu[r] *= __ldg(P.cnt + q);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!live[r]) continue;
+        const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x[r]);
+        acc_sum += mu[r] * fj::checksum_word(h);
+        acc_lo += mu[r];
+        if (acc_lo < mu[r]) ++acc_hi;
+        if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x[r] : bmin);
+      }
+      i = bend;
+      ++e;
+    }
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  uint64_t lo2 = acc_lo, hi2 = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
+    const uint64_t sm = lo2 + l2;
+    hi2 += h2 + (sm < lo2 ? 1 : 0);
+    lo2 = sm;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (lo2) {
+      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
+      if (old + lo2 < old) ++hi2;
+    }
+    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
+    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+  }
+}
+
+#ifndef FJG_GJ_R
+#define FJG_GJ_R 2
+#endif
+#ifndef FJG_GJ_WRITE
+#define FJG_GJ_WRITE 1
+#endif
+#ifndef FJG_STREAM_WRITE
+#define FJG_STREAM_WRITE 1
+#endif
+
+// GJ-shaped frontier-writing node: every subatom is a one-variable cover of the
+// new variable x; atoms whose subatom is not their last continue with the
+// child of their cover (keys mode) or probe (q, cnt[q]). Survivors are
+// block-compacted into the next frontier.
+template <int NS, int W>
+__global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                   uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
+                                                   DevCounters* ctr) {
+  __shared__ uint32_t s_warp[TILE / 32];
+  __shared__ uint32_t s_base;
+  uint64_t probes = 0, misses = 0, body = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t* __restrict__ scan = N.scan;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    const uint64_t i = base + threadIdx.x;
+    bool alive = i < c1;
+    uint64_t e = 0, mult = 1;
+    int32_t x = 0;
+    uint32_t chp[NS], chl[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) chp[s] = chl[s] = 0;
+    if (alive) {
+      e = upper_bound_u64(scan, lo, hi, i);
+      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+      const int ci = N.chosen[e];
+      uint32_t sp[NS], sl[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const KSub& P = N.sub[s];
+        if (P.in_p) {
+          sp[s] = __ldg(P.in_p + e);
+          sl[s] = __ldg(P.in_len + e);
+        } else {
+          sp[s] = 0;
+          sl[s] = P.root_n;
+        }
+      }
+      if (N.in_mult) mult = __ldg(N.in_mult + e);
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (s == ci) {
+          const KSub& S = N.sub[s];
+          const uint32_t pos = sp[s] + (uint32_t)j;
+          if (!S.stream) {  // forced map: distinct keys are the child starts
+            const uint32_t c = __ldg(S.cnt + pos);
+            if (c == 0) alive = false;
+            chp[s] = pos;
+            chl[s] = c;
+          } else {
+            chp[s] = kSingleton;
+            chl[s] = 1;
+          }
+          if (alive) x = __ldg(S.src[0] + pos);
+        }
+      if (alive) ++body;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s == ci || !alive) continue;
+        const KSub& P = N.sub[s];
+        ++probes;
+        const uint32_t kw = (uint32_t)x;
+        uint64_t b = region_bucket(sp[s], sl[s], kw);
+        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+        uint32_t q = kEmpty;
+        while (true) {
+          const uint4 h0 = __ldg(tb + 2 * b);
+          if (h0.y == kEmpty) break;
+          if (h0.x == kw) { q = h0.y; break; }
+          if (h0.w == kEmpty) break;
+          if (h0.z == kw) { q = h0.w; break; }
+          const uint4 h1 = __ldg(tb + 2 * b + 1);
+          if (h1.y == kEmpty) break;
+          if (h1.x == kw) { q = h1.y; break; }
+          if (h1.w == kEmpty) break;
+          if (h1.z == kw) { q = h1.w; break; }
+          if (++b == bhi) b = blo;
+        }
+        if (q == kEmpty) {
+          ++misses;
+          alive = false;
+        } else {
+          const uint32_t ql = __ldg(P.cnt + q);
+          if (P.last)
+            mult *= ql;
+          else {
+            chp[s] = q;
+            chl[s] = ql;
+          }
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, alive);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < TILE / 32; ++w) {
+        const uint32_t c = s_warp[w];
+        s_warp[w] = tot;
+        tot += c;
+      }
+      s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
+    }
+    __syncthreads();
+    if (alive) {
+      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if ((N.out_vars >> v) & 1u) N.out_var[v][o] = (v == xvar) ? x : __ldg(N.in_var[v] + e);
+#pragma unroll
+      for (int a = 0; a < W; ++a)
+        if ((N.out_atoms >> a) & 1u) {
+          uint32_t pa = 0, la = 0;
+          bool here = false;
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            if (N.sub[s].atom == a) {
+              pa = chp[s];
+              la = chl[s];
+              here = true;
+            }
+          if (!here) {
+            pa = __ldg(N.in_p[a] + e);
+            la = __ldg(N.in_len[a] + e);
+          }
+          N.out_p[a][o] = pa;
+          N.out_len[a][o] = la;
+        }
+      if (N.out_mult) N.out_mult[o] = mult;
+    }
+    __syncthreads();
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+  }
+}
+
+// Binary-join-pipeline node (frontier-writing): one cover iterated in stream
+// mode, every other subatom a single-variable probe keyed on a variable the
+// cover binds (C1 chain, C3 star node 0). Cover columns are loaded lazily, in
+// probe order, so a candidate that dies at its first probe reads one column.
+template <int W>
+__global__ void __launch_bounds__(TILE) k_write_stream(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
+                                                       uint64_t F, const uint64_t* __restrict__ bounds,
+                                                       DevCounters* ctr) {
+  __shared__ uint32_t s_warp[TILE / 32];
+  __shared__ uint32_t s_base;
+  uint64_t probes = 0, misses = 0, body = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t* __restrict__ scan = N.scan;
+  const int ci = N.cov[0];
+  const KSub& S = N.sub[ci];
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t = (base - c0) / TILE;
+    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    const uint64_t i = base + threadIdx.x;
+    bool alive = i < c1;
+    uint64_t e = 0, mult = 1;
+    uint32_t pos = 0;
+    int32_t xv[MAXK];
+    uint32_t have = 0;  // bit t: cover column t loaded
+    uint32_t chp[MAXS], chl[MAXS];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) xv[k] = 0;
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) chp[s] = chl[s] = 0;
+    if (alive) {
+      e = upper_bound_u64(scan, lo, hi, i);
+      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+      uint32_t p;
+      if (S.in_p) {
+        p = __ldg(S.in_p + e);
+      } else {
+        p = 0;
+      }
+      pos = p + (uint32_t)j;
+      if (N.in_mult) mult = __ldg(N.in_mult + e);
+      ++body;
+#pragma unroll
+      for (int s = 0; s < MAXS; ++s) {
+        if (s >= N.nsub || s == ci || !alive) continue;
+        const KSub& P = N.sub[s];
+        // key: the cover column bound to P's variable (loaded on first use)
+        int tk = 0;
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k < S.nv && S.var[k] == P.var[0]) tk = k;
+        int32_t key = 0;
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k == tk) {
+            if (!((have >> k) & 1u)) {
+              xv[k] = __ldg(S.src[k] + pos);
+              have |= 1u << k;
+            }
+            key = xv[k];
+          }
+        uint32_t pp, pl;
+        if (P.in_p) {
+          pp = __ldg(P.in_p + e);
+          pl = __ldg(P.in_len + e);
+        } else {
+          pp = 0;
+          pl = P.root_n;
+        }
+        ++probes;
+        const uint32_t kw = (uint32_t)key;
+        uint64_t b = region_bucket(pp, pl, kw);
+        const uint64_t blo = pp, bhi = (uint64_t)pp + pl;
+        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
+        uint32_t q = kEmpty;
+        while (true) {
+          const uint4 h0 = __ldg(tb + 2 * b);
+          if (h0.y == kEmpty) break;
+          if (h0.x == kw) { q = h0.y; break; }
+          if (h0.w == kEmpty) break;
+          if (h0.z == kw) { q = h0.w; break; }
+          const uint4 h1 = __ldg(tb + 2 * b + 1);
+          if (h1.y == kEmpty) break;
+          if (h1.x == kw) { q = h1.y; break; }
+          if (h1.w == kEmpty) break;
+          if (h1.z == kw) { q = h1.w; break; }
+          if (++b == bhi) b = blo;
+        }
+        if (q == kEmpty) {
+          ++misses;
+          alive = false;
+        } else {
+          const uint32_t ql = __ldg(P.cnt + q);
+          if (P.last)
+            mult *= ql;
+          else {
+            chp[s] = q;
+            chl[s] = ql;
+          }
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, alive);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < TILE / 32; ++w) {
+        const uint32_t c = s_warp[w];
+        s_warp[w] = tot;
+        tot += c;
+      }
+      s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
+    }
+    __syncthreads();
+    if (alive) {
+      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if ((N.out_vars >> v) & 1u) {
+          int32_t val = 0;
+          bool cov = false;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            if (k < S.nv && S.var[k] == v) {
+              val = ((have >> k) & 1u) ? xv[k] : __ldg(S.src[k] + pos);
+              cov = true;
+            }
+          N.out_var[v][o] = cov ? val : __ldg(N.in_var[v] + e);
+        }
+#pragma unroll
+      for (int a = 0; a < W; ++a)
+        if ((N.out_atoms >> a) & 1u) {
+          uint32_t pa = 0, la = 0;
+          bool here = false;
+#pragma unroll
+          for (int s = 0; s < MAXS; ++s)
+            if (s < N.nsub && N.sub[s].atom == a) {
+              pa = s == ci ? kSingleton : chp[s];
+              la = s == ci ? 1u : chl[s];
+              here = true;
+            }
+          if (!here) {
+            pa = __ldg(N.in_p[a] + e);
+            la = __ldg(N.in_len[a] + e);
+          }
+          N.out_p[a][o] = pa;
+          N.out_len[a][o] = la;
+        }
+      if (N.out_mult) N.out_mult[o] = mult;
+    }
+    __syncthreads();
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+  }
+}
+
+// The stream fast path: a single cover in stream mode whose subtrie is never a
+// singleton, all its variables fresh; every other subatom probes one variable
+// the cover binds.
+static bool stream_write_ok(const DevNode& N, const KNode& G) {
+  if (N.ncov != 1 || N.nsub < 2) return false;
+  const DevSub& C = N.sub[N.cov[0]];
+  if (!C.stream || C.bound_mask || C.nv < 1) return false;
+  if (G.sub[N.cov[0]].in_p == nullptr && C.depth != 0) return false;
+  for (int s = 0; s < N.nsub; ++s) {
+    if (s == N.cov[0]) continue;
+    const DevSub& P = N.sub[s];
+    if (P.nv != 1) return false;
+    bool found = false;
+    for (int t = 0; t < C.nv; ++t)
+      if (C.var[t] == P.var[0]) found = true;
+    if (!found) return false;
+  }
+  return true;
+}
+
+// A frontier-writing node is GJ-shaped when every subatom is a one-variable
+// cover of the same fresh variable (levels of depth >= 0, no bound check).
+static int gj_write_var(const DevNode& N, int width) {
+  if (N.nsub < 2 || N.nsub > 3 || N.ncov != N.nsub || width > 8) return -1;
+  int x = -1;
+  for (int s = 0; s < N.nsub; ++s) {
+    const DevSub& D = N.sub[s];
+    if (D.nv != 1 || D.bound_mask) return -1;
+    if (x >= 0 && D.var[0] != x) return -1;
+    x = D.var[0];
+  }
+  return x;
+}
+
+// The GJ fast path applies when every subatom of the node is a one-variable
+// cover of the same new, unbound variable, and no subtrie can be a streamed
+// singleton (all subatoms keys-or-stream levels of depth >= 0 with nv == 1).
+static int gj_last_var(const KNode& G, const DevNode& N) {
+  if (N.nsub < 2 || N.nsub > 3 || N.ncov != N.nsub || N.nhead > 8) return -1;
+  int x = -1;
+  for (int s = 0; s < N.nsub; ++s) {
+    const DevSub& D = N.sub[s];
+    if (D.nv != 1 || D.bound_mask || !D.stream) return -1;
+    if (x >= 0 && D.var[0] != x) return -1;
+    x = D.var[0];
+  }
+  // every earlier subatom of these atoms bound variables (no singleton residuals)
+  for (int s = 0; s < N.nsub; ++s)
+    if (G.sub[s].in_p == nullptr && N.sub[s].depth != 0) return -1;
+  return x;
+}
+

@@ -1,0 +1,76 @@
+// select: k_select: dynamic cover, candidate counts, force claims
+// Included by engine.cu (one translation unit: the kernels share templates and helpers).
+#pragma once
+
+// ============================================================================
+// k_select: cover choice, candidate counts, force claims
+// ============================================================================
+__device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters* ctr, const KSub& S, uint32_t p,
+                                              uint32_t len, bool need) {
+  // Warp-level dedup of identical subtries (bindings of one parent are
+  // adjacent in the frontier), then a CAS on the state word.
+  const unsigned act = __activemask();
+  const unsigned want = __ballot_sync(act, need);
+  if (!need) return;
+  const unsigned grp = __match_any_sync(want, p);
+  const int leader = __ffs(grp) - 1;
+  if ((int)(threadIdx.x & 31) != leader) return;
+  if (S.depth == 0) {
+    ctr->root_need[S.trie] = 1;
+    return;
+  }
+  const DevLevel& L = tries[S.trie].lev[S.depth];
+  if (atomicCAS(L.state + p, 0u, 1u) == 0u) {
+    L.cursor[p] = 0;
+    L.nkeys[p] = 0;
+    const uint32_t idx = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], 1u);
+    L.list_p[idx] = p;
+    L.list_len[idx] = len;
+  }
+}
+
+__global__ void k_select(const __grid_constant__ KNode N, const DevTrie* __restrict__ tries, uint64_t F,
+                         int dynamic, DevCounters* ctr) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t iters = (F + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t e = start + it * stride;
+    const bool ok = e < F;
+    int best = N.cov[0];
+    uint32_t bp = 0, bl = 0;
+    if (ok) {
+      subtrie_of(N.sub[best], e, bp, bl);
+      if (dynamic && N.ncov > 1) {
+        uint64_t best_est = estimate(N.sub[best], bp, bl);
+        for (int ci = 1; ci < N.ncov; ++ci) {
+          const int s = N.cov[ci];
+          uint32_t p, l;
+          subtrie_of(N.sub[s], e, p, l);
+          const uint64_t est = estimate(N.sub[s], p, l);
+          if (est < best_est) {  // ties keep the lowest position
+            best_est = est;
+            best = s;
+            bp = p;
+            bl = l;
+          }
+        }
+      }
+      N.chosen[e] = (uint8_t)best;
+      N.m[e] = (bp == kSingleton) ? 1ull : (uint64_t)bl;
+    }
+    // claims: the keys-iterated cover and every probed subatom must be forced
+    for (int s = 0; s < N.nsub; ++s) {
+      const KSub& S = N.sub[s];
+      uint32_t p = 0, l = 0;
+      bool need = false;
+      if (ok) {
+        subtrie_of(S, e, p, l);
+        need = (p != kSingleton) && (s != best || !S.stream);
+        if (need) need = *((volatile const uint32_t*)(S.state + (S.depth == 0 ? 0u : p))) == 0u;
+      }
+      claim_subtrie(tries, ctr, S, p, l, need);
+    }
+  }
+}
+
