@@ -1148,38 +1148,48 @@ int fjg_relation_filter(const fjg_relation* in, const fjg_predicate* preds, int 
 // Stable hash-partition of `in` on column `col`: rows for destination d land in
 // out_cols[c][base_d ...) in their original order (flags -> scan -> compact per
 // destination).
+// Stable hash-partition of `in` on column `col` (counting sort by destination,
+// one host sync): rows for destination d land in out_cols[c][base_d ...) in
+// their original order.
 static void partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_cols, uint64_t* counts) {
   fjg_engine* eng = in->eng;
   if (col < 0 || col >= in->ncols) throw fj::ValidationError("partition column out of range");
   if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
   const uint64_t n = in->nrows;
-  uint32_t* flags = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
-  uint32_t* excl = (uint32_t*)eng->pool->alloc(std::max<uint64_t>(n, 1) * 4);
-  size_t bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, excl, (int64_t)std::max<uint64_t>(n, 1)));
-  void* tmp = eng->pool->alloc(bytes);
-  uint64_t base = 0;
-  for (int d = 0; d < nparts; ++d) {
-    uint32_t total = 0;
-    if (n) {
-      LAUNCH(eng, k_partition_flags<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[col], n, nparts, d, flags));
-      size_t b = bytes;
-      CK(cub::DeviceScan::ExclusiveSum(tmp, b, flags, excl, (int64_t)n, eng->stream));
-      uint32_t last[2];
-      CK(cudaMemcpyAsync(&last[0], excl + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
-      CK(cudaMemcpyAsync(&last[1], flags + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
-      CK(cudaStreamSynchronize(eng->stream));
-      total = last[0] + last[1];
-      for (int c = 0; c < in->ncols; ++c)
-        LAUNCH(eng, k_compact_col<<<grid_for(n), 256, 0, eng->stream>>>(in->cols[c], flags, excl, n,
-                                                                      out_cols[c] + base));
-    }
-    counts[d] = total;
-    base += total;
+  if (n == 0) {
+    for (int d = 0; d < nparts; ++d) counts[d] = 0;
+    return;
   }
+  const uint32_t nblocks = (uint32_t)((n + kPartChunk - 1) / kPartChunk);
+  const uint64_t nh = (uint64_t)nparts * nblocks;
+  uint32_t* hist = (uint32_t*)eng->pool->alloc((nh + 1) * 4);
+  uint32_t* offs = (uint32_t*)eng->pool->alloc((nh + 1) * 4);
+  uint32_t* tot = (uint32_t*)eng->pool->alloc((nparts + 1) * 4);
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, offs, (int64_t)(nh + 1)));
+  void* tmp = eng->pool->alloc(bytes);
+  const size_t smem = (size_t)nparts * 4 * (PART_WARPS + 1);
+  CK(cudaMemsetAsync(hist + nh, 0, 4, eng->stream));
+  LAUNCH(eng, k_part_count<<<nblocks, 256, (size_t)nparts * 4, eng->stream>>>(in->cols[col], n, nparts, nblocks,
+                                                                              hist));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, hist, offs, (int64_t)(nh + 1), eng->stream));
+  ++eng->launches;
+  DevPartCols pc{};
+  pc.ncols = in->ncols;
+  for (int c = 0; c < in->ncols; ++c) {
+    pc.in[c] = in->cols[c];
+    pc.out[c] = out_cols[c];
+  }
+  LAUNCH(eng, k_part_scatter<<<nblocks, 256, smem, eng->stream>>>(pc, col, n, nparts, nblocks, offs));
+  LAUNCH(eng, k_part_totals<<<grid_for(nparts + 1), 256, 0, eng->stream>>>(offs, nparts, nblocks, tot));
+  std::vector<uint32_t> h(nparts + 1);
+  CK(cudaMemcpyAsync(h.data(), tot, (nparts + 1) * 4, cudaMemcpyDeviceToHost, eng->stream));
   CK(cudaStreamSynchronize(eng->stream));
-  eng->pool->free(flags);
-  eng->pool->free(excl);
+  ++eng->syncs;
+  for (int d = 0; d < nparts; ++d) counts[d] = h[d + 1] - h[d];
+  eng->pool->free(hist);
+  eng->pool->free(offs);
+  eng->pool->free(tot);
   eng->pool->free(tmp);
 }
 

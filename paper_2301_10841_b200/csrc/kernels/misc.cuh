@@ -47,8 +47,72 @@ __global__ void k_compact_col(const int32_t* in, const uint32_t* flags, const ui
     if (flags[i]) out[excl[i]] = in[i];
 }
 
-__global__ void k_partition_flags(const int32_t* col, uint64_t n, int nparts, int part, uint32_t* flags) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    flags[i] = fj::partition_of(col[i], (uint32_t)nparts) == (uint32_t)part ? 1u : 0u;
+// Stable hash partition (multi-GPU sharding on the first plan variable):
+// counting sort by destination. Block b owns rows [b*kPartChunk, ...); hist is
+// destination-major (d * nblocks + b) so its exclusive scan gives every
+// (destination, block) its output base.
+constexpr uint32_t kPartChunk = 8192;
+constexpr int PART_WARPS = 8;
+
+struct DevPartCols {
+  int ncols;
+  const int32_t* in[MAXC];
+  int32_t* out[MAXC];
+};
+
+__global__ void k_part_count(const int32_t* __restrict__ key, uint64_t n, int nparts, uint32_t nblocks,
+                             uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t s_cnt[];
+  for (int d = threadIdx.x; d < nparts; d += blockDim.x) s_cnt[d] = 0;
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * kPartChunk, hi = min(n, lo + kPartChunk);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+    atomicAdd(&s_cnt[fj::partition_of(key[i], (uint32_t)nparts)], 1u);
+  __syncthreads();
+  for (int d = threadIdx.x; d < nparts; d += blockDim.x) hist[(uint64_t)d * nblocks + blockIdx.x] = s_cnt[d];
+}
+
+__global__ void k_part_scatter(DevPartCols pc, int col, uint64_t n, int nparts, uint32_t nblocks,
+                               const uint32_t* __restrict__ offs) {
+  extern __shared__ uint32_t s_mem[];
+  uint32_t* s_run = s_mem;               // [nparts] rows already placed per destination
+  uint32_t* s_wc = s_mem + nparts;       // [PART_WARPS][nparts] per-warp counts of this round
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < nparts; d += blockDim.x) s_run[d] = 0;
+  const uint64_t lo = (uint64_t)blockIdx.x * kPartChunk, hi = min(n, lo + kPartChunk);
+  for (uint64_t r0 = lo; r0 < hi; r0 += blockDim.x) {
+    for (int t = threadIdx.x; t < PART_WARPS * nparts; t += blockDim.x) s_wc[t] = 0;
+    __syncthreads();
+    const uint64_t i = r0 + threadIdx.x;
+    const bool ok = i < hi;
+    const uint32_t d = ok ? fj::partition_of(pc.in[col][i], (uint32_t)nparts) : 0u;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    unsigned grp = 0;
+    if (ok) {
+      grp = __match_any_sync(act, d);
+      if (lane == __ffs(grp) - 1) s_wc[warp * nparts + d] = __popc(grp);
+    }
+    __syncthreads();
+    if (ok) {
+      uint32_t before = s_run[d];
+      for (int w = 0; w < warp; ++w) before += s_wc[w * nparts + d];
+      const uint64_t o = (uint64_t)offs[(uint64_t)d * nblocks + blockIdx.x] + before +
+                         __popc(grp & ((1u << lane) - 1));
+      for (int c = 0; c < pc.ncols; ++c) pc.out[c][o] = pc.in[c][i];
+    }
+    __syncthreads();
+    for (int dd = threadIdx.x; dd < nparts; dd += blockDim.x) {
+      uint32_t add = 0;
+      for (int w = 0; w < PART_WARPS; ++w) add += s_wc[w * nparts + dd];
+      s_run[dd] += add;
+    }
+    __syncthreads();
+  }
+}
+
+// tot[d] = base of destination d (tot[nparts] = n)
+__global__ void k_part_totals(const uint32_t* __restrict__ offs, int nparts, uint32_t nblocks, uint32_t* tot) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d <= nparts; d += gridDim.x * blockDim.x)
+    tot[d] = offs[(uint64_t)d * nblocks];
 }
 

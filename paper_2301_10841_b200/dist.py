@@ -47,36 +47,54 @@ def local_slice(n, world, rank):
     return lo, hi
 
 
-def all_to_all_partitioned(cols, col, world, ops, group=None):
-    """Send each row to rank partition_of(row[col]); returns this rank's rows."""
+def _reuse(out, i, n, ops):
+    """out[i] if it exists with n rows (persistent exchange buffers), else a new buffer."""
+    if out is not None and i < len(out) and out[i].numel() == n:
+        return out[i]
+    return ops.empty(n)
+
+
+def all_to_all_partitioned(cols, col, world, ops, group=None, out=None):
+    """Send each row to rank partition_of(row[col]); returns this rank's rows
+    (written into `out` when its buffers have the right sizes)."""
     grouped, counts = ops.partition(cols, col, world)
     send = torch.tensor(counts, dtype=torch.int64, device=ops.device)
     recv = torch.empty(world, dtype=torch.int64, device=ops.device)
     dist.all_to_all_single(recv, send, group=group)
     rc = [int(x) for x in recv.tolist()]
-    out = []
-    for g in grouped:
-        o = ops.empty(sum(rc))
+    res = []
+    for i, g in enumerate(grouped):
+        o = _reuse(out, i, sum(rc), ops)
         dist.all_to_all_single(o, g, output_split_sizes=rc, input_split_sizes=counts, group=group)
-        out.append(o)
-    return out
+        res.append(o)
+    return res
 
 
-def all_gather_rows(cols, world, ops, group=None):
+def all_gather_rows(cols, world, ops, group=None, out=None):
     n = cols[0].numel() if cols else 0
     sizes = [torch.zeros(1, dtype=torch.int64, device=ops.device) for _ in range(world)]
     dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=ops.device), group=group)
     sizes = [int(s.item()) for s in sizes]
     m = max(sizes) if sizes else 0
-    out = []
-    for c in cols:
+    res = []
+    for i, c in enumerate(cols):
+        if world == 1:
+            o = _reuse(out, i, n, ops)
+            o.copy_(c)
+            res.append(o)
+            continue
         pad = ops.empty(m)
         if n:
             pad[:n].copy_(c)
         buf = ops.empty(m * world)
         dist.all_gather_into_tensor(buf, pad, group=group)
-        out.append(torch.cat([buf[r * m: r * m + sizes[r]] for r in range(world)]) if world > 1 else buf[:n])
-    return out
+        o = _reuse(out, i, sum(sizes), ops)
+        off = 0
+        for r in range(world):
+            o[off: off + sizes[r]].copy_(buf[r * m: r * m + sizes[r]])
+            off += sizes[r]
+        res.append(o)
+    return res
 
 
 def reduce_results(count, checksum, minv, device, group=None):
@@ -95,15 +113,17 @@ def reduce_results(count, checksum, minv, device, group=None):
     return total, cs, (None if mv == INT64_MAX else mv)
 
 
-def exchange(relations, views, world, rank, ops, group=None):
+def exchange(relations, views, world, rank, ops, group=None, bufs=None):
     """relations: base -> list of local-slice column tensors. Returns
-    view -> list of column tensors held by this rank after the exchange."""
+    view -> list of column tensors held by this rank after the exchange
+    (reusing `bufs`, the previous step's result, when sizes match)."""
     out = {}
     for view in sorted(set(views), key=lambda v: (v[0], -1 if v[1] is None else v[1])):
         base, col = view
         cols = relations[base]
-        out[view] = all_gather_rows(cols, world, ops, group) if col is None else \
-            all_to_all_partitioned(cols, col, world, ops, group)
+        prev = bufs.get(view) if bufs else None
+        out[view] = all_gather_rows(cols, world, ops, group, prev) if col is None else \
+            all_to_all_partitioned(cols, col, world, ops, group, prev)
     return out
 
 
@@ -113,15 +133,17 @@ class DeviceOps:
     def __init__(self, engine):
         self.engine = engine
         self.device = torch.device("cuda", engine.device)
+        self._send = {}  # (column pointers, key column) -> persistent send buffers
 
     def empty(self, n):
         return torch.empty(n, dtype=torch.int32, device=self.device)
 
     def partition(self, cols, col, world):
-        rel = self.engine.relation_from_torch(cols)
-        grouped = [self.empty(cols[0].numel()) for _ in cols]
+        key = (tuple(c.data_ptr() for c in cols), col)
+        if key not in self._send:
+            self._send[key] = (self.engine.relation_from_torch(cols), [self.empty(cols[0].numel()) for _ in cols])
+        rel, grouped = self._send[key]
         counts = rel.partition_into(col, world, [g.data_ptr() for g in grouped])
-        rel.close()
         return grouped, counts
 
 
@@ -150,9 +172,12 @@ class ShardedQuery:
         self._q = self.engine.query({"query": self.w.query}, self.plan, [rels[v] for v in self.views])
 
     def execute(self, min_var=None, timing=False, **kw):
-        held = exchange(self.local, self.views, self.world, self.rank, self.ops, self.group)
+        prev = getattr(self, "_held", None)
+        held = exchange(self.local, self.views, self.world, self.rank, self.ops, self.group, prev)
         torch.cuda.current_stream(self.ops.device).synchronize()
-        self._bind(held)  # zero-copy relations over the exchanged buffers
+        same = prev is not None and all(h is p for v in held for h, p in zip(held[v], prev[v]))
+        if self._q is None or not same:
+            self._bind(held)  # zero-copy relations over the exchanged buffers, bound once
         r = self._q.execute(min_var=min_var, timing=timing, **kw)
         r.extra["local_count"] = r.count
         r.count, r.checksum, r.min_value = reduce_results(r.count, r.checksum, r.min_value, self.ops.device,
