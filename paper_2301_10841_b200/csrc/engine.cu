@@ -242,6 +242,7 @@ struct fjg_query {
   uint32_t* newslots = nullptr;
   uint32_t* newslot_p = nullptr;
   uint32_t* owner_scratch = nullptr;  // force: offset index -> claimed subtrie
+  uint8_t* sort_flags = nullptr;      // sorted root force: group-start flags
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
   int32_t* out_tuples = nullptr;
@@ -426,6 +427,7 @@ static void prepare_query(fjg_query* q) {
   q->newslots = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->newslot_p = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->owner_scratch = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
+  q->sort_flags = (uint8_t*)q->alloc(std::max<uint64_t>(q->max_n, 1));
   if (q->max_n >= (1ull << 31)) throw ValidationError("relations must have fewer than 2^31 rows");
   // static node descriptors
   const size_t K = plan.nodes.size();
@@ -704,7 +706,13 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   size_t b3 = 0;
   CK(cub::DeviceScan::InclusiveScan(nullptr, b3, (uint32_t*)nullptr, (uint32_t*)nullptr, MaxOp(),
                                     (int64_t)std::max<uint64_t>(q->max_n, 1)));
-  size_t need = std::max(std::max(b1, b2), b3);
+  size_t b4 = 0, b5 = 0;
+  const int64_t nm = (int64_t)std::max<uint64_t>(q->max_n, 1);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, b4, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                     (uint32_t*)nullptr, nm));
+  CK(cub::DeviceSelect::Flagged(nullptr, b5, cub::CountingInputIterator<uint32_t>(0), (uint8_t*)nullptr,
+                                (uint32_t*)nullptr, (uint32_t*)nullptr, nm));
+  size_t need = std::max(std::max(std::max(b1, b2), b3), std::max(b4, b5));
   if (need > q->cub_tmp_bytes) {
     q->cub_tmp = q->alloc(need);
     q->cub_tmp_bytes = need;
@@ -726,10 +734,52 @@ static void sync_counters(fjg_query* q) {
 }
 
 // Force the listed subtries of (trie t, level l): Fig 12 `force` in batch.
+#ifndef FJG_SORTED_ROOT
+#define FJG_SORTED_ROOT 1
+#endif
+// Sort-based root force (arity <= 1 keys): see kernels/force.cuh.
+static void force_root_sorted(fjg_query* q, int t) {
+  fjg_engine* eng = q->eng;
+  auto& T = q->tries[t];
+  const uint32_t n = (uint32_t)T.rel->nrows;
+  q->mark(eng->stream, -1);
+  ForceRange R{};
+  R.single = 1;
+  R.p0 = 0;
+  R.len0 = n;
+  const unsigned g = grid_for(n, 256, eng->num_sms * 16);
+  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, 0, R));
+  uint32_t *keys = q->tmp_slot, *rows = q->tmp_rank, *skeys = q->newslots, *srows = q->newslot_p;
+  uint32_t* starts = q->owner_scratch;
+  uint8_t* flags = q->sort_flags;
+  uint32_t* ng = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, survivors));
+  LAUNCH(eng, k_root_keys<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, keys, rows));
+  size_t bytes = q->cub_tmp_bytes;
+  const int kb = T.levels[0].empty() ? 1 : 32;
+  CK(cub::DeviceRadixSort::SortPairs(q->cub_tmp, bytes, keys, skeys, rows, srows, (int64_t)n, 0, kb, eng->stream));
+  ++eng->launches;
+  LAUNCH(eng, k_root_starts<<<g, 256, 0, eng->stream>>>(skeys, n, flags));
+  bytes = q->cub_tmp_bytes;
+  CK(cub::DeviceSelect::Flagged(q->cub_tmp, bytes, cub::CountingInputIterator<uint32_t>(0), flags, starts, ng,
+                                (int64_t)n, eng->stream));
+  ++eng->launches;
+  LAUNCH(eng, k_root_insert<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, skeys, starts, ng, q->d_ctr));
+  LAUNCH(eng, k_root_gather<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, srows));
+  q->mark(eng->stream, 0);
+  q->forces += 1;
+  q->maps_built += 1;
+  q->rows_forced += n;
+  T.lev[0].dirty = true;
+}
+
 static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, uint32_t len0, uint32_t count) {
   fjg_engine* eng = q->eng;
   auto& T = q->tries[t];
   DevLevel& L = T.dev.lev[l];
+  if (single && l == 0 && T.levels[0].size() <= 1 && len0 >= (1u << 21) && FJG_SORTED_ROOT) {
+    force_root_sorted(q, t);
+    return;
+  }
   ForceRange R{};
   R.single = single ? 1 : 0;
   R.p0 = p0;

@@ -228,3 +228,62 @@ __global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, in
     L.state[R.list_p[i]] = 2u;
 }
 
+
+// ---------------------------------------------------------------------------
+// Sort-based force of a root (the single subtrie [0, n) of level 0) with a
+// key of arity <= 1: radix-sort (key, row), mark group starts, insert one slot
+// per distinct key (no contention), gather the clustered columns. Produces the
+// same structure as the atomic path without per-row atomics on hot keys.
+__global__ void k_root_keys(const DevTrie* __restrict__ tries, int trie, uint32_t n, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ rows) {
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[0];
+  const int32_t* kc = L.nk ? T.base[L.keycol[0]] : nullptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    keys[i] = kc ? (uint32_t)kc[i] : 0u;
+    rows[i] = i;
+  }
+}
+
+__global__ void k_root_starts(const uint32_t* __restrict__ skeys, uint32_t n, uint8_t* __restrict__ flags) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
+}
+
+// one thread per distinct key: its group is [starts[g], starts[g+1])
+__global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint32_t n, const uint32_t* __restrict__ skeys,
+                              const uint32_t* __restrict__ starts, const uint32_t* __restrict__ ngroups,
+                              DevCounters* ctr) {
+  const DevLevel& L = tries[trie].lev[0];
+  const uint32_t G = *ngroups;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    const uint32_t q = starts[g];
+    const uint32_t c = (g + 1 < G ? starts[g + 1] : n) - q;
+    const uint32_t kw = skeys[q];
+    const uint64_t lo = 0, hi = 4ull * n;
+    uint64_t h = 4ull * region_bucket(0u, n, kw);
+    const unsigned long long mine = ((unsigned long long)q << 32) | kw;
+    while (true) {
+      unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
+      if (atomicCAS(addr, kEmpty64, mine) == kEmpty64) break;
+      if (++h == hi) h = lo;
+    }
+    L.cnt[q] = c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    L.nkeys[0] = G;
+    L.state[0] = 2u;
+    ctr->newslots = G;
+  }
+}
+
+__global__ void k_root_gather(const DevTrie* __restrict__ tries, int trie, uint32_t n,
+                              const uint32_t* __restrict__ srows) {
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[0];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t r = srows[i];
+    for (int c = 0; c < T.ncols; ++c)
+      if (L.cval[c]) L.cval[c][i] = T.base[c][r];
+  }
+}
