@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <map>
 #include <memory>
 #include <set>
@@ -710,7 +711,7 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   const int64_t nm = (int64_t)std::max<uint64_t>(q->max_n, 1);
   CK(cub::DeviceRadixSort::SortPairs(nullptr, b4, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                      (uint32_t*)nullptr, nm));
-  CK(cub::DeviceSelect::Flagged(nullptr, b5, cub::CountingInputIterator<uint32_t>(0), (uint8_t*)nullptr,
+  CK(cub::DeviceSelect::Flagged(nullptr, b5, thrust::counting_iterator<uint32_t>(0), (uint8_t*)nullptr,
                                 (uint32_t*)nullptr, (uint32_t*)nullptr, nm));
   size_t need = std::max(std::max(std::max(b1, b2), b3), std::max(b4, b5));
   if (need > q->cub_tmp_bytes) {
@@ -760,7 +761,7 @@ static void force_root_sorted(fjg_query* q, int t) {
   ++eng->launches;
   LAUNCH(eng, k_root_starts<<<g, 256, 0, eng->stream>>>(skeys, n, flags));
   bytes = q->cub_tmp_bytes;
-  CK(cub::DeviceSelect::Flagged(q->cub_tmp, bytes, cub::CountingInputIterator<uint32_t>(0), flags, starts, ng,
+  CK(cub::DeviceSelect::Flagged(q->cub_tmp, bytes, thrust::counting_iterator<uint32_t>(0), flags, starts, ng,
                                 (int64_t)n, eng->stream));
   ++eng->launches;
   LAUNCH(eng, k_root_insert<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, skeys, starts, ng, q->d_ctr));

@@ -2,6 +2,15 @@
 // Included by engine.cu (one translation unit: the kernels share templates and helpers).
 #pragma once
 
+// streaming (read-once) loads: evict-first so the probed slot regions keep L2
+#ifndef FJG_STREAM_HINT
+#define FJG_STREAM_HINT 0
+#endif
+#if FJG_STREAM_HINT
+#define FJG_LD_STREAM(p) __ldcs(p)
+#else
+#define FJG_LD_STREAM(p) __ldg(p)
+#endif
 #ifndef FJG_GJ_WARPSEARCH
 #define FJG_GJ_WARPSEARCH 0
 #endif
@@ -175,8 +184,8 @@ __global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KN
       for (int s = 0; s < NS; ++s) {
         const KSub& P = N.sub[s];
         if (P.in_p) {
-          sp[s] = __ldg(P.in_p + e);
-          sl[s] = __ldg(P.in_len + e);
+          sp[s] = FJG_LD_STREAM(P.in_p + e);
+          sl[s] = FJG_LD_STREAM(P.in_len + e);
         } else {
           sp[s] = 0;
           sl[s] = P.root_n;
@@ -188,7 +197,7 @@ __global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KN
 #pragma unroll
       for (int v = 0; v < W; ++v)
         if (v < nhead - 1) {
-          const int32_t hvv = __ldg(N.in_var[v] + e);
+          const int32_t hvv = FJG_LD_STREAM(N.in_var[v] + e);
           pre = fj::tuple_hash_step(pre, (int64_t)hvv);
           if (v == min_var) bmin = hvv;
         }
@@ -207,7 +216,7 @@ __global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KN
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         live[r] = i + r < bend;
-        x[r] = live[r] ? __ldg(csrc + cbase + r) : 0;
+        x[r] = live[r] ? FJG_LD_STREAM(csrc + cbase + r) : 0;
         mu[r] = mult0;
         if (live[r]) ++body;
       }
