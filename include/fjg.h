@@ -164,7 +164,8 @@ int fjg_relation_partition_into(const fjg_relation* in, int col, int nparts, int
                                 uint64_t* counts);
 
 /* ---- queries: build phase + join phase ----
- * query_json: {"query":[{"rel":..,"vars":[..]},..]}; plan_json: a Free Join
+ * query_json: {"query":[{"rel":..,"vars":[..]},..], "head": [..] (optional:
+ * the output/checksum variable order, default first appearance)}; plan_json: a Free Join
  * plan in the SPEC.md:171 dialect. atom_rels[i] binds query atom i; several
  * atoms may bind the same relation (renamed self-joins) and
  * then share device COLT levels. */
@@ -178,6 +179,10 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out);
  * row-major, num_head_vars int32 each, unsorted bag) to host_out. */
 int fjg_query_output(fjg_query* q, int32_t* host_out, uint64_t cap_rows, uint64_t* rows);
 int fjg_query_num_head_vars(const fjg_query* q);
+/* run_segments: the enumerated output as a new device
+ * relation (one int32 column per head variable), for use as an atom of the
+ * parent segment of a bushy plan. */
+int fjg_query_output_relation(fjg_query* q, fjg_relation** out);
 void fjg_query_destroy(fjg_query* q);
 
 /* ---- test hooks ---- */

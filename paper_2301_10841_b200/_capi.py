@@ -93,6 +93,7 @@ def _load():
         "fjg_execute": (I, [P, C.POINTER(ExecOptions), C.POINTER(Result)]),
         "fjg_query_output": (I, [P, P, U64, C.POINTER(U64)]),
         "fjg_query_num_head_vars": (I, [P]),
+        "fjg_query_output_relation": (I, [P, C.POINTER(P)]),
         "fjg_query_destroy": (None, [P]),
         "fjg_device_tuple_hash": (I, [P, P, I, U64, P]),
         "fjg_host_tuple_hash": (U64, [P, I]),
@@ -112,7 +113,7 @@ EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_o
             "fjg_relation_filter", "fjg_relation_rows", "fjg_relation_cols", "fjg_relation_device_col",
             "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition",
             "fjg_relation_partition_into", "fjg_query_create",
-            "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_destroy",
+            "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_output_relation", "fjg_query_destroy",
             "fjg_device_tuple_hash", "fjg_host_tuple_hash"]
 
 

@@ -227,6 +227,7 @@ struct fjg_query {
   fjg_engine* eng = nullptr;
   fj::FreeJoinPlan plan;
   std::vector<std::string> head;  // variable names, id order
+  std::vector<std::string> head_override;
   std::vector<AtomInfo> atoms;
   std::vector<fjg_relation*> rels;
   std::vector<PhysTrieHost> tries;
@@ -323,6 +324,13 @@ static void prepare_query(fjg_query* q) {
   if (A > (size_t)MAXA) throw ValidationError("too many atoms for the device executor (max 16)");
   if (plan.nodes.size() > (size_t)MAXN) throw ValidationError("too many plan nodes (max 32)");
   q->head = fj::head_variables(plan.query);
+  if (!q->head_override.empty()) {  // explicit head order (e.g. the original query's, for bushy segments)
+    std::vector<std::string> a = q->head, b = q->head_override;
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    if (a != b) throw ValidationError("\"head\" must list every query variable exactly once");
+    q->head = q->head_override;
+  }
   q->width = (int)std::max(q->head.size(), A);
   if (q->head.size() > (size_t)MAXV) throw ValidationError("too many variables (max 16)");
   std::map<std::string, int> vid;
@@ -780,6 +788,10 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   if (single && l == 0 && T.levels[0].size() <= 1 && len0 >= (1u << 21) && FJG_SORTED_ROOT) {
     force_root_sorted(q, t);
     return;
+  }
+  if (single && len0 == 0) {
+    // empty root: probes read bucket p of a zero-length region and must see EMPTY
+    CK(cudaMemsetAsync(L.table + 4ull * p0, 0xFF, 4 * sizeof(Slot), eng->stream));
   }
   ForceRange R{};
   R.single = single ? 1 : 0;
@@ -1302,6 +1314,8 @@ int fjg_query_create(fjg_engine* eng, const char* query_json, const char* plan_j
       throw fj::ValidationError("query has " + std::to_string(query.size()) + " atoms but " +
                                 std::to_string(natoms) + " relations were bound");
     q->plan = fj::plan_from_json(fj::json::parse(plan_json), query);
+    if (const fj::json::Value* hv = qv.is_object() ? qv.find("head") : nullptr)
+      for (auto& x : hv->arr) q->head_override.push_back(x.str);
     std::string err = fj::validate(q->plan);
     if (!err.empty()) throw fj::ValidationError("invalid plan: " + err);
     for (int a = 0; a < natoms; ++a) {
@@ -1391,6 +1405,26 @@ int fjg_query_output(fjg_query* q, int32_t* host_out, uint64_t cap_rows, uint64_
 }
 
 int fjg_query_num_head_vars(const fjg_query* q) { return q ? (int)q->head.size() : 0; }
+
+// Device-resident materialisation of the enumerated output (run_segments,
+// SPEC.md:414-422): a new columnar relation, one column per head variable.
+int fjg_query_output_relation(fjg_query* q, fjg_relation** out) {
+  return guard([&] {
+    fjg_engine* eng = q->eng;
+    ScopedDevice sd(eng->device);
+    const int nv = (int)q->head.size();
+    if (nv > MAXC) throw fj::ResourceError("materialised segment has more than 8 variables");
+    fjg_relation* r = new_relation(eng, nv, q->out_rows);
+    if (q->out_rows) {
+      DevPartCols pc{};
+      pc.ncols = nv;
+      for (int c = 0; c < nv; ++c) pc.out[c] = r->cols[c];
+      LAUNCH(eng, k_transpose_rows<<<grid_for(q->out_rows), 256, 0, eng->stream>>>(q->out_tuples, q->out_rows, pc));
+    }
+    CK(cudaStreamSynchronize(eng->stream));
+    *out = r;
+  });
+}
 
 void fjg_query_destroy(fjg_query* q) {
   if (!q) return;

@@ -116,3 +116,9 @@ __global__ void k_part_totals(const uint32_t* __restrict__ offs, int nparts, uin
     tot[d] = offs[(uint64_t)d * nblocks];
 }
 
+
+// row-major tuples (enumerate output) -> columnar relation
+__global__ void k_transpose_rows(const int32_t* __restrict__ rows, uint64_t n, DevPartCols pc) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < pc.ncols; ++c) pc.out[c][i] = rows[i * pc.ncols + c];
+}

@@ -197,12 +197,15 @@ class Query:
         self.engine = engine
         if isinstance(query, dict):
             qd = query
+            head = query.get("head")
         elif isinstance(query, str):
             qd = json.loads(query)
+            head = qd.get("head")
         else:
             qd = {"query": query}
+            head = None
         self.atoms = qd["query"]
-        self.query_json = json.dumps({"query": self.atoms})
+        self.query_json = json.dumps({"query": self.atoms, **({"head": head} if head else {})})
         self.plan = plan
         self.plan_json = plan if isinstance(plan, str) else json.dumps([[[r, list(v)] for (r, v) in n] for n in plan])
         self.relations = list(atom_relations)
@@ -217,6 +220,8 @@ class Query:
             for v in a["vars"]:
                 if v not in self.head:
                     self.head.append(v)
+        if head:
+            self.head = list(head)
 
     def execute(self, batch_size=0, dynamic_cover=True, output_mode="count", min_var=None, timing=False):
         o = _capi.ExecOptions()
@@ -247,6 +252,12 @@ class Query:
         rows = C.c_uint64(0)
         check(lib.fjg_query_output(self._h, buf.ctypes.data, r.output_rows, C.byref(rows)))
         return buf[: rows.value], r
+
+    def output_relation(self):
+        """After an enumerate execute: the output as a device Relation (one column per head var)."""
+        h = C.c_void_p()
+        check(lib.fjg_query_output_relation(self._h, C.byref(h)))
+        return Relation(self.engine, h)
 
     def close(self):
         if self._h and self.engine._h:

@@ -268,3 +268,47 @@ def test_scale_path5_residues(engine):
             assert tot == res.count % 2 ** 64
         else:
             assert tot % mod == res.count % mod
+
+
+def test_run_segments_bushy(engine):
+    """SPEC acceptance #7: bushy trees decompose into segments whose
+    device-materialised results feed the parent; output == brute force."""
+    from paper_2301_10841_b200.segments import run_segments
+    rng = np.random.default_rng(31)
+    trees = [["join", ["join", "A0", "A1"], ["join", "A2", "A3"]],
+             ["join", "A0", ["join", "A1", ["join", "A2", "A3"]]],
+             ["join", ["join", "A0", ["join", "A1", "A2"]], "A3"]]
+    done = 0
+    while done < 24:
+        q, cols = random_query(rng, max_atoms=4)
+        if len(q["query"]) != 4:
+            continue
+        truth = oracle.brute_force(q, cols)
+        if len(truth) > 20000:
+            continue
+        done += 1
+        rels = {a["rel"]: engine.relation(c) for a, c in zip(q["query"], cols)}
+        for tree in trees:
+            for mode in ("free", "generic"):
+                try:
+                    r, qq, trace = run_segments(engine, q["query"], tree, rels, mode=mode, output_mode="enumerate")
+                except fjg.ResourceError:
+                    continue  # a segment wider than 8 variables
+                assert bag_equal(r.extra["rows"], truth), (tree, mode)
+                assert r.checksum == oracle.checksum_of(truth)
+                assert len(trace) == len(P.decompose_bushy(tree, q["query"]))
+
+
+def test_empty_root_after_reuse(engine):
+    """A 0-row relation probed after its trie memory held an earlier query's
+    slots must miss (regression: stale buckets of an empty region)."""
+    q = [{"rel": "A", "vars": ["x", "y"]}, {"rel": "B", "vars": ["x"]}]
+    plan = P.compile_plan(q, "free")
+    a = [np.arange(100, dtype=np.int32) % 7, np.arange(100, dtype=np.int32)]
+    for _ in range(3):
+        big = engine.query({"query": q}, plan, [engine.relation(a), engine.relation([a[0]])])
+        assert big.execute().count > 0
+        big.close()
+        empty = engine.query({"query": q}, plan, [engine.relation(a), engine.relation([np.zeros(0, np.int32)])])
+        assert empty.execute().count == 0
+        empty.close()
