@@ -127,6 +127,13 @@ int fjg_compile_plan(const char* query_json, int mode, int factor_fixpoint, char
 int fjg_plan_op(const char* op, const char* query_json, const char* arg_json, char* out, size_t cap,
                 size_t* needed);
 
+/* ---- ingestion ----
+ * Header-less CSV of int fields into a row-major host buffer (cap_rows x
+ * ncols). *rows = rows in the file (also on FJG_E_RESOURCE when cap_rows is
+ * too small). Errors: FJG_E_IO (open), FJG_E_PARSE (row, column), 
+ * FJG_E_VALIDATION (field count). Text columns are not supported. */
+int fjg_parse_csv(const char* path, int ncols, int32_t* out, uint64_t cap_rows, uint64_t* rows);
+
 /* ---- engine (one per device/stream) ---- */
 int fjg_engine_create(int device, fjg_engine** out);
 void fjg_engine_destroy(fjg_engine* eng);

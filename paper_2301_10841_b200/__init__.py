@@ -4,7 +4,7 @@ Free Join node execution as sm_100a kernels behind a C-ABI (include/fjg.h).
 Host side (this package) mirrors the reference's interfaces: plan compiler
 (plan.py -> host C++), relations / queries / execution (engine.py -> device),
 multi-GPU sharding on the first plan variable (dist.py)."""
-from . import plan
+from . import fixtures, plan
 from ._capi import EngineError, Error, IoError, ParseError, ResourceError, ValidationError
 from .engine import Engine, ExecResult, Query, Relation
 

@@ -97,6 +97,7 @@ def _load():
         "fjg_query_destroy": (None, [P]),
         "fjg_device_tuple_hash": (I, [P, P, I, U64, P]),
         "fjg_host_tuple_hash": (U64, [P, I]),
+        "fjg_parse_csv": (I, [C.c_char_p, I, P, U64, C.POINTER(U64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -114,7 +115,7 @@ EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_o
             "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition",
             "fjg_relation_partition_into", "fjg_query_create",
             "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_output_relation", "fjg_query_destroy",
-            "fjg_device_tuple_hash", "fjg_host_tuple_hash"]
+            "fjg_device_tuple_hash", "fjg_host_tuple_hash", "fjg_parse_csv"]
 
 
 def check(rc):

@@ -1,5 +1,9 @@
 // C-ABI for the host plan compiler and error plumbing
 // (error.hpp:8-33). Device entry points live in engine.cu.
+#include <cerrno>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -127,6 +131,67 @@ int fjg_plan_op(const char* op_c, const char* query_json, const char* arg_json, 
         throw fj::ValidationError("unknown plan op '" + op + "'");
     }
     emit(res, out, cap, needed);
+  });
+}
+
+// load_csv: header-less, comma-separated, no quoting
+// (reject fields with quotes), int columns. Rows land row-major
+// in `out` (capacity cap_rows x ncols); *rows receives the row count even
+// when the buffer is too small (then FJG_E_RESOURCE), so callers can size it.
+int fjg_parse_csv(const char* path, int ncols, int32_t* out, uint64_t cap_rows, uint64_t* rows) {
+  return guard([&] {
+    if (ncols < 1) throw fj::ValidationError("load_csv: ncols must be >= 1");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw fj::IoError(std::string("load_csv: cannot open ") + path);
+    std::string data;
+    char buf[1 << 16];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) data.append(buf, got);
+    std::fclose(f);
+    uint64_t r = 0;
+    size_t i = 0;
+    const size_t n = data.size();
+    while (i < n) {
+      size_t e = data.find('\n', i);
+      if (e == std::string::npos) e = n;
+      size_t end = e;
+      if (end > i && data[end - 1] == '\r') --end;
+      if (end > i) {
+        int c = 0;
+        size_t a = i;
+        while (true) {
+          size_t b = a;
+          while (b < end && data[b] != ',') ++b;
+          const std::string field = data.substr(a, b - a);
+          if (field.find('"') != std::string::npos)
+            throw fj::ParseError("load_csv: quoted field at row " + std::to_string(r) + " column " +
+                                 std::to_string(c));
+          if (c >= ncols)
+            throw fj::ValidationError("load_csv: row " + std::to_string(r) + " has more than " +
+                                      std::to_string(ncols) + " fields");
+          char* stop = nullptr;
+          errno = 0;
+          const long long v = std::strtoll(field.c_str(), &stop, 10);
+          if (field.empty() || *stop != '\0' || errno == ERANGE)
+            throw fj::ParseError("load_csv: cannot parse '" + field + "' as int at row " + std::to_string(r) +
+                                 " column " + std::to_string(c));
+          if (v < INT32_MIN || v > INT32_MAX)
+            throw fj::ParseError("load_csv: value " + field + " at row " + std::to_string(r) +
+                                 " exceeds the device's int32 columns");
+          if (out && r < cap_rows) out[r * (uint64_t)ncols + c] = (int32_t)v;
+          ++c;
+          if (b >= end) break;
+          a = b + 1;
+        }
+        if (c != ncols)
+          throw fj::ValidationError("load_csv: row " + std::to_string(r) + " has " + std::to_string(c) +
+                                    " fields, expected " + std::to_string(ncols));
+        ++r;
+      }
+      i = e + 1;
+    }
+    *rows = r;
+    if (r > cap_rows) throw fj::ResourceError("load_csv: buffer too small");
   });
 }
 
