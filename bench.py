@@ -242,7 +242,7 @@ def run_reference(args):
     v = statistics.median(vals)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators)",
             "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "parallelism": "cpu-threads"},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port",
@@ -348,7 +348,7 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators, resident in HBM)",
             "config": {"workload": w.name, **w.params, "plan_mode": w.mode,
                        "parallelism": f"hash-partition x{world}" if (world > 1 or args.shard) else "single-gpu",

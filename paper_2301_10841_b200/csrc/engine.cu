@@ -918,18 +918,24 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
                FJG_GJ_R > 1) {
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const unsigned gi = grid_for(c1 - c0, TILE * FJG_GJ_R, eng->num_sms * 8);
+#define FJG_LAST_GJ(NS_, W_)                                                                               \
+  do {                                                                                                      \
+    if (FJG_GJ_KERNEL == 1)                                                                                 \
+      LAUNCH(eng, (k_last_gj_bf<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,    \
+                                                                                q->min_var, q->d_ctr)));    \
+    else                                                                                                    \
+      LAUNCH(eng, (k_last_gj_ilp<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,   \
+                                                                                 q->min_var, q->d_ctr)));   \
+  } while (0)
         if (N.nsub == 2 && W8 == 4)
-          LAUNCH(eng, (k_last_gj_ilp<2, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
-                                                                                 q->min_var, q->d_ctr)));
+          FJG_LAST_GJ(2, 4);
         else if (N.nsub == 2)
-          LAUNCH(eng, (k_last_gj_ilp<2, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
-                                                                                 q->min_var, q->d_ctr)));
+          FJG_LAST_GJ(2, 8);
         else if (W8 == 4)
-          LAUNCH(eng, (k_last_gj_ilp<3, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
-                                                                                 q->min_var, q->d_ctr)));
+          FJG_LAST_GJ(3, 4);
         else
-          LAUNCH(eng, (k_last_gj_ilp<3, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,
-                                                                                 q->min_var, q->d_ctr)));
+          FJG_LAST_GJ(3, 8);
+#undef FJG_LAST_GJ
       } else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT) {
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const int ns = N.nsub;

@@ -320,6 +320,233 @@ __global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KN
   }
 }
 
+#ifndef FJG_GJ_BF_MINB
+#define FJG_GJ_BF_MINB 4
+#endif
+// One 32-byte bucket (4 slots) in a single 256-bit load (LDG.E.ENL2.256).
+struct Bucket8 {
+  uint32_t k0, q0, k1, q1, k2, q2, k3, q3;
+};
+__device__ __forceinline__ Bucket8 ld_bucket(const Slot* table, uint64_t b) {
+  Bucket8 r;
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.k0), "=r"(r.q0), "=r"(r.k1), "=r"(r.q1), "=r"(r.k2), "=r"(r.q2), "=r"(r.k3), "=r"(r.q3)
+               : "l"(table + 4 * b));
+  return r;
+}
+// Branch-free match over a bucket: slots fill in order, so a priority select
+// finds the key; `more` = all four slots taken and none matched (the probe
+// continues in the next bucket of the region).
+__device__ __forceinline__ uint32_t bucket_match(const Bucket8& a, uint32_t kw, bool& more) {
+  uint32_t q = (a.q3 != kEmpty && a.k3 == kw) ? a.q3 : kEmpty;
+  q = (a.q2 != kEmpty && a.k2 == kw) ? a.q2 : q;
+  q = (a.q1 != kEmpty && a.k1 == kw) ? a.q1 : q;
+  q = (a.q0 != kEmpty && a.k0 == kw) ? a.q0 : q;
+  more = a.q3 != kEmpty && q == kEmpty;
+  return q;
+}
+
+// Per-warp queue of surviving candidates (binding, cover value, probe
+// results): the checksum / multiplicity fold runs on full batches of 32 with
+// every lane busy instead of on the ~7% of lanes that hit (C2).
+template <int NS>
+struct HitQueue {  // per-warp ring buffers
+  static constexpr int NW = TILE / 32, QC = 128;
+  int32_t x[NW][QC];
+  uint32_t e[NW][QC];
+  uint32_t q[NS - 1][NW][QC];
+  uint8_t c[NW][QC];
+  uint32_t tail[NW];
+};
+
+// k_last_gj_ilp with the probe path made branch-free and the fold batched:
+// the probed subatoms are selected by index (s = j + (j >= chosen)) so one
+// code path serves every cover choice; each probe is one 256-bit bucket load
+// and a priority select; survivors are folded from a per-warp queue (leaf
+// multiplicities, head-prefix hash, checksum, MIN). Same algorithm and
+// results as k_last_gj_ilp (the fold is order-independent).
+template <int NS, int R, int W>
+__global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_bf(const __grid_constant__ KNode N, uint64_t c0,
+                                                                     uint64_t c1, uint64_t F,
+                                                                     const uint64_t* __restrict__ bounds,
+                                                                     int min_var, DevCounters* ctr) {
+  __shared__ HitQueue<NS> Q;
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint64_t* __restrict__ scan = N.scan;
+  const int nhead = N.nhead;
+  uint32_t head = 0;  // warp-uniform ring head
+  if (lane == 0) Q.tail[wi] = 0;
+  __syncwarp();
+
+  auto fold = [&](uint32_t h0, uint32_t n) {  // lanes < n fold ring entries h0 + lane
+    if ((uint32_t)lane < n) {
+      const uint32_t slot = (h0 + lane) & (HitQueue<NS>::QC - 1);
+      const int32_t x = Q.x[wi][slot];
+      const uint32_t e = Q.e[wi][slot];
+      const int ci = Q.c[wi][slot];
+      uint64_t mu = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+#pragma unroll
+      for (int j = 0; j < NS - 1; ++j) {
+        const uint32_t* cnt = j >= ci ? N.sub[j + 1].cnt : N.sub[j].cnt;
+        const bool plast = j >= ci ? N.sub[j + 1].last : N.sub[j].last;
+        if (plast) mu *= __ldg(cnt + Q.q[j][wi][slot]);
+      }
+      uint64_t pre = fj::kTupleHashSeed;
+      long long bmin = LLONG_MAX;
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if (v < nhead - 1) {
+          const int32_t hvv = __ldg(N.in_var[v] + e);
+          pre = fj::tuple_hash_step(pre, (int64_t)hvv);
+          if (v == min_var) bmin = hvv;
+        }
+      const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x);
+      acc_sum += mu * fj::checksum_word(h);
+      acc_lo += mu;
+      if (acc_lo < mu) ++acc_hi;
+      if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x : bmin);
+    }
+  };
+
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * R; base < c1; base += (uint64_t)gridDim.x * TILE * R) {
+    uint64_t i = base + (uint64_t)threadIdx.x * R;
+    const uint64_t iend = min(i + R, c1);
+    if (i < iend) {
+      const uint64_t t = (i - c0) / TILE;
+      uint64_t e = upper_bound_u64(scan, __ldg(bounds + t), __ldg(bounds + t + 1), i);
+      while (i < iend) {
+        const uint64_t se = __ldg(scan + e);
+        const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
+        const uint64_t bend = min(iend, se);
+        const int ci = N.chosen[e];
+        uint32_t sp[NS], sl[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const KSub& P = N.sub[s];
+          if (P.in_p) {
+            sp[s] = __ldg(P.in_p + e);
+            sl[s] = __ldg(P.in_len + e);
+          } else {
+            sp[s] = 0;
+            sl[s] = P.root_n;
+          }
+        }
+        uint32_t cbase = sp[0];
+        const int32_t* csrc = N.sub[0].src[0];
+#pragma unroll
+        for (int s = 1; s < NS; ++s)
+          if (s == ci) {
+            cbase = sp[s];
+            csrc = N.sub[s].src[0];
+          }
+        cbase += (uint32_t)(i - prev);
+        int32_t x[R];
+        bool live[R];
+        uint32_t qv[R][NS - 1];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          live[r] = i + r < bend;
+          x[r] = live[r] ? __ldg(csrc + cbase + r) : 0;
+          body += live[r] ? 1 : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < NS - 1; ++j) {
+          // probed subatom s = j + (j >= ci), selected without branching
+          const Slot* tb = j >= ci ? N.sub[j + 1].table : N.sub[j].table;
+          const uint32_t p = j >= ci ? sp[j + 1] : sp[j];
+          const uint32_t len = j >= ci ? sl[j + 1] : sl[j];
+          Bucket8 h[R];
+          uint64_t b0[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            b0[r] = region_bucket(p, len, (uint32_t)x[r]);
+            if (live[r]) h[r] = ld_bucket(tb, b0[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (!live[r]) continue;
+            ++probes;
+            const uint32_t kw = (uint32_t)x[r];
+            bool more;
+            uint32_t q = bucket_match(h[r], kw, more);
+            if (more) {
+              uint64_t b = b0[r];
+              const uint64_t blo = p, bhi = (uint64_t)p + len;
+              do {
+                if (++b == bhi) b = blo;
+                q = bucket_match(ld_bucket(tb, b), kw, more);
+              } while (more);
+            }
+            if (q == kEmpty) {
+              ++misses;
+              live[r] = false;
+            }
+            qv[r][j] = q;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!live[r]) continue;
+          const uint32_t slot = atomicAdd(&Q.tail[wi], 1u) & (HitQueue<NS>::QC - 1);
+          Q.x[wi][slot] = x[r];
+          Q.e[wi][slot] = (uint32_t)e;
+          Q.c[wi][slot] = (uint8_t)ci;
+#pragma unroll
+          for (int j = 0; j < NS - 1; ++j) Q.q[j][wi][slot] = qv[r][j];
+        }
+        i = bend;
+        ++e;
+      }
+    }
+    // warp-convergent: fold full batches of 32 (at most 32*R + 31 < QC pending)
+    __syncwarp();
+    const uint32_t tail = *(volatile uint32_t*)&Q.tail[wi];
+    while (tail - head >= 32) {
+      fold(head, 32);
+      head += 32;
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  fold(head, *(volatile uint32_t*)&Q.tail[wi] - head);
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  uint64_t lo2 = acc_lo, hi2 = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
+    const uint64_t sm = lo2 + l2;
+    hi2 += h2 + (sm < lo2 ? 1 : 0);
+    lo2 = sm;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (lo2) {
+      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
+      if (old + lo2 < old) ++hi2;
+    }
+    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
+    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+  }
+}
+
+#ifndef FJG_GJ_KERNEL
+#define FJG_GJ_KERNEL 1  // GJ last node: 0 k_last_gj_ilp, 1 k_last_gj_bf
+#endif
 #ifndef FJG_GJ_R
 #define FJG_GJ_R 2
 #endif

@@ -24,7 +24,10 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__
 // (bounds[ntiles] = F-1). Each k_expand tile then searches only
 // [bounds[t], bounds[t+1]] instead of the whole scan.
 constexpr int TILE = 256;
-constexpr uint64_t kLastChunk = 1ull << 28;  // last-node candidates per launch
+#ifndef FJG_LAST_CHUNK_LOG
+#define FJG_LAST_CHUNK_LOG 28
+#endif
+constexpr uint64_t kLastChunk = 1ull << FJG_LAST_CHUNK_LOG;  // last-node candidates per launch
 __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1,
                               uint64_t* __restrict__ bounds) {
   const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;

@@ -202,7 +202,18 @@ def test_device_rmat_matches_host():
     torch.cuda.synchronize()
 
 
-def test_scale_triangle_partition(engine):
+@pytest.fixture
+def own_engine():
+    """A private engine for the full-size tests: closing it returns its memory
+    pool (tens of GB at 2^27) before the next test allocates."""
+    import torch
+    eng = fjg.Engine(0)
+    yield eng
+    eng.close()
+    torch.cuda.empty_cache()
+
+
+def test_scale_triangle_partition(own_engine):
     """C5 at full size (R-MAT 2^27, 512M edges): the first-variable hash
     partition r of G (E1, E3 restricted, E2 whole) vs the oracle's committed
     result (tests/golden/make_scale_goldens.py)."""
@@ -218,6 +229,7 @@ def test_scale_triangle_partition(engine):
     cols = restricted(w)
     assert len(cols[0][0]) == g["rows_partition"]
     plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+    engine = own_engine
     part = engine.relation(cols[0])
     full = engine.relation(cols[1])
     r = engine.query({"query": w.query}, plan, [part, full, part]).execute()
@@ -243,17 +255,19 @@ def test_path5_memoised_count(engine, scale, m):
         assert fjg.run_workload(engine, w)[0].count == res.count
 
 
-def test_scale_path5_residues(engine):
+def test_scale_path5_residues(own_engine):
     """C5 5-path at full size (~4.9e21 walks, > 2^64): the device memoised count
     agrees with 1^T A^5 1 computed independently by torch index_add SpMV,
     modulo 2^64 and modulo two primes (exact integer residues)."""
     import torch
     w = configs.scale_path5()
-    res, q, plan, rels = fjg.run_workload(engine, w)
+    res, q, plan, rels = fjg.run_workload(own_engine, w)
     assert res.count > 2 ** 64
     q.close()
     for r in rels.values():
         r.close()
+    own_engine.close()  # return the pool before the torch SpMV below
+    torch.cuda.empty_cache()
     src = torch.from_numpy(w.relations["E"][0]).cuda().long()
     dst = torch.from_numpy(w.relations["E"][1]).cuda().long()
     n = 1 << w.params["scale"]
