@@ -364,7 +364,7 @@ def run_ours(args):
                          "keys_inserted": r0.keys_inserted, "host_syncs": r0.host_syncs},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "fused last node (k_last_gj_ilp for GJ-shaped nodes, else k_expand<COUNT>)",
+                         "kernel": "fused last node (k_last_gj_bf for GJ-shaped nodes, else k_expand<COUNT>)",
                          "algorithmic_bytes_per_launch": last_bytes, "peak_kind": hbm_kind},
             "gpu_launches": launches,
             "clocks": clk,

@@ -269,6 +269,7 @@ struct fjg_query {
   bool sw[MAXN];   // per node: the stream-cover frontier-writing fast path applies
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
+  uint32_t* chunk_owner = nullptr;  // chunk -> owning entry (GJ last node)
   // non-blocking phase timer: event pairs resolved after the final sync
   std::vector<cudaEvent_t> events;
   std::vector<std::pair<int, int>> marks;  // (event index, phase) ; phase<0 = start
@@ -705,6 +706,7 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   const uint64_t nb = std::max<uint64_t>(cap, kLastChunk) / TILE + 2;
   if (nb > q->bounds_cap) {
     q->bounds = (uint64_t*)q->alloc(nb * 8);
+    q->chunk_owner = (uint32_t*)q->alloc((kLastChunk / (32 * FJG_GJ_R) + 2) * 4);
     q->bounds_cap = nb;
   }
   // CUB temp storage for the largest scans
@@ -906,7 +908,12 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     for (uint64_t c0 = 0; c0 < M; c0 += kLastChunk) {
       const uint64_t c1 = std::min(M, c0 + kLastChunk);
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
-      LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
+      const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
+                           FJG_GJ_R > 1 && FJG_GJ_KERNEL == 1;
+      if (gj_fast)
+        LAUNCH(eng, k_chunk_owner<<<grid_for(F), 256, 0, eng->stream>>>(N.scan, F, c0, c1, 32 * FJG_GJ_R, q->chunk_owner));
+      else
+        LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
       if (mode == EXPAND_ENUM)
         LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1,
@@ -921,7 +928,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
 #define FJG_LAST_GJ(NS_, W_)                                                                               \
   do {                                                                                                      \
     if (FJG_GJ_KERNEL == 1)                                                                                 \
-      LAUNCH(eng, (k_last_gj_bf<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,    \
+      LAUNCH(eng, (k_last_gj_bf<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,\
                                                                                 q->min_var, q->d_ctr)));    \
     else                                                                                                    \
       LAUNCH(eng, (k_last_gj_ilp<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,   \

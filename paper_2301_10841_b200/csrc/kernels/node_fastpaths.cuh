@@ -368,7 +368,7 @@ struct HitQueue {  // per-warp ring buffers
 template <int NS, int R, int W>
 __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_bf(const __grid_constant__ KNode N, uint64_t c0,
                                                                      uint64_t c1, uint64_t F,
-                                                                     const uint64_t* __restrict__ bounds,
+                                                                     const uint32_t* __restrict__ owner,
                                                                      int min_var, DevCounters* ctr) {
   __shared__ HitQueue<NS> Q;
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
@@ -415,8 +415,8 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_
     uint64_t i = base + (uint64_t)threadIdx.x * R;
     const uint64_t iend = min(i + R, c1);
     if (i < iend) {
-      const uint64_t t = (i - c0) / TILE;
-      uint64_t e = upper_bound_u64(scan, __ldg(bounds + t), __ldg(bounds + t + 1), i);
+      const uint64_t t = (i - c0) / (32 * R);  // this warp's chunk
+      uint64_t e = upper_bound_u64(scan, __ldg(owner + t), __ldg(owner + t + 1), i);
       while (i < iend) {
         const uint64_t se = __ldg(scan + e);
         const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
