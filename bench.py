@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-target-s", type=float, default=30.0)
+    ap.add_argument("--backend", default="colt", choices=["colt", "slt", "simple"],
+                    help="GHT backend (SPEC.md:286-294): the §5.3 ablation ladder")
     ap.add_argument("--shard", action="store_true",
                     help="use the multi-GPU sharded path (partition + NCCL exchange) even at one rank")
     return ap.parse_args()
@@ -181,35 +183,35 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------- CPU leg ---
-def _orc_run(w, plan, cols, min_var, T, P):
+def _orc_run(w, plan, cols, min_var, T, P, backend="colt"):
     from oracle import oracle
     t0 = time.perf_counter()
-    r = oracle.execute(w.query, plan, cols, part=0, nparts=P, nthreads=T, min_var=min_var)
+    r = oracle.execute(w.query, plan, cols, part=0, nparts=P, nthreads=T, min_var=min_var, backend=backend)
     return time.perf_counter() - t0, r
 
 
-def cpu_plan(w, plan, min_var, T):
+def cpu_plan(w, plan, min_var, T, backend="colt"):
     """Two-point calibration of the oracle on T threads: t(P) = B + W/P for T of
     P first-variable partitions (B: per-thread build, W: join work)."""
     cols = w.atom_columns()
-    t16, _ = _orc_run(w, plan, cols, min_var, T, 16 * T)
-    t4, _ = _orc_run(w, plan, cols, min_var, T, 4 * T)
+    t16, _ = _orc_run(w, plan, cols, min_var, T, 16 * T, backend)
+    t4, _ = _orc_run(w, plan, cols, min_var, T, 4 * T, backend)
     W = max(t4 - t16, 0.0) / (1.0 / (4 * T) - 1.0 / (16 * T))
     B = max(t16 - W / (16 * T), 0.0)
     return B, W
 
 
-def cpu_sample(w, plan, min_var, target_s, threads=None, calib=None):
+def cpu_sample(w, plan, min_var, target_s, threads=None, calib=None, backend="colt"):
     """Time the oracle (CPU restatement of the reference path) on all host
     threads. Thread t runs first-variable hash partition t of P with its own
     trie set; P = T is the whole query. P is the smallest
     multiple of T whose predicted time fits target_s."""
     T = threads or max(1, min(os.cpu_count() or 1, 64))
-    B, W = calib or cpu_plan(w, plan, min_var, T)
+    B, W = calib or cpu_plan(w, plan, min_var, T, backend)
     P = T
     while B + W / P > target_s and P < (1 << 16):
         P *= 2
-    dt, r = _orc_run(w, plan, w.atom_columns(), min_var, T, P)
+    dt, r = _orc_run(w, plan, w.atom_columns(), min_var, T, P, backend)
     frac = T / P
     tuples = w.input_tuples() * frac + r["count"]
     what = "the whole query" if P == T else f"{T} of {P} first-variable hash partitions ({frac:.4f} of the query)"
@@ -230,20 +232,21 @@ def run_reference(args):
     head = P.head_variables(w.query)
     mv = head.index(w.min_var) if w.min_var else -1
     T = max(1, min(os.cpu_count() or 1, 64))
-    calib = cpu_plan(w, plan, mv, T)
+    calib = cpu_plan(w, plan, mv, T, args.backend)
     target = max(1.0, min(60.0, 200.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_sample(w, plan, mv, target, threads=T, calib=calib)
+        cpu_sample(w, plan, mv, target, threads=T, calib=calib, backend=args.backend)
     vals, secs, last = [], [], None
     for _ in range(args.steps):
-        last = cpu_sample(w, plan, mv, target, threads=T, calib=calib)
+        last = cpu_sample(w, plan, mv, target, threads=T, calib=calib, backend=args.backend)
         vals.append(last["value"])
         secs.append(last["seconds"])
     v = statistics.median(vals)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators)",
-            "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "parallelism": "cpu-threads"},
+            "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "backend": args.backend,
+                       "parallelism": "cpu-threads"},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port",
                              "sample": last["sample"]},
@@ -273,12 +276,12 @@ def run_ours(args):
         from paper_2301_10841_b200 import dist as D
         sharded = D.ShardedQuery(eng, w, plan, world, rank)
         step = lambda timing=False: sharded.execute(min_var=mv, timing=timing,  # noqa: E731
-                                                    output_mode=w.output_mode)
+                                                    output_mode=w.output_mode, backend=args.backend)
         input_tuples_local = sharded.input_tuples_local
     else:
         q, _, rels = fjg.prepare_workload(eng, w)
         step = lambda timing=False: q.execute(min_var=mv, timing=timing, batch_size=args.batch,  # noqa: E731
-                                              output_mode=w.output_mode)
+                                              output_mode=w.output_mode, backend=args.backend)
         input_tuples_local = w.input_tuples()
 
     for _ in range(max(args.warmup, 1)):
@@ -339,7 +342,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_sample(w, plan, head.index(mv) if mv else -1, args.cpu_target_s)
+            cpu = cpu_sample(w, plan, head.index(mv) if mv else -1, args.cpu_target_s, backend=args.backend)
             for k in ("seconds", "sample_output_tuples", "calib"):
                 cpu.pop(k, None)
         except Exception as ex:  # the CPU leg must not sink the GPU number
@@ -350,7 +353,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators, resident in HBM)",
-            "config": {"workload": w.name, **w.params, "plan_mode": w.mode,
+            "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "backend": args.backend,
                        "parallelism": f"hash-partition x{world}" if (world > 1 or args.shard) else "single-gpu",
                        "l2": "flushed between timed steps (2x126MB write)",
                        "input_tuples": w.input_tuples(), "output_tuples": out_local if world == 1 else None},

@@ -69,7 +69,16 @@ typedef struct {
   int32_t output_mode;   /* FJG_OUT_* */
   int32_t min_var;       /* head-variable index aggregated with MIN, or -1 */
   int32_t collect_timing;/* record build/join phase times (CUDA events) */
+  int32_t backend;       /* FJG_BACKEND_*: GHT backend of new() */
 } fjg_exec_options;
+
+/* GHT backends (the §5.3 ablation ladder):
+ * COLT builds nothing up front and forces subtries lazily in batch; SLT
+ * forces every trie's level 0 before the join and deeper levels lazily;
+ * SIMPLE forces every level of every trie before the join. */
+#define FJG_BACKEND_COLT 0
+#define FJG_BACKEND_SLT 1
+#define FJG_BACKEND_SIMPLE 2
 
 /* Result: OutputSink counter + ExecStats/TrieStats
  * (SPEC.md:377-380, :280-283). count is 128-bit (count_hi:count_lo). */

@@ -44,7 +44,7 @@ _BY_CODE = {c.code: c for c in (IoError, ParseError, ValidationError, ResourceEr
 
 class ExecOptions(C.Structure):
     _fields_ = [("batch_size", C.c_uint64), ("dynamic_cover", C.c_int32), ("output_mode", C.c_int32),
-                ("min_var", C.c_int32), ("collect_timing", C.c_int32)]
+                ("min_var", C.c_int32), ("collect_timing", C.c_int32), ("backend", C.c_int32)]
 
 
 class Result(C.Structure):

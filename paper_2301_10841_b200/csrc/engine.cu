@@ -212,6 +212,7 @@ struct PhysTrieHost {
   std::vector<PhysLevelHost> lev;
   DevTrie dev{};
   bool root_forced = false;
+  int map_levels = 0;  // levels that are maps in some sharing atom's GHT schema (SIMPLE / SLT eager builds)
 };
 
 struct AtomInfo {
@@ -270,6 +271,7 @@ struct fjg_query {
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   uint32_t* chunk_owner = nullptr;  // chunk -> owning entry (GJ last node)
+  int backend = FJG_BACKEND_COLT;
   // non-blocking phase timer: event pairs resolved after the final sync
   std::vector<cudaEvent_t> events;
   std::vector<std::pair<int, int>> marks;  // (event index, phase) ; phase<0 = start
@@ -393,6 +395,11 @@ static void prepare_query(fjg_query* q) {
       found = (int)q->tries.size() - 1;
     }
     q->atoms[a].trie = found;
+    // derive_ght_schemas (fj_plan.cpp): every level is a map unless the atom's
+    // last subatom is its node's cover (then that level stays an offset vector)
+    const bool last_is_cover = !q->atoms[a].subs.empty() && q->atoms[a].subs.back().second == 0;
+    const int ml = (int)levels.size() - (last_is_cover ? 1 : 0);
+    q->tries[found].map_levels = std::max(q->tries[found].map_levels, ml);
   }
   // allocate trie storage
   for (size_t t = 0; t < q->tries.size(); ++t) {
@@ -1060,8 +1067,42 @@ static void run_memo_passes(fjg_query* q) {
   q->mark(eng->stream, 1);
 }
 
+// SLT / SIMPLE backends: force level 0 of every trie (SLT)
+// or every level of every trie (SIMPLE) before the join; COLT does neither.
+static void eager_build(fjg_query* q) {
+  fjg_engine* eng = q->eng;
+  for (size_t t = 0; t < q->tries.size(); ++t) {
+    auto& T = q->tries[t];
+    if (T.map_levels < 1) continue;
+    if (!T.root_forced) {
+      force_level(q, (int)t, 0, true, 0, (uint32_t)T.rel->nrows, 1);
+      LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
+      T.root_forced = true;
+    }
+    if (q->backend != FJG_BACKEND_SIMPLE) continue;
+    const uint64_t nslots = 4 * std::max<uint64_t>(T.rel->nrows, 1);
+    for (int l = 1; l < T.map_levels; ++l) {
+      uint32_t* cntp = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(q->d_ctr) +
+                                                   offsetof(DevCounters, list_count)) +
+                       (t * MAXL + l);
+      CK(cudaMemsetAsync(cntp, 0, 4, eng->stream));
+      const DevLevel& P = T.dev.lev[l - 1];
+      const DevLevel& L = T.dev.lev[l];
+      LAUNCH(eng, k_eager_list<<<grid_for(nslots), 256, 0, eng->stream>>>(P.table, nslots, P.cnt, L, cntp));
+      sync_counters(q);
+      const uint32_t c = q->h_ctr->list_count[t * MAXL + l];
+      if (c) {
+        force_level(q, (int)t, l, false, 0, 0, c);
+        LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
+      }
+      CK(cudaMemsetAsync(cntp, 0, 4, eng->stream));
+    }
+  }
+}
+
 static void execute_once(fjg_query* q, int mode) {
   reset_query(q);
+  if (q->backend != FJG_BACKEND_COLT) eager_build(q);
   q->stop_node = -1;
   if (mode == EXPAND_MEMO) {
     run_memo_passes(q);
@@ -1356,6 +1397,9 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     q->timing = o.collect_timing != 0;
     q->batch = batch;
     q->min_var = o.min_var;
+    if (o.backend < FJG_BACKEND_COLT || o.backend > FJG_BACKEND_SIMPLE)
+      throw fj::ValidationError("backend must be colt(0), slt(1) or simple(2)");
+    q->backend = o.backend;
     const uint32_t l0 = eng->launches, s0 = eng->syncs;
     const bool memo = o.output_mode == FJG_OUT_FACTORIZED_COUNT && q->chain_start >= 1;
     execute_once(q, memo ? EXPAND_MEMO : EXPAND_COUNT);

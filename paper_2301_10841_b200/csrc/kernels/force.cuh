@@ -287,3 +287,21 @@ __global__ void k_root_gather(const DevTrie* __restrict__ tries, int trie, uint3
       if (L.cval[c]) L.cval[c][i] = T.base[c][r];
   }
 }
+
+// Eager (SIMPLE backend) level list: every key of a fully forced level l-1
+// names a child subtrie (start q, length cnt[q]) to force at level l.
+// (Same bookkeeping as a claim in k_select: the child's cursor / key count restart.)
+__global__ void k_eager_list(const Slot* __restrict__ table, uint64_t nslots, const uint32_t* __restrict__ cnt,
+                             DevLevel child, uint32_t* __restrict__ list_count) {
+  uint32_t* __restrict__ list_p = child.list_p;
+  uint32_t* __restrict__ list_len = child.list_len;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = table[s].q;
+    if (q == kEmpty) continue;
+    child.cursor[q] = 0;
+    child.nkeys[q] = 0;
+    const uint32_t i = atomicAdd(list_count, 1u);
+    list_p[i] = q;
+    list_len[i] = cnt[q];
+  }
+}

@@ -18,6 +18,7 @@ from ._capi import check, lib
 
 OUT_COUNT, OUT_ENUMERATE, OUT_FACTORIZED_COUNT = 0, 1, 2
 _OUT = {"count": OUT_COUNT, "enumerate": OUT_ENUMERATE, "factorized_count": OUT_FACTORIZED_COUNT}
+_BACKEND = {"colt": 0, "slt": 1, "simple": 2}  # FJG_BACKEND_*
 CMP = {"=": 0, "==": 0, "!=": 1, "<": 2, "<=": 3, ">": 4, ">=": 5}
 
 
@@ -223,8 +224,10 @@ class Query:
         if head:
             self.head = list(head)
 
-    def execute(self, batch_size=0, dynamic_cover=True, output_mode="count", min_var=None, timing=False):
+    def execute(self, batch_size=0, dynamic_cover=True, output_mode="count", min_var=None, timing=False,
+                backend="colt"):
         o = _capi.ExecOptions()
+        o.backend = _BACKEND[backend] if isinstance(backend, str) else int(backend)
         o.batch_size = int(batch_size)
         o.dynamic_cover = int(bool(dynamic_cover))
         o.output_mode = _OUT[output_mode] if isinstance(output_mode, str) else int(output_mode)
@@ -243,10 +246,10 @@ class Query:
                           last_node_candidates=r.last_node_candidates,
                           kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
 
-    def enumerate(self, batch_size=0, dynamic_cover=True, min_var=None):
+    def enumerate(self, batch_size=0, dynamic_cover=True, min_var=None, backend="colt"):
         """Enumerate mode: (tuples as an (n, |head|) int32 array in head-variable order, ExecResult)."""
         r = self.execute(batch_size=batch_size, dynamic_cover=dynamic_cover, output_mode="enumerate",
-                         min_var=min_var)
+                         min_var=min_var, backend=backend)
         nv = len(self.head)
         buf = np.empty((max(r.output_rows, 1), nv), dtype=np.int32)
         rows = C.c_uint64(0)

@@ -58,7 +58,9 @@ def test_random_queries(engine, block):
             plan = P.compile_plan(q, mode)
             dyn = bool(rng.random() < 0.7)
             batch = int(rng.choice([0, 3, 7, 1000]))
-            check(engine, q, plan, cols, enumerate=(n % 4 == 0), dynamic_cover=dyn, batch_size=batch)
+            backend = str(rng.choice(["colt", "colt", "slt", "simple"]))
+            check(engine, q, plan, cols, enumerate=(n % 4 == 0), dynamic_cover=dyn, batch_size=batch,
+                  backend=backend)
 
 
 def test_self_joins_share_tries(engine):
@@ -326,3 +328,43 @@ def test_empty_root_after_reuse(engine):
         empty = engine.query({"query": q}, plan, [engine.relation(a), engine.relation([np.zeros(0, np.int32)])])
         assert empty.execute().count == 0
         empty.close()
+
+
+def test_backend_ladder(engine):
+    """GHT backends on the device (acceptance #5, the §5.3
+    ladder): identical outputs; keys_inserted colt <= slt <= simple with
+    colt < simple; the eager SIMPLE build inserts exactly the oracle's keys."""
+    rng = np.random.default_rng(5)
+    n = 100_000
+    zipf = lambda: np.minimum(rng.zipf(1.3, n) - 1, 5000).astype(np.int32)  # noqa: E731
+    uni = lambda: rng.integers(0, 100_000_000, n).astype(np.int32)  # noqa: E731
+    q = [{"rel": "R", "vars": ["x", "y"]}, {"rel": "S", "vars": ["y", "z"]}, {"rel": "T", "vars": ["x", "z"]}]
+    cols = [[zipf(), uni()], [uni(), zipf()], [zipf(), zipf()]]
+    plan = P.compile_plan(q, "generic")
+    rels = [engine.relation(c) for c in cols]
+    query = engine.query({"query": q}, plan, rels)
+    dev = {b: query.execute(backend=b) for b in ("colt", "slt", "simple")}
+    ref = {b: oracle.execute(q, plan, cols, backend=b) for b in ("colt", "simple")}
+    for b, r in dev.items():
+        assert r.count == ref["colt"]["count"] and r.checksum == ref["colt"]["checksum"], b
+    k = {b: r.keys_inserted for b, r in dev.items()}
+    assert k["colt"] <= k["slt"] <= k["simple"] and k["colt"] < k["simple"]
+    assert k["simple"] == ref["simple"]["keys_inserted"]
+    # enumerate through an eager backend: same bag as the lazy one
+    t_colt, _ = query.enumerate(backend="colt")
+    t_simple, _ = query.enumerate(backend="simple")
+    assert sorted(map(tuple, t_colt.tolist())) == sorted(map(tuple, t_simple.tolist()))
+
+
+@pytest.mark.parametrize("name", ["chain", "triangle", "clique4"])
+def test_backends_configs(engine, name):
+    """Eager backends on reduced configs (shared physical tries, leaf levels):
+    same count and checksum as COLT and the oracle."""
+    w = {"chain": lambda: configs.chain(n=20000, domain=20000),
+         "triangle": lambda: configs.triangle(scale=12, m=30000, seed=3),
+         "clique4": lambda: configs.clique4(scale=12, m=40000)}[name]()
+    q, plan, _ = fjg.prepare_workload(engine, w)
+    ref = oracle.execute(w.query, plan, w.atom_columns())
+    for b in ("colt", "slt", "simple"):  # noqa: B007
+        r = q.execute(backend=b)
+        assert (r.count, r.checksum) == (ref["count"], ref["checksum"]), b
