@@ -916,7 +916,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const uint64_t c1 = std::min(M, c0 + kLastChunk);
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
       const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
-                           FJG_GJ_R > 1 && FJG_GJ_KERNEL == 1;
+                           FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
       if (gj_fast)
         LAUNCH(eng, k_chunk_owner<<<grid_for(F), 256, 0, eng->stream>>>(N.scan, F, c0, c1, 32 * FJG_GJ_R, q->chunk_owner));
       else
@@ -928,28 +928,21 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       else if (mode == EXPAND_MEMO)
         LAUNCH(eng, launch_expand<EXPAND_MEMO>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
                                                q->d_ctr));
-      else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
-               FJG_GJ_R > 1) {
+      else if (gj_fast) {  // k_last_gj_bf: x is the last head variable
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const unsigned gi = grid_for(c1 - c0, TILE * FJG_GJ_R, eng->num_sms * 8);
-#define FJG_LAST_GJ(NS_, W_)                                                                               \
-  do {                                                                                                      \
-    if (FJG_GJ_KERNEL == 1)                                                                                 \
-      LAUNCH(eng, (k_last_gj_bf<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,\
-                                                                                q->min_var, q->d_ctr)));    \
-    else                                                                                                    \
-      LAUNCH(eng, (k_last_gj_ilp<NS_, FJG_GJ_R, W_><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds,   \
-                                                                                 q->min_var, q->d_ctr)));   \
-  } while (0)
         if (N.nsub == 2 && W8 == 4)
-          FJG_LAST_GJ(2, 4);
+          LAUNCH(eng, (k_last_gj_bf<2, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
+                                                                                q->min_var, q->d_ctr)));
         else if (N.nsub == 2)
-          FJG_LAST_GJ(2, 8);
+          LAUNCH(eng, (k_last_gj_bf<2, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
+                                                                                q->min_var, q->d_ctr)));
         else if (W8 == 4)
-          FJG_LAST_GJ(3, 4);
+          LAUNCH(eng, (k_last_gj_bf<3, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
+                                                                                q->min_var, q->d_ctr)));
         else
-          FJG_LAST_GJ(3, 8);
-#undef FJG_LAST_GJ
+          LAUNCH(eng, (k_last_gj_bf<3, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
+                                                                                q->min_var, q->d_ctr)));
       } else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT) {
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const int ns = N.nsub;

@@ -2,25 +2,12 @@
 // Included by engine.cu (one translation unit: the kernels share templates and helpers).
 #pragma once
 
-// streaming (read-once) loads: evict-first so the probed slot regions keep L2
-#ifndef FJG_STREAM_HINT
-#define FJG_STREAM_HINT 0
-#endif
-#if FJG_STREAM_HINT
-#define FJG_LD_STREAM(p) __ldcs(p)
-#else
-#define FJG_LD_STREAM(p) __ldg(p)
-#endif
-#ifndef FJG_GJ_WARPSEARCH
-#define FJG_GJ_WARPSEARCH 0
-#endif
-#ifndef FJG_GJ_PREFETCH
-#define FJG_GJ_PREFETCH 1
-#endif
 // Fast path for the Generic-Join-shaped aggregating last node: every subatom
-// is a cover over the same single new variable x (triangle C2/C5, 4-clique
-// C4). Per candidate: binding lookup, one coalesced cover read, NS-1 bucket
-// probes, fold into count / checksum -- no generic state machinery.
+// is a cover over the same single new variable x. Per candidate: binding
+// lookup, one coalesced cover read, NS-1 bucket probes, fold into count /
+// checksum -- no generic state machinery. Used when x is not the last head
+// variable (the hash then needs x in the middle of the tuple); the common
+// case (triangle C2/C5, 4-clique C4) runs k_last_gj_bf below.
 template <int NS, int W>
 __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
                                                   uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
@@ -33,22 +20,9 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
     const uint64_t t = (base - c0) / TILE;
     const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
     const uint64_t i = base + threadIdx.x;
-    // binding of candidate i: the tile's bindings [lo, hi] are usually few, so
-    // the warp loads their scan values in one coalesced load and each lane
-    // counts the ones <= i with shuffles; long spans fall back to a search.
-    uint64_t e, j;
-    if (FJG_GJ_WARPSEARCH && hi - lo < 32) {
-      const uint32_t span = (uint32_t)(hi - lo) + 1;
-      const uint64_t sv = lane < (int)span ? __ldg(scan + lo + lane) : ~0ull;
-      uint32_t k = 0;
-      for (uint32_t u = 0; u < span; ++u) k += __shfl_sync(0xffffffffu, sv, u) <= i ? 1u : 0u;
-      const uint64_t prev = __shfl_sync(0xffffffffu, sv, k > 0 ? k - 1 : 0);
-      e = lo + k;
-      j = i - (k > 0 ? prev : (lo ? __ldg(scan + lo - 1) : 0ull));
-    } else {
-      e = i < c1 ? upper_bound_u64(scan, lo, hi, i) : lo;
-      j = i - (e ? __ldg(scan + e - 1) : 0ull);
-    }
+    // binding of candidate i (search within the tile's bounds)
+    const uint64_t e = i < c1 ? upper_bound_u64(scan, lo, hi, i) : lo;
+    const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
     if (i >= c1) continue;
     const int ci = N.chosen[e];
     uint32_t sp[NS], sl[NS];
@@ -66,7 +40,7 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
     uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
     int32_t hv[W];  // bound head variables, prefetched off the critical path
 #pragma unroll
-    for (int v = 0; v < W; ++v) hv[v] = (FJG_GJ_PREFETCH && v < N.nhead && v != xvar) ? __ldg(N.in_var[v] + e) : 0;
+    for (int v = 0; v < W; ++v) hv[v] = (v < N.nhead && v != xvar) ? __ldg(N.in_var[v] + e) : 0;
     uint32_t cpos = 0;
     const int32_t* csrc = nullptr;
 #pragma unroll
@@ -113,180 +87,13 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
 #pragma unroll
     for (int v = 0; v < W; ++v)
       if (v < N.nhead) {
-        const int32_t val = (v == xvar) ? x : (FJG_GJ_PREFETCH ? hv[v] : __ldg(N.in_var[v] + e));
+        const int32_t val = (v == xvar) ? x : hv[v];
         h = fj::tuple_hash_step(h, (int64_t)val);
         if (v == min_var) acc_min = min(acc_min, (long long)val);
       }
     acc_sum += mult * fj::checksum_word(h);
     acc_lo += mult;
     if (acc_lo < mult) ++acc_hi;
-  }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
-  uint64_t lo2 = acc_lo, hi2 = acc_hi;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
-    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
-    const uint64_t sm = lo2 + l2;
-    hi2 += h2 + (sm < lo2 ? 1 : 0);
-    lo2 = sm;
-  }
-  acc_sum = warp_sum(acc_sum);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
-  if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
-    }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
-    if (lo2) {
-      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
-      if (old + lo2 < old) ++hi2;
-    }
-    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
-    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
-    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
-  }
-}
-
-// ILP variant of k_last_gj for the common case where the new variable x is the
-// last head variable (so the tuple hash is step(prefix(binding), x)): each
-// thread owns a run of R consecutive candidates, split at binding
-// boundaries; inside a run the binding state is loaded once and the R cover
-// reads and R first-bucket probes are issued back to back.
-template <int NS, int R, int W>
-__global__ void __launch_bounds__(TILE) k_last_gj_ilp(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                      uint64_t F, const uint64_t* __restrict__ bounds,
-                                                      int min_var, DevCounters* ctr) {
-  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
-  long long acc_min = LLONG_MAX;
-  const int lane = threadIdx.x & 31;
-  const uint64_t* __restrict__ scan = N.scan;
-  const int nhead = N.nhead;
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * R; base < c1; base += (uint64_t)gridDim.x * TILE * R) {
-    uint64_t i = base + (uint64_t)threadIdx.x * R;
-    const uint64_t iend = min(i + R, c1);
-    if (i >= iend) continue;
-    const uint64_t t = (i - c0) / TILE;
-    uint64_t e = upper_bound_u64(scan, __ldg(bounds + t), __ldg(bounds + t + 1), i);
-    while (i < iend) {
-      const uint64_t se = __ldg(scan + e);
-      const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
-      const uint64_t bend = min(iend, se);  // this batch: candidates [i, bend) of binding e
-      // binding state
-      const int ci = N.chosen[e];
-      uint32_t sp[NS], sl[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const KSub& P = N.sub[s];
-        if (P.in_p) {
-          sp[s] = FJG_LD_STREAM(P.in_p + e);
-          sl[s] = FJG_LD_STREAM(P.in_len + e);
-        } else {
-          sp[s] = 0;
-          sl[s] = P.root_n;
-        }
-      }
-      const uint64_t mult0 = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
-      uint64_t pre = fj::kTupleHashSeed;
-      long long bmin = LLONG_MAX;
-#pragma unroll
-      for (int v = 0; v < W; ++v)
-        if (v < nhead - 1) {
-          const int32_t hvv = FJG_LD_STREAM(N.in_var[v] + e);
-          pre = fj::tuple_hash_step(pre, (int64_t)hvv);
-          if (v == min_var) bmin = hvv;
-        }
-      uint32_t cbase = 0;
-      const int32_t* csrc = nullptr;
-#pragma unroll
-      for (int s = 0; s < NS; ++s)
-        if (s == ci) {
-          cbase = sp[s] + (uint32_t)(i - prev);
-          csrc = N.sub[s].src[0];
-        }
-      // R cover reads
-      int32_t x[R];
-      bool live[R];
-      uint64_t mu[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        live[r] = i + r < bend;
-        x[r] = live[r] ? FJG_LD_STREAM(csrc + cbase + r) : 0;
-        mu[r] = mult0;
-        if (live[r]) ++body;
-      }
-      // probes, R first buckets in flight per subatom
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s == ci) continue;
-        const KSub& P = N.sub[s];
-        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
-        uint4 h0[R];
-        uint64_t b0[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          b0[r] = region_bucket(sp[s], sl[s], (uint32_t)x[r]);
-          h0[r] = live[r] ? __ldg(tb + 2 * b0[r]) : make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!live[r]) continue;
-          ++probes;
-          const uint32_t kw = (uint32_t)x[r];
-          uint32_t q = kEmpty;
-          bool more = false;
-          if (h0[r].y == kEmpty) {
-          } else if (h0[r].x == kw) {
-            q = h0[r].y;
-          } else if (h0[r].w == kEmpty) {
-          } else if (h0[r].z == kw) {
-            q = h0[r].w;
-          } else {
-            more = true;
-          }
-          if (more) {  // rest of the bucket, then the following buckets
-            uint64_t b = b0[r];
-            uint4 h1 = __ldg(tb + 2 * b + 1);
-            while (true) {
-              if (h1.y == kEmpty) break;
-              if (h1.x == kw) { q = h1.y; break; }
-              if (h1.w == kEmpty) break;
-              if (h1.z == kw) { q = h1.w; break; }
-              if (++b == bhi) b = blo;
-              const uint4 a0 = __ldg(tb + 2 * b);
-              if (a0.y == kEmpty) break;
-              if (a0.x == kw) { q = a0.y; break; }
-              if (a0.w == kEmpty) break;
-              if (a0.z == kw) { q = a0.w; break; }
-              h1 = __ldg(tb + 2 * b + 1);
-            }
-          }
-          if (q == kEmpty) {
-            ++misses;
-            live[r] = false;
-          } else if (P.last) {
-            mu[r] *= __ldg(P.cnt + q);
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!live[r]) continue;
-        const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x[r]);
-        acc_sum += mu[r] * fj::checksum_word(h);
-        acc_lo += mu[r];
-        if (acc_lo < mu[r]) ++acc_hi;
-        if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x[r] : bmin);
-      }
-      i = bend;
-      ++e;
-    }
   }
   probes = warp_sum(probes);
   misses = warp_sum(misses);
@@ -359,12 +166,15 @@ struct HitQueue {  // per-warp ring buffers
   uint32_t tail[NW];
 };
 
-// k_last_gj_ilp with the probe path made branch-free and the fold batched:
-// the probed subatoms are selected by index (s = j + (j >= chosen)) so one
-// code path serves every cover choice; each probe is one 256-bit bucket load
-// and a priority select; survivors are folded from a per-warp queue (leaf
-// multiplicities, head-prefix hash, checksum, MIN). Same algorithm and
-// results as k_last_gj_ilp (the fold is order-independent).
+// GJ-shaped last node when x is the last head variable (tuple hash =
+// step(prefix(binding), x)): each thread owns a run of R consecutive
+// candidates (its binding found inside the warp's 64-candidate chunk owner
+// range, split at binding boundaries); binding state is loaded once per run,
+// cover reads are coalesced, and the R probes are issued back to back. The
+// probed subatoms are selected by index (s = j + (j >= chosen)) so one code
+// path serves every cover choice; each probe is one 256-bit bucket load and a
+// priority select; survivors are folded from a per-warp queue (leaf
+// multiplicities, head-prefix hash, checksum, MIN) with every lane busy.
 template <int NS, int R, int W>
 __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_bf(const __grid_constant__ KNode N, uint64_t c0,
                                                                      uint64_t c1, uint64_t F,
@@ -544,9 +354,6 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_
   }
 }
 
-#ifndef FJG_GJ_KERNEL
-#define FJG_GJ_KERNEL 1  // GJ last node: 0 k_last_gj_ilp, 1 k_last_gj_bf
-#endif
 #ifndef FJG_GJ_R
 #define FJG_GJ_R 2
 #endif

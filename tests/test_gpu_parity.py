@@ -368,3 +368,61 @@ def test_backends_configs(engine, name):
     for b in ("colt", "slt", "simple"):  # noqa: B007
         r = q.execute(backend=b)
         assert (r.count, r.checksum) == (ref["count"], ref["checksum"]), b
+
+
+def _fmix32(h):
+    h = np.asarray(h, dtype=np.uint64) & 0xFFFFFFFF
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & 0xFFFFFFFF
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & 0xFFFFFFFF
+    h ^= h >> 16
+    return h
+
+
+def _colliding_keys(rng, length, bucket, n, exclude=()):
+    """n int32 keys whose first bucket inside a `length`-bucket region is
+    `bucket` (region_bucket in kernels/common.cuh)."""
+    out = []
+    while len(out) < n:
+        k = rng.integers(-2**31, 2**31, 4096, dtype=np.int64)
+        off = (_fmix32((k & 0xFFFFFFFF) ^ 0x9E3779B9) * length) >> 32
+        out.extend(int(x) for x in k[off == bucket] if int(x) not in exclude and int(x) not in out)
+    return out[:n]
+
+
+def test_bucket_collisions_and_extreme_keys(engine):
+    """Adversarial probes for the last-node kernels: 40 keys of one subtrie
+    all hashed to its last bucket (a 10-bucket overflow chain that wraps to
+    the region start), misses that walk the whole chain, and the int32
+    extremes (INT32_MIN, INT32_MAX, -1 whose key word equals the empty
+    marker, 0) as vertices -- every plan mode and backend vs the oracle."""
+    rng = np.random.default_rng(99)
+    A, B, C = 7, 11, 13
+    extremes = [-2**31, 2**31 - 1, -1, 0]
+    sa = _colliding_keys(rng, 48, 47, 44, exclude=[A, B, C] + extremes)     # A's region: 48 rows
+    sa = sa[:44] + [B, C] + extremes[:2]                                   # 48 out-neighbours of A
+    miss = _colliding_keys(rng, 48, 47, 6, exclude=sa + [A] + extremes)    # collide with A's chain, absent
+    tb = sa[:3] + sa[-6:-2] + miss + extremes                              # B: hits, misses, extremes
+    tc = sa[10:30] + miss[:2]                                              # C: longer list
+    edges = [(A, x) for x in sa] + [(B, x) for x in tb] + [(C, x) for x in tc]
+    edges += [(x, y) for x, y in zip(extremes, reversed(extremes)) if x != y]
+    edges += [(int(x), int(y)) for x, y in rng.integers(-50, 50, (300, 2)) if x != y]
+    edges = sorted(set(edges))
+    order = rng.permutation(len(edges))
+    src = np.array([edges[i][0] for i in order], np.int32)
+    dst = np.array([edges[i][1] for i in order], np.int32)
+    q = [{"rel": "E1", "vars": ["a", "b"]}, {"rel": "E2", "vars": ["b", "c"]}, {"rel": "E3", "vars": ["a", "c"]}]
+    cols = [[src, dst]] * 3
+    rel = engine.relation([src, dst])
+    for mode in ("binary", "free", "generic"):
+        plan = P.compile_plan({"query": q, "binary_plan": ["join", ["join", "E1", "E2"], "E3"]}, mode)
+        ref = oracle.execute(q, plan, cols, output_mode="enumerate")
+        qq = engine.query({"query": q}, plan, [rel, rel, rel])
+        for backend in ("colt", "simple"):
+            r = qq.execute(backend=backend)
+            assert (r.count, r.checksum) == (ref["count"], ref["checksum"]), (mode, backend)
+        rows, _ = qq.enumerate()
+        assert bag_equal(rows, ref["tuples"])
+        qq.close()
+    assert ref["count"] > 0
