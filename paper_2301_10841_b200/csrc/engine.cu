@@ -713,7 +713,7 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   const uint64_t nb = std::max<uint64_t>(cap, kLastChunk) / TILE + 2;
   if (nb > q->bounds_cap) {
     q->bounds = (uint64_t*)q->alloc(nb * 8);
-    q->chunk_owner = (uint32_t*)q->alloc((kLastChunk / (32 * FJG_GJ_R) + 2) * 4);
+    q->chunk_owner = (uint32_t*)q->alloc((std::max<uint64_t>(cap, kLastChunk) / 32 + 2) * 4);
     q->bounds_cap = nb;
   }
   // CUB temp storage for the largest scans
@@ -723,7 +723,8 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
                                    (int64_t)std::max<uint64_t>(q->max_n, 1)));
   size_t b3 = 0;
   CK(cub::DeviceScan::InclusiveScan(nullptr, b3, (uint32_t*)nullptr, (uint32_t*)nullptr, MaxOp(),
-                                    (int64_t)std::max<uint64_t>(q->max_n, 1)));
+                                    (int64_t)std::max<uint64_t>(std::max<uint64_t>(q->max_n, 1),
+                                                                std::max<uint64_t>(cap, kLastChunk) / 32 + 2)));
   size_t b4 = 0, b5 = 0;
   const int64_t nm = (int64_t)std::max<uint64_t>(q->max_n, 1);
   CK(cub::DeviceRadixSort::SortPairs(nullptr, b4, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -788,6 +789,18 @@ static void force_root_sorted(fjg_query* q, int t) {
   q->maps_built += 1;
   q->rows_forced += n;
   T.lev[0].dirty = true;
+}
+
+// Chunk owners for [c0, c1) at `chunk` candidates per chunk (k_chunk_marks + max-scan).
+static void chunk_owners(fjg_query* q, const uint64_t* scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk) {
+  fjg_engine* eng = q->eng;
+  const uint64_t n = (c1 - c0 + chunk - 1) / chunk + 1;
+  CK(cudaMemsetAsync(q->chunk_owner, 0, n * 4, eng->stream));
+  LAUNCH(eng, k_chunk_marks<<<grid_for(F), 256, 0, eng->stream>>>(scan, F, c0, c1, chunk, q->chunk_owner));
+  size_t bytes = q->cub_tmp_bytes;
+  CK(cub::DeviceScan::InclusiveScan(q->cub_tmp, bytes, q->chunk_owner, q->chunk_owner, MaxOp(), (int64_t)n,
+                                    eng->stream));
+  ++eng->launches;
 }
 
 static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, uint32_t len0, uint32_t count) {
@@ -918,7 +931,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
                            FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
       if (gj_fast)
-        LAUNCH(eng, k_chunk_owner<<<grid_for(F), 256, 0, eng->stream>>>(N.scan, F, c0, c1, 32 * FJG_GJ_R, q->chunk_owner));
+        chunk_owners(q, N.scan, F, c0, c1, 32 * FJG_GJ_R);
       else
         LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
@@ -972,18 +985,22 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, survivors), 0, 4, eng->stream));
     q->mark(eng->stream, -1);
     const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
-    LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
+    const bool gj_write = q->gj_w[k] >= 0 && FJG_GJ_WRITE;
+    if (gj_write)
+      chunk_owners(q, N.scan, F, c0, c1, 32);
+    else
+      LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
     const unsigned gw = grid_for(c1 - c0, TILE, eng->num_sms * 8);
-    if (q->gj_w[k] >= 0 && FJG_GJ_WRITE) {
+    if (gj_write) {
       const int w8 = q->width <= 4 ? 4 : 8;
       if (N.nsub == 2 && w8 == 4)
-        LAUNCH(eng, (k_write_gj<2, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+        LAUNCH(eng, (k_write_gj<2, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner, q->gj_w[k], q->d_ctr)));
       else if (N.nsub == 2)
-        LAUNCH(eng, (k_write_gj<2, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+        LAUNCH(eng, (k_write_gj<2, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner, q->gj_w[k], q->d_ctr)));
       else if (w8 == 4)
-        LAUNCH(eng, (k_write_gj<3, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+        LAUNCH(eng, (k_write_gj<3, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner, q->gj_w[k], q->d_ctr)));
       else
-        LAUNCH(eng, (k_write_gj<3, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->gj_w[k], q->d_ctr)));
+        LAUNCH(eng, (k_write_gj<3, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner, q->gj_w[k], q->d_ctr)));
     } else if (q->sw[k] && FJG_STREAM_WRITE) {
       if (q->width <= 4)
         LAUNCH(eng, (k_write_stream<4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->d_ctr)));

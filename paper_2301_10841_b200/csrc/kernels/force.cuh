@@ -77,58 +77,68 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
   const int32_t* src[MAXK];
 #pragma unroll
   for (int t = 0; t < MAXK; ++t) src[t] = t < nk ? level_src(T, lev, L.keycol[t]) : nullptr;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t p, len, pos;
-    force_locate(R, i, p, len, pos);
-    int32_t vals[MAXK];
-#pragma unroll
-    for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
-    const uint32_t kw = key_word_r(nk, vals);
-    const unsigned long long mine = ((unsigned long long)kPendBit << 32) | kw;
-    const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
-    uint64_t h = 4ull * region_bucket(p, len, kw);
+  __shared__ uint32_t s_cnt, s_base;
+  const int lane = threadIdx.x & 31;
+  // block-uniform trip count: the new-slot append is aggregated per block
+  for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < total; b0 += gridDim.x * blockDim.x) {
+    const uint32_t i = b0 + threadIdx.x;
     bool won = false;
-    while (true) {
-      unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
-      unsigned long long cur = *((volatile unsigned long long*)addr);
-      if ((uint32_t)(cur >> 32) == kEmpty) {
-        const unsigned long long old = atomicCAS(addr, cur, mine);
-        if (old == cur) {
-          won = true;
-          if (MULTI) {
-            *((volatile uint32_t*)(L.srep + h)) = pos + 1;
-            __threadfence();
-          }
-          break;
-        }
-        cur = old;
-      }
-      if ((uint32_t)cur == kw) {
-        if (!MULTI) break;
-        uint32_t r;
-        while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
-        }
-        bool eq = true;
+    uint64_t h = 0;
+    uint32_t p = 0;
+    if (i < total) {
+      uint32_t len, pos;
+      force_locate(R, i, p, len, pos);
+      int32_t vals[MAXK];
 #pragma unroll
-        for (int t = 0; t < MAXK; ++t)
-          if (t < nk && src[t][r - 1] != vals[t]) eq = false;
-        if (eq) break;
+      for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
+      const uint32_t kw = key_word_r(nk, vals);
+      const unsigned long long mine = ((unsigned long long)kPendBit << 32) | kw;
+      const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
+      h = 4ull * region_bucket(p, len, kw);
+      while (true) {
+        unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
+        unsigned long long cur = *((volatile unsigned long long*)addr);
+        if ((uint32_t)(cur >> 32) == kEmpty) {
+          const unsigned long long old = atomicCAS(addr, cur, mine);
+          if (old == cur) {
+            won = true;
+            if (MULTI) {
+              *((volatile uint32_t*)(L.srep + h)) = pos + 1;
+              __threadfence();
+            }
+            break;
+          }
+          cur = old;
+        }
+        if ((uint32_t)cur == kw) {
+          if (!MULTI) break;
+          uint32_t r;
+          while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
+          }
+          bool eq = true;
+#pragma unroll
+          for (int t = 0; t < MAXK; ++t)
+            if (t < nk && src[t][r - 1] != vals[t]) eq = false;
+          if (eq) break;
+        }
+        if (++h == hi) h = lo;
       }
-      if (++h == hi) h = lo;
+      const uint32_t rank = atomicAdd(&L.table[h].q, 1u) & ~kPendBit;
+      tmp_slot[pos] = (uint32_t)h;
+      tmp_rank[pos] = rank;
     }
-    const uint32_t rank = atomicAdd(&L.table[h].q, 1u) & ~kPendBit;
-    tmp_slot[pos] = (uint32_t)h;
-    tmp_rank[pos] = rank;
-    // warp-aggregated append of new slots
-    const unsigned act = __activemask();
-    const unsigned wmask = __ballot_sync(act, won);
+    // append the new slots: one global atomic per block iteration
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const unsigned wmask = __ballot_sync(0xffffffffu, won);
+    uint32_t wbase = 0;
+    if (lane == 0 && wmask) wbase = atomicAdd(&s_cnt, (uint32_t)__popc(wmask));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(&ctr->newslots, s_cnt) : 0u;
+    __syncthreads();
     if (won) {
-      const int lane = threadIdx.x & 31;
-      const int leader = __ffs(wmask) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&ctr->newslots, (uint32_t)__popc(wmask));
-      base = __shfl_sync(wmask, base, leader);
-      const uint32_t o = base + __popc(wmask & ((1u << lane) - 1));
+      const uint32_t o = s_base + wbase + __popc(wmask & ((1u << lane) - 1));
       newslots[o] = (uint32_t)h;
       newslot_p[o] = p;
     }

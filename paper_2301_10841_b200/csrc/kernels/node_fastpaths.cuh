@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_
 // block-compacted into the next frontier.
 template <int NS, int W>
 __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
-                                                   uint64_t F, const uint64_t* __restrict__ bounds, int xvar,
+                                                   uint64_t F, const uint32_t* __restrict__ owner, int xvar,
                                                    DevCounters* ctr) {
   __shared__ uint32_t s_warp[TILE / 32];
   __shared__ uint32_t s_base;
@@ -378,8 +378,6 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t* __restrict__ scan = N.scan;
   for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
-    const uint64_t t = (base - c0) / TILE;
-    const uint64_t lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
     const uint64_t i = base + threadIdx.x;
     bool alive = i < c1;
     uint64_t e = 0, mult = 1;
@@ -388,7 +386,8 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
 #pragma unroll
     for (int s = 0; s < NS; ++s) chp[s] = chl[s] = 0;
     if (alive) {
-      e = upper_bound_u64(scan, lo, hi, i);
+      const uint64_t t = (i - c0) / 32;  // this warp's 32-candidate chunk
+      e = upper_bound_u64(scan, __ldg(owner + t), __ldg(owner + t + 1), i);
       const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
       const int ci = N.chosen[e];
       uint32_t sp[NS], sl[NS];
@@ -429,20 +428,11 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
         const uint32_t kw = (uint32_t)x;
         uint64_t b = region_bucket(sp[s], sl[s], kw);
         const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
-        const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
-        uint32_t q = kEmpty;
-        while (true) {
-          const uint4 h0 = __ldg(tb + 2 * b);
-          if (h0.y == kEmpty) break;
-          if (h0.x == kw) { q = h0.y; break; }
-          if (h0.w == kEmpty) break;
-          if (h0.z == kw) { q = h0.w; break; }
-          const uint4 h1 = __ldg(tb + 2 * b + 1);
-          if (h1.y == kEmpty) break;
-          if (h1.x == kw) { q = h1.y; break; }
-          if (h1.w == kEmpty) break;
-          if (h1.z == kw) { q = h1.w; break; }
+        bool more;
+        uint32_t q = bucket_match(ld_bucket(P.table, b), kw, more);
+        while (more) {
           if (++b == bhi) b = blo;
+          q = bucket_match(ld_bucket(P.table, b), kw, more);
         }
         if (q == kEmpty) {
           ++misses;

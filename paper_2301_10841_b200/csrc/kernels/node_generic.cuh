@@ -37,18 +37,20 @@ __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uin
 }
 
 // Owner of every CHUNK-candidate chunk of [c0, c1) (the binding containing the
-// chunk's first candidate), written by scattering from the bindings: each
-// binding owns the chunk starts inside its candidate range. owner[nchunks] =
+// chunk's first candidate), pass 1: each binding marks the first chunk start
+// inside its candidate range (owner[] zeroed first); an inclusive max-scan
+// then fills the rest (owners grow with the chunk index). owner[nchunks] =
 // owner of c1 - 1. A thread's run then searches only [owner[t], owner[t+1]],
 // which is usually a single binding.
-__global__ void k_chunk_owner(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk,
+__global__ void k_chunk_marks(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk,
                               uint32_t* __restrict__ owner) {
   const uint64_t nch = (c1 - c0 + chunk - 1) / chunk;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < F; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull, se = __ldg(scan + e);
     const uint64_t lo = max(prev, c0), hi = min(se, c1);
     if (lo >= hi) continue;
-    for (uint64_t c = (lo - c0 + chunk - 1) / chunk; c * chunk + c0 < hi; ++c) owner[c] = (uint32_t)e;
+    const uint64_t c = (lo - c0 + chunk - 1) / chunk;
+    if (c * chunk + c0 < hi) owner[c] = (uint32_t)e;
     if (hi == c1) owner[nch] = (uint32_t)e;
   }
 }

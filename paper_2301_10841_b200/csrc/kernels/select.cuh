@@ -8,22 +8,36 @@
 __device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters* ctr, const KSub& S, uint32_t p,
                                               uint32_t len, bool need) {
   // Warp-level dedup of identical subtries (bindings of one parent are
-  // adjacent in the frontier), then a CAS on the state word.
+  // adjacent in the frontier), a CAS on the state word, then one list append
+  // per warp (the list counter is a single hot address).
   const unsigned act = __activemask();
   const unsigned want = __ballot_sync(act, need);
-  if (!need) return;
-  const unsigned grp = __match_any_sync(want, p);
-  const int leader = __ffs(grp) - 1;
-  if ((int)(threadIdx.x & 31) != leader) return;
+  if (!want) return;
+  const int lane = threadIdx.x & 31;
+  bool lead = false;
+  if (need) {
+    const unsigned grp = __match_any_sync(want, p);
+    lead = lane == __ffs(grp) - 1;
+  }
   if (S.depth == 0) {
-    ctr->root_need[S.trie] = 1;
+    if (lead) ctr->root_need[S.trie] = 1;
     return;
   }
   const DevLevel& L = tries[S.trie].lev[S.depth];
-  if (atomicCAS(L.state + p, 0u, 1u) == 0u) {
+  bool won = false;
+  if (lead && atomicCAS(L.state + p, 0u, 1u) == 0u) {
+    won = true;
     L.cursor[p] = 0;
     L.nkeys[p] = 0;
-    const uint32_t idx = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], 1u);
+  }
+  const unsigned wm = __ballot_sync(act, won);
+  if (!wm) return;
+  const int first = __ffs(wm) - 1;
+  uint32_t base = 0;
+  if (lane == first) base = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], (uint32_t)__popc(wm));
+  base = __shfl_sync(act, base, first);
+  if (won) {
+    const uint32_t idx = base + __popc(wm & ((1u << lane) - 1u));
     L.list_p[idx] = p;
     L.list_len[idx] = len;
   }
