@@ -566,6 +566,7 @@ static void build_knodes(fjg_query* q) {
       S.in_p = open ? N.in.p[D.atom] : nullptr;
       S.in_len = open ? N.in.len[D.atom] : nullptr;
       S.root_n = N.atom_n[D.atom];
+      S.rregion = q->d_ctr->root_region + D.trie;
       S.nv = (uint8_t)D.nv;
       S.bound_mask = (uint8_t)D.bound_mask;
       S.stream = (uint8_t)D.stream;
@@ -767,7 +768,6 @@ static void force_root_sorted(fjg_query* q, int t) {
   R.p0 = 0;
   R.len0 = n;
   const unsigned g = grid_for(n, 256, eng->num_sms * 16);
-  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, 0, R));
   uint32_t *keys = q->tmp_slot, *rows = q->tmp_rank, *skeys = q->newslots, *srows = q->newslot_p;
   uint32_t* starts = q->owner_scratch;
   uint8_t* flags = q->sort_flags;
@@ -782,6 +782,8 @@ static void force_root_sorted(fjg_query* q, int t) {
   CK(cub::DeviceSelect::Flagged(q->cub_tmp, bytes, thrust::counting_iterator<uint32_t>(0), flags, starts, ng,
                                 (int64_t)n, eng->stream));
   ++eng->launches;
+  // the root's slot region shrinks to one bucket per distinct key (load <= 0.25)
+  LAUNCH(eng, k_root_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, ng, q->d_ctr));
   LAUNCH(eng, k_root_insert<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, skeys, starts, ng, q->d_ctr));
   LAUNCH(eng, k_root_gather<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, srows));
   q->mark(eng->stream, 0);
@@ -1034,6 +1036,7 @@ static void reset_query(fjg_query* q) {
   DevCounters z;
   memset(&z, 0, sizeof(z));
   z.minv = LLONG_MAX;
+  for (size_t t = 0; t < q->tries.size(); ++t) z.root_region[t] = (uint32_t)std::max<uint64_t>(q->tries[t].rel->nrows, 1);
   memcpy(q->h_ctr, &z, sizeof(z));
   CK(cudaMemcpyAsync(q->d_ctr, q->h_ctr, sizeof(z), cudaMemcpyHostToDevice, eng->stream));
   q->maps_built = q->forces = q->rows_forced = 0;
@@ -1098,7 +1101,8 @@ static void eager_build(fjg_query* q) {
       CK(cudaMemsetAsync(cntp, 0, 4, eng->stream));
       const DevLevel& P = T.dev.lev[l - 1];
       const DevLevel& L = T.dev.lev[l];
-      LAUNCH(eng, k_eager_list<<<grid_for(nslots), 256, 0, eng->stream>>>(P.table, nslots, P.cnt, L, cntp));
+      LAUNCH(eng, k_eager_list<<<grid_for(nslots), 256, 0, eng->stream>>>(
+                      P.table, nslots, P.cnt, L, cntp, l == 1 ? q->d_ctr->root_region + t : nullptr));
       sync_counters(q);
       const uint32_t c = q->h_ctr->list_count[t * MAXL + l];
       if (c) {

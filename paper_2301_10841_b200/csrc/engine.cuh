@@ -134,6 +134,7 @@ struct KSub {
   const uint32_t* in_p;       // frontier subtrie column of this atom (null: root)
   const uint32_t* in_len;
   uint32_t root_n;
+  const uint32_t* rregion;    // root probe region (DevCounters::root_region[trie])
   int8_t var[MAXK];
   uint8_t nv, bound_mask, stream, last, atom, trie, depth, pad;
 };
@@ -188,6 +189,7 @@ struct DevCounters {
   uint32_t newslots;
   uint32_t list_count[MAXT * MAXL];
   uint32_t root_need[MAXT];
+  uint32_t root_region[MAXT];  // buckets of each trie's root slot region (rows, or distinct keys once sorted)
 };
 
 }  // namespace fjg

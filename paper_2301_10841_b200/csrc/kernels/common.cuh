@@ -40,6 +40,12 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Probe region (buckets) of a subtrie: its length, except for a root, whose
+// region is set by its force (rows, or distinct keys when force-sorted).
+__device__ __forceinline__ uint32_t probe_region(const KSub& S, uint32_t len) {
+  return S.in_p ? len : *S.rregion;
+}
+
 // COLT get (Fig 12 `get` = force, then lookup): the subtrie was forced by an
 // earlier kernel of this node, so this is a pure lookup in its slot region:
 // read a bucket (one sector, as two 16-byte halves), stop at a match or at the
@@ -48,6 +54,7 @@ __device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len
                                          uint32_t& q, uint32_t& ql) {
   const int nk = P.nv;
   const uint32_t kw = key_word_r(nk, key);
+  len = probe_region(P, len);
   uint64_t b = region_bucket(p, len, kw);
   const uint64_t blo = p, bhi = (uint64_t)p + len;
   const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);

@@ -260,6 +260,22 @@ __global__ void k_root_starts(const uint32_t* __restrict__ skeys, uint32_t n, ui
     flags[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
 }
 
+// clear the sorted root's G-bucket slot region and all n child counts
+__global__ void k_root_clear(const DevTrie* __restrict__ tries, int trie, uint32_t n,
+                             const uint32_t* __restrict__ ngroups, DevCounters* ctr) {
+  const DevLevel& L = tries[trie].lev[0];
+  const uint32_t G = max(*ngroups, 1u);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    L.cnt[i] = 0;
+    if (i < G) {
+      uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * i;
+      t[0] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      t[1] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->root_region[trie] = G;
+}
+
 // one thread per distinct key: its group is [starts[g], starts[g+1])
 __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint32_t n, const uint32_t* __restrict__ skeys,
                               const uint32_t* __restrict__ starts, const uint32_t* __restrict__ ngroups,
@@ -270,8 +286,9 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
     const uint32_t q = starts[g];
     const uint32_t c = (g + 1 < G ? starts[g + 1] : n) - q;
     const uint32_t kw = skeys[q];
-    const uint64_t lo = 0, hi = 4ull * n;
-    uint64_t h = 4ull * region_bucket(0u, n, kw);
+    const uint32_t RG = max(G, 1u);  // region: one bucket per distinct key
+    const uint64_t lo = 0, hi = 4ull * RG;
+    uint64_t h = 4ull * region_bucket(0u, RG, kw);
     const unsigned long long mine = ((unsigned long long)q << 32) | kw;
     while (true) {
       unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
@@ -302,9 +319,11 @@ __global__ void k_root_gather(const DevTrie* __restrict__ tries, int trie, uint3
 // names a child subtrie (start q, length cnt[q]) to force at level l.
 // (Same bookkeeping as a claim in k_select: the child's cursor / key count restart.)
 __global__ void k_eager_list(const Slot* __restrict__ table, uint64_t nslots, const uint32_t* __restrict__ cnt,
-                             DevLevel child, uint32_t* __restrict__ list_count) {
+                             DevLevel child, uint32_t* __restrict__ list_count,
+                             const uint32_t* __restrict__ root_region) {
   uint32_t* __restrict__ list_p = child.list_p;
   uint32_t* __restrict__ list_len = child.list_len;
+  if (root_region) nslots = 4ull * *root_region;  // a root's live slots
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t q = table[s].q;
     if (q == kEmpty) continue;

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
         sl[s] = __ldg(P.in_len + e);
       } else {
         sp[s] = 0;
-        sl[s] = P.root_n;
+        sl[s] = *P.rregion;  // root: its probe region
       }
     }
     uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_
             sl[s] = __ldg(P.in_len + e);
           } else {
             sp[s] = 0;
-            sl[s] = P.root_n;
+            sl[s] = *P.rregion;  // root: its probe region
           }
         }
         uint32_t cbase = sp[0];
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
           sl[s] = __ldg(P.in_len + e);
         } else {
           sp[s] = 0;
-          sl[s] = P.root_n;
+          sl[s] = *P.rregion;  // root: its probe region
         }
       }
       if (N.in_mult) mult = __ldg(N.in_mult + e);
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(TILE) k_write_stream(const __grid_constant__ K
           pl = __ldg(P.in_len + e);
         } else {
           pp = 0;
-          pl = P.root_n;
+          pl = *P.rregion;  // root: its probe region
         }
         ++probes;
         const uint32_t kw = (uint32_t)key;
