@@ -848,7 +848,8 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     CK(cudaMemsetAsync(L.cursor + (l == 0 ? 0 : p0), 0, 4, eng->stream));
     CK(cudaMemsetAsync(L.nkeys + (l == 0 ? 0 : p0), 0, 4, eng->stream));
   }
-  CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, newslots), 0, 4, eng->stream));
+  CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, newslots), 0, 8, eng->stream));
+  static_assert(offsetof(DevCounters, dup) == offsetof(DevCounters, newslots) + 4, "newslots, dup adjacent");
   const unsigned g = grid_for(upper, 256, eng->num_sms * 16);
   LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   if (T.lev[l].multi)
@@ -864,7 +865,8 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   else
     LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, q->newslots,
                                                                    q->newslot_p, q->d_ctr));
-  LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank));
+  LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank, q->d_ctr));
+  LAUNCH(eng, k_force_unique<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->d_ctr));
   LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   // keys inserted accumulate on the device
   q->mark(eng->stream, 0);

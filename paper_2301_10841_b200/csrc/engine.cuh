@@ -187,6 +187,7 @@ struct DevCounters {
   uint64_t total_m;
   uint32_t survivors;
   uint32_t newslots;
+  uint32_t dup;  // the running force met a repeated key (else every child is a single row)
   uint32_t list_count[MAXT * MAXL];
   uint32_t root_need[MAXT];
   uint32_t root_region[MAXT];  // buckets of each trie's root slot region (rows, or distinct keys once sorted)

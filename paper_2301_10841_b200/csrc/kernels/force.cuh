@@ -111,7 +111,10 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
           cur = old;
         }
         if ((uint32_t)cur == kw) {
-          if (!MULTI) break;
+          if (!MULTI) {
+            ctr->dup = 1u;
+            break;
+          }
           uint32_t r;
           while ((r = *((volatile uint32_t*)(L.srep + h))) == 0u) {
           }
@@ -119,7 +122,10 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
 #pragma unroll
           for (int t = 0; t < MAXK; ++t)
             if (t < nk && src[t][r - 1] != vals[t]) eq = false;
-          if (eq) break;
+          if (eq) {
+            ctr->dup = 1u;
+            break;
+          }
         }
         if (++h == hi) h = lo;
       }
@@ -150,6 +156,7 @@ template <bool SINGLE>
 __global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0,
                                const uint32_t* __restrict__ newslots, const uint32_t* __restrict__ newslot_p,
                                DevCounters* ctr) {
+  if (!ctr->dup) return;  // k_force_unique handles the all-distinct case
   const DevLevel& L = tries[trie].lev[lev];
   const uint32_t total = ctr->newslots;
   typedef cub::BlockScan<uint32_t, 256> BS;
@@ -211,7 +218,9 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int 
 }
 
 __global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
-                                const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank) {
+                                const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank,
+                                const DevCounters* __restrict__ ctr) {
+  if (!ctr->dup) return;
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[lev];
   const uint32_t total = force_total(R);
@@ -223,6 +232,32 @@ __global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int
     for (int c = 0; c < T.ncols; ++c) {
       int32_t* out = L.cval[c];
       if (out) out[dst] = level_src(T, lev, c)[pos];
+    }
+  }
+}
+
+// All keys distinct (no repeated key met by k_force_insert): every row is its
+// own child group, so the grouping is the identity -- child start = the row's
+// position, count 1, clustered columns copied in place. Replaces assign +
+// scatter (a graph level of deduplicated edges always takes this path).
+__global__ void k_force_unique(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                               const uint32_t* __restrict__ tmp_slot, const DevCounters* __restrict__ ctr) {
+  if (ctr->dup) return;
+  const DevTrie& T = tries[trie];
+  const DevLevel& L = T.lev[lev];
+  const uint32_t total = force_total(R);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t p, len, pos;
+    force_locate(R, i, p, len, pos);
+    L.table[tmp_slot[pos]].q = pos;
+    L.cnt[pos] = 1;
+    if (pos == p) {
+      L.nkeys[lev == 0 ? 0 : p] = len;
+      L.cursor[lev == 0 ? 0 : p] = len;
+    }
+    for (int c = 0; c < T.ncols; ++c) {
+      int32_t* out = L.cval[c];
+      if (out) out[pos] = level_src(T, lev, c)[pos];
     }
   }
 }
