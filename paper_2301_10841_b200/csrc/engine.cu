@@ -567,6 +567,7 @@ static void build_knodes(fjg_query* q) {
       S.in_len = open ? N.in.len[D.atom] : nullptr;
       S.root_n = N.atom_n[D.atom];
       S.rregion = q->d_ctr->root_region + D.trie;
+      S.ldup = q->d_ctr->level_dup + D.trie * MAXL + D.depth;
       S.nv = (uint8_t)D.nv;
       S.bound_mask = (uint8_t)D.bound_mask;
       S.stream = (uint8_t)D.stream;

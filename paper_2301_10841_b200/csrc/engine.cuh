@@ -135,6 +135,7 @@ struct KSub {
   const uint32_t* in_len;
   uint32_t root_n;
   const uint32_t* rregion;    // root probe region (DevCounters::root_region[trie])
+  const uint32_t* ldup;       // DevCounters::level_dup of this level: 0 = every child count is 1
   int8_t var[MAXK];
   uint8_t nv, bound_mask, stream, last, atom, trie, depth, pad;
 };
@@ -191,6 +192,7 @@ struct DevCounters {
   uint32_t list_count[MAXT * MAXL];
   uint32_t root_need[MAXT];
   uint32_t root_region[MAXT];  // buckets of each trie's root slot region (rows, or distinct keys once sorted)
+  uint32_t level_dup[MAXT * MAXL];  // some force of (trie, level) met a repeated key: child counts can exceed 1
 };
 
 }  // namespace fjg

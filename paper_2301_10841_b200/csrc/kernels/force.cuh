@@ -113,6 +113,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
         if ((uint32_t)cur == kw) {
           if (!MULTI) {
             ctr->dup = 1u;
+            ctr->level_dup[trie * MAXL + lev] = 1u;
             break;
           }
           uint32_t r;
@@ -124,6 +125,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
             if (t < nk && src[t][r - 1] != vals[t]) eq = false;
           if (eq) {
             ctr->dup = 1u;
+            ctr->level_dup[trie * MAXL + lev] = 1u;
             break;
           }
         }
@@ -331,6 +333,7 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
       if (++h == hi) h = lo;
     }
     L.cnt[q] = c;
+    if (c > 1) ctr->level_dup[trie * MAXL] = 1u;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     L.nkeys[0] = G;

@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_
       for (int j = 0; j < NS - 1; ++j) {
         const uint32_t* cnt = j >= ci ? N.sub[j + 1].cnt : N.sub[j].cnt;
         const bool plast = j >= ci ? N.sub[j + 1].last : N.sub[j].last;
-        if (plast) mu *= __ldg(cnt + Q.q[j][wi][slot]);
+        const uint32_t* ldup = j >= ci ? N.sub[j + 1].ldup : N.sub[j].ldup;
+        if (plast && *ldup) mu *= __ldg(cnt + Q.q[j][wi][slot]);  // leaf multiplicity (1 on unit levels)
       }
       uint64_t pre = fj::kTupleHashSeed;
       long long bmin = LLONG_MAX;
