@@ -268,6 +268,7 @@ struct fjg_query {
   int gj_x[MAXN];  // per node: the GJ fast-path variable, or -1
   int gj_w[MAXN];  // per node: the GJ frontier-writing fast-path variable, or -1
   bool sw[MAXN];   // per node: the stream-cover frontier-writing fast path applies
+  SProbe sprobe[MAXN];  // per node: probe plan of the single-binding stream kernel (np = 0: n/a)
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   uint32_t* chunk_owner = nullptr;  // chunk -> owning entry (GJ last node)
@@ -515,6 +516,32 @@ static int gj_last_var(const KNode& G, const DevNode& N);
 static int gj_write_var(const DevNode& N, int width);
 static bool stream_write_ok(const DevNode& N, const KNode& G);
 
+// Probe plan of k_stream_one: probe j = the j-th non-cover subatom in node
+// order, keyed on the cover column binding its variable. Needs distinct cover
+// variables and at most four probes (else np = 0: the generic stream kernel).
+static SProbe stream_probe_plan(const DevNode& N, bool sw) {
+  SProbe P;
+  memset(&P, 0, sizeof(P));
+  if (!sw || N.nsub - 1 > 4) return P;
+  const DevSub& C = N.sub[N.cov[0]];
+  for (int a = 0; a < C.nv; ++a)
+    for (int b = a + 1; b < C.nv; ++b)
+      if (C.var[a] == C.var[b]) return P;
+  int np = 0;
+  for (int s = 0; s < N.nsub; ++s) {
+    if (s == N.cov[0]) continue;
+    int kc = -1;
+    for (int t = 0; t < C.nv; ++t)
+      if (C.var[t] == N.sub[s].var[0]) kc = t;
+    if (kc < 0) return SProbe{};
+    P.s[np] = (int8_t)s;
+    P.kc[np] = (int8_t)kc;
+    ++np;
+  }
+  P.np = np;
+  return P;
+}
+
 static void build_knodes(fjg_query* q) {
   const size_t K = q->nodes.size();
   q->knodes.assign(K, KNode{});
@@ -581,6 +608,7 @@ static void build_knodes(fjg_query* q) {
     q->gj_x[k] = gj_last_var(q->knodes[k], q->nodes[k]);
     q->gj_w[k] = gj_write_var(q->nodes[k], q->width);
     q->sw[k] = stream_write_ok(q->nodes[k], q->knodes[k]);
+    q->sprobe[k] = stream_probe_plan(q->nodes[k], q->sw[k]);
   }
 }
 
@@ -909,6 +937,36 @@ static void force_claims(fjg_query* q, int k) {
   (void)k;
 }
 
+#ifndef FJG_STREAM_ONE
+#define FJG_STREAM_ONE 1
+#endif
+template <int NP, int W>
+static void launch_stream_one_w(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
+  constexpr int R = 4;
+  fjg_engine* eng = q->eng;
+  const uint64_t warps = (c1 - c0 + 32 * R - 1) / (32 * R);
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((warps + TILE / 32 - 1) / (TILE / 32),
+                                                                         (uint64_t)eng->num_sms * 8));
+  LAUNCH(eng, (k_stream_one<NP, R, W><<<g, TILE, 0, eng->stream>>>(KN, SP, c0, c1, q->d_ctr)));
+}
+template <int NP>
+static void launch_stream_one_np(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
+  if (q->width <= 4)
+    launch_stream_one_w<NP, 4>(q, KN, SP, c0, c1);
+  else if (q->width <= 8)
+    launch_stream_one_w<NP, 8>(q, KN, SP, c0, c1);
+  else
+    launch_stream_one_w<NP, 16>(q, KN, SP, c0, c1);
+}
+static void launch_stream_one(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
+  switch (SP.np) {
+    case 1: launch_stream_one_np<1>(q, KN, SP, c0, c1); break;
+    case 2: launch_stream_one_np<2>(q, KN, SP, c0, c1); break;
+    case 3: launch_stream_one_np<3>(q, KN, SP, c0, c1); break;
+    default: launch_stream_one_np<4>(q, KN, SP, c0, c1); break;
+  }
+}
+
 static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (F == 0) return;
   q->node_inputs[k] += F;
@@ -991,9 +1049,10 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     q->mark(eng->stream, -1);
     const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
     const bool gj_write = q->gj_w[k] >= 0 && FJG_GJ_WRITE;
+    const bool one = F == 1 && q->sprobe[k].np > 0 && FJG_STREAM_ONE;
     if (gj_write)
       chunk_owners(q, N.scan, F, c0, c1, 32);
-    else
+    else if (!one)
       LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
     const unsigned gw = grid_for(c1 - c0, TILE, eng->num_sms * 8);
     if (gj_write) {
@@ -1006,6 +1065,8 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
         LAUNCH(eng, (k_write_gj<3, 4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner, q->gj_w[k], q->d_ctr)));
       else
         LAUNCH(eng, (k_write_gj<3, 8><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner, q->gj_w[k], q->d_ctr)));
+    } else if (one) {
+      launch_stream_one(q, KN, q->sprobe[k], c0, c1);
     } else if (q->sw[k] && FJG_STREAM_WRITE) {
       if (q->width <= 4)
         LAUNCH(eng, (k_write_stream<4><<<gw, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->bounds, q->d_ctr)));

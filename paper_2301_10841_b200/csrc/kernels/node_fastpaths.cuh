@@ -668,6 +668,174 @@ __global__ void __launch_bounds__(TILE) k_write_stream(const __grid_constant__ K
   }
 }
 
+// Single-binding stream node (F == 1: node 0 of a plan whose first node
+// iterates a base table, C1 chain / C3 star): no binding search at all, the
+// candidate index is the row. Each warp owns 32*R consecutive rows, lane l the
+// rows base + r*32 + l (every column load is coalesced); the probes are issued
+// subatom by subatom with the R bucket loads of a lane back to back, and a
+// warp stops as soon as none of its rows is alive (most star rows die at the
+// first dimension). The probe key columns are resolved on the host (SProbe),
+// child lengths are read only for survivors, and survivors take one
+// warp-aggregated atomic -- no block barriers.
+struct SProbe {
+  int np;          // probed subatoms
+  int8_t s[4];     // subatom index of probe j (node order)
+  int8_t kc[4];    // cover column (index into the cover's src[]) holding probe j's key
+};
+
+template <int NP, int R, int W>
+__global__ void __launch_bounds__(TILE) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
+                                                     uint64_t c1, DevCounters* ctr) {
+  uint64_t probes = 0, misses = 0, body = 0;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int ci = N.cov[0];
+  const KSub& S = N.sub[ci];
+  const uint32_t pos0 = S.in_p ? __ldg(S.in_p) : 0u;
+  const uint64_t mult0 = N.in_mult ? __ldg(N.in_mult) : 1ull;
+  uint32_t pp[NP], pl[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const KSub& P = N.sub[SP.s[j]];
+    if (P.in_p) {
+      pp[j] = __ldg(P.in_p);
+      pl[j] = __ldg(P.in_len);
+    } else {
+      pp[j] = 0;
+      pl[j] = *P.rregion;
+    }
+  }
+  const uint64_t gw = (uint64_t)gridDim.x * (TILE / 32);
+  for (uint64_t w = (uint64_t)blockIdx.x * (TILE / 32) + (threadIdx.x >> 5);; w += gw) {
+    const uint64_t base = c0 + w * (32ull * R);
+    if (base >= c1) break;
+    bool live[R];
+    uint32_t qv[R][NP];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      live[r] = base + r * 32 + lane < c1;
+      body += live[r] ? 1 : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) any |= live[r];
+      if (!__any_sync(0xffffffffu, any)) break;
+      const KSub& P = N.sub[SP.s[j]];
+      const int32_t* __restrict__ kcol = S.src[SP.kc[j]];
+      uint32_t kw[R];
+      uint64_t b0[R];
+      Bucket8 h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        kw[r] = live[r] ? (uint32_t)__ldg(kcol + pos0 + (uint32_t)(base + r * 32 + lane)) : 0u;
+        b0[r] = region_bucket(pp[j], pl[j], kw[r]);
+        if (live[r]) h[r] = ld_bucket(P.table, b0[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!live[r]) continue;
+        ++probes;
+        bool more;
+        uint32_t q = bucket_match(h[r], kw[r], more);
+        if (more) {
+          uint64_t b = b0[r];
+          const uint64_t blo = pp[j], bhi = (uint64_t)pp[j] + pl[j];
+          do {
+            if (++b == bhi) b = blo;
+            q = bucket_match(ld_bucket(P.table, b), kw[r], more);
+          } while (more);
+        }
+        if (q == kEmpty) {
+          ++misses;
+          live[r] = false;
+        }
+        qv[r][j] = q;
+      }
+    }
+    // survivors: one warp-aggregated atomic for the warp's R rounds
+    unsigned bal[R];
+    uint32_t tot = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      bal[r] = __ballot_sync(0xffffffffu, live[r]);
+      tot += __popc(bal[r]);
+    }
+    if (tot == 0) continue;
+    uint32_t o = 0;
+    if (lane == 0) o = atomicAdd(&ctr->survivors, tot);
+    o = __shfl_sync(0xffffffffu, o, 0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (live[r]) {
+        const uint32_t at = o + __popc(bal[r] & lt_mask);
+        const uint32_t pos = pos0 + (uint32_t)(base + r * 32 + lane);
+        uint64_t mult = mult0;
+        uint32_t chp[NP], chl[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          const KSub& P = N.sub[SP.s[j]];
+          const uint32_t ql = __ldg(P.cnt + qv[r][j]);
+          chp[j] = P.last ? 0u : qv[r][j];
+          chl[j] = P.last ? 0u : ql;
+          if (P.last) mult *= ql;
+        }
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+          if ((N.out_vars >> v) & 1u) {
+            int32_t val = 0;
+            bool cov = false;
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k)
+              if (k < S.nv && S.var[k] == v) {
+                val = __ldg(S.src[k] + pos);
+                cov = true;
+              }
+            N.out_var[v][at] = cov ? val : __ldg(N.in_var[v]);
+          }
+#pragma unroll
+        for (int a = 0; a < W; ++a)
+          if ((N.out_atoms >> a) & 1u) {
+            uint32_t pa = 0, la = 0;
+            bool here = false;
+            if (S.atom == a) {
+              pa = kSingleton;
+              la = 1u;
+              here = true;
+            }
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+              if (N.sub[SP.s[j]].atom == a) {
+                pa = chp[j];
+                la = chl[j];
+                here = true;
+              }
+            if (!here) {
+              pa = __ldg(N.in_p[a]);
+              la = __ldg(N.in_len[a]);
+            }
+            N.out_p[a][at] = pa;
+            N.out_len[a][at] = la;
+          }
+        if (N.out_mult) N.out_mult[at] = mult;
+      }
+      o += __popc(bal[r]);
+    }
+  }
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+  }
+}
+
 // The stream fast path: a single cover in stream mode whose subtrie is never a
 // singleton, all its variables fresh; every other subatom probes one variable
 // the cover binds.
