@@ -940,14 +940,22 @@ static void force_claims(fjg_query* q, int k) {
 #ifndef FJG_STREAM_ONE
 #define FJG_STREAM_ONE 1
 #endif
-template <int NP, int W>
-static void launch_stream_one_w(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
-  constexpr int R = 4;
+template <int NP, int R, int W>
+static void launch_stream_one_rw(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
   fjg_engine* eng = q->eng;
+  static int occ = 0;  // resident blocks per SM (persistent grid: one wave)
+  if (!occ) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream_one<NP, R, W>, TILE, 0));
+    occ = std::max(occ, 1);
+  }
   const uint64_t warps = (c1 - c0 + 32 * R - 1) / (32 * R);
   const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((warps + TILE / 32 - 1) / (TILE / 32),
-                                                                         (uint64_t)eng->num_sms * 8));
+                                                                         (uint64_t)eng->num_sms * occ));
   LAUNCH(eng, (k_stream_one<NP, R, W><<<g, TILE, 0, eng->stream>>>(KN, SP, c0, c1, q->d_ctr)));
+}
+template <int NP, int W>
+static void launch_stream_one_w(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
+  launch_stream_one_rw<NP, 4, W>(q, KN, SP, c0, c1);
 }
 template <int NP>
 static void launch_stream_one_np(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {

@@ -683,11 +683,121 @@ struct SProbe {
   int8_t kc[4];    // cover column (index into the cover's src[]) holding probe j's key
 };
 
+// First half of a bucket (slots 0-1) in one 128-bit load; slots fill in order,
+// so a free slot among them ends a miss, and only a full half without the key
+// reads the second half (rare at load <= 0.25).
+__device__ __forceinline__ uint32_t half_match(const uint4& a, uint32_t kw, bool& more) {
+  uint32_t q = (a.w != kEmpty && a.z == kw) ? a.w : kEmpty;
+  q = (a.y != kEmpty && a.x == kw) ? a.y : q;
+  more = a.w != kEmpty && q == kEmpty;
+  return q;
+}
+__device__ __forceinline__ uint32_t probe_rest(const Slot* table, uint64_t b, uint64_t blo, uint64_t bhi,
+                                               uint32_t kw) {
+  const uint4* tb = reinterpret_cast<const uint4*>(table);
+  bool more;
+  const uint4 h1 = __ldg(tb + 2 * b + 1);
+  uint32_t q = half_match(h1, kw, more);
+  while (more) {
+    if (++b == bhi) b = blo;
+    q = bucket_match(ld_bucket(table, b), kw, more);
+  }
+  return q;
+}
+
+// probe one key in a subtrie region (first half-bucket already loaded)
+__device__ __forceinline__ uint32_t probe_region_one(const Slot* table, uint32_t p, uint32_t len, uint32_t kw) {
+  const uint32_t b = (uint32_t)region_bucket(p, len, kw);
+  bool more;
+  const uint32_t q = half_match(__ldg(reinterpret_cast<const uint4*>(table) + 2ull * b), kw, more);
+  return more ? probe_rest(table, b, p, (uint64_t)p + len, kw) : q;
+}
+
+template <int NP, int W>
+struct StreamOneCtx {
+  static constexpr int QC = 256;  // per-warp ring capacity per stage (>= 32*R + 31)
+};
+template <int NP, int R>
+struct StreamOneQC {
+  static constexpr int QC = R <= 7 ? 256 : 512;  // per-warp ring capacity per stage (>= 32*R + 31)
+};
+
+// Write one surviving row (lanes with live set) to the next frontier. qlast is
+// the last probe's result; earlier probes are repeated (survivors only).
+template <int NP, int W>
+__device__ __forceinline__ void stream_one_write(const KNode& N, const SProbe& SP, const KSub& S, bool live,
+                                                 uint32_t row, uint32_t qlast, uint32_t pos0, uint64_t mult0,
+                                                 const uint32_t (&pp)[NP], const uint32_t (&pl)[NP],
+                                                 DevCounters* ctr, int lane) {
+  const unsigned bal = __ballot_sync(0xffffffffu, live);
+  if (!bal) return;
+  uint32_t o = 0;
+  if (lane == 0) o = atomicAdd(&ctr->survivors, (uint32_t)__popc(bal));
+  o = __shfl_sync(0xffffffffu, o, 0);
+  if (!live) return;
+  const uint32_t at = o + __popc(bal & ((1u << lane) - 1u));
+  const uint32_t pos = pos0 + row;
+  uint64_t mult = mult0;
+  uint32_t chp[NP], chl[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const KSub& P = N.sub[SP.s[j]];
+    const uint32_t q =
+        j == NP - 1 ? qlast
+                    : probe_region_one(P.table, pp[j], pl[j], (uint32_t)__ldg(S.src[SP.kc[j]] + pos));
+    const uint32_t ql = __ldg(P.cnt + q);
+    chp[j] = P.last ? 0u : q;
+    chl[j] = P.last ? 0u : ql;
+    if (P.last) mult *= ql;
+  }
+#pragma unroll
+  for (int v = 0; v < W; ++v)
+    if ((N.out_vars >> v) & 1u) {
+      int32_t val = 0;
+      bool cov = false;
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k)
+        if (k < S.nv && S.var[k] == v) {
+          val = __ldg(S.src[k] + pos);
+          cov = true;
+        }
+      N.out_var[v][at] = cov ? val : __ldg(N.in_var[v]);
+    }
+#pragma unroll
+  for (int a = 0; a < W; ++a)
+    if ((N.out_atoms >> a) & 1u) {
+      uint32_t pa = 0, la = 0;
+      bool here = false;
+      if (S.atom == a) {
+        pa = kSingleton;
+        la = 1u;
+        here = true;
+      }
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+        if (N.sub[SP.s[j]].atom == a) {
+          pa = chp[j];
+          la = chl[j];
+          here = true;
+        }
+      if (!here) {
+        pa = __ldg(N.in_p[a]);
+        la = __ldg(N.in_len[a]);
+      }
+      N.out_p[a][at] = pa;
+      N.out_len[a][at] = la;
+    }
+  if (N.out_mult) N.out_mult[at] = mult;
+}
+
 template <int NP, int R, int W>
-__global__ void __launch_bounds__(TILE) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
-                                                     uint64_t c1, DevCounters* ctr) {
-  uint64_t probes = 0, misses = 0, body = 0;
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(TILE, R <= 4 ? 4 : 3) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
+                                                        uint64_t c1, DevCounters* ctr) {
+  constexpr int QC = StreamOneQC<NP, R>::QC;
+  constexpr int NQ = NP > 1 ? NP - 1 : 1;
+  __shared__ uint32_t Q[NQ][TILE / 32][QC];  // stage j+1 input: rows alive after probe j
+  uint32_t probes = 0, misses = 0, body = 0;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int ci = N.cov[0];
   const KSub& S = N.sub[ci];
@@ -705,134 +815,123 @@ __global__ void __launch_bounds__(TILE) k_stream_one(const __grid_constant__ KNo
       pl[j] = *P.rregion;
     }
   }
-  const uint64_t gw = (uint64_t)gridDim.x * (TILE / 32);
-  for (uint64_t w = (uint64_t)blockIdx.x * (TILE / 32) + (threadIdx.x >> 5);; w += gw) {
-    const uint64_t base = c0 + w * (32ull * R);
-    if (base >= c1) break;
-    bool live[R];
-    uint32_t qv[R][NP];
+  uint32_t qhead[NQ], qtail[NQ];  // warp-uniform ring cursors
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      live[r] = base + r * 32 + lane < c1;
-      body += live[r] ? 1 : 0;
+  for (int j = 0; j < NQ; ++j) qhead[j] = qtail[j] = 0;
+
+  // push rows alive after probe j into stage j+1's queue, or write them (last probe)
+  auto advance = [&](int j, bool live, uint32_t row, uint32_t q) {
+    if (j == NP - 1) {
+      stream_one_write<NP, W>(N, SP, S, live, row, q, pos0, mult0, pp, pl, ctr, lane);
+    } else {
+      const unsigned bal = __ballot_sync(0xffffffffu, live);
+#pragma unroll
+      for (int t = 0; t < NQ; ++t)
+        if (t == j) {
+          if (live) Q[t][wi][(qtail[t] + __popc(bal & lt_mask)) & (QC - 1)] = row;
+          qtail[t] += __popc(bal);
+        }
     }
+  };
+  // stage j >= 1: n (<= 32) queued rows, one per lane
+  auto stage = [&](int j, uint32_t n) {
+    bool live = (uint32_t)lane < n;
+    uint32_t row = 0;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      bool any = false;
+    for (int t = 0; t < NQ; ++t)
+      if (t == j - 1) {
+        if (live) row = Q[t][wi][(qhead[t] + lane) & (QC - 1)];
+        qhead[t] += n;
+      }
+    __syncwarp();
+    uint32_t q = kEmpty;
 #pragma unroll
-      for (int r = 0; r < R; ++r) any |= live[r];
-      if (!__any_sync(0xffffffffu, any)) break;
-      const KSub& P = N.sub[SP.s[j]];
-      const int32_t* __restrict__ kcol = S.src[SP.kc[j]];
-      uint32_t kw[R];
-      uint64_t b0[R];
-      Bucket8 h[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        kw[r] = live[r] ? (uint32_t)__ldg(kcol + pos0 + (uint32_t)(base + r * 32 + lane)) : 0u;
-        b0[r] = region_bucket(pp[j], pl[j], kw[r]);
-        if (live[r]) h[r] = ld_bucket(P.table, b0[r]);
+    for (int t = 1; t < NP; ++t)
+      if (t == j && live) {
+        const KSub& P = N.sub[SP.s[t]];
+        ++probes;
+        q = probe_region_one(P.table, pp[t], pl[t], (uint32_t)__ldg(S.src[SP.kc[t]] + pos0 + row));
+        if (q == kEmpty) {
+          ++misses;
+          live = false;
+        }
       }
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!live[r]) continue;
+    for (int t = 1; t < NP; ++t)
+      if (t == j) advance(t, live, row, q);
+  };
+
+  // F == 1: candidates are positions of one subtrie (< 2^31), 32-bit indices
+  const uint32_t gstep = gridDim.x * (TILE / 32) * 32u * R;
+  const uint32_t e1 = (uint32_t)c1;
+  const int32_t* __restrict__ kcol0 = S.src[SP.kc[0]] + pos0;
+  const KSub& P0 = N.sub[SP.s[0]];
+  const uint4* __restrict__ tb0 = reinterpret_cast<const uint4*>(P0.table);
+  uint32_t base = (uint32_t)c0 + (blockIdx.x * (TILE / 32) + wi) * 32u * R;
+  // software pipeline: the next chunk's first-probe keys stream into shared
+  // memory (cp.async, double buffer) while this chunk probes; each lane copies
+  // and reads only its own slots, so no warp barrier is needed.
+  __shared__ uint32_t KB[2][TILE / 32][32 * R];
+  auto prefetch = [&](uint32_t b, int buf) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = b + r * 32 + lane;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&KB[buf][wi][r * 32 + lane]);
+      const int32_t* src = kcol0 + (i < e1 ? i : 0u);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(i < e1 ? 4 : 0));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  prefetch(base, 0);
+  int buf = 0;
+  for (; base < e1; base += gstep, buf ^= 1) {
+    prefetch(base + gstep, buf ^ 1);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    uint32_t kw[R], b0[R];
+    bool live[R];
+    uint4 h[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      live[r] = base + r * 32 + lane < e1;
+      body += live[r] ? 1u : 0u;
+      kw[r] = KB[buf][wi][r * 32 + lane];
+      b0[r] = (uint32_t)region_bucket(pp[0], pl[0], kw[r]);
+      if (live[r]) h[r] = __ldg(tb0 + 2ull * b0[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t q = kEmpty;
+      if (live[r]) {
         ++probes;
         bool more;
-        uint32_t q = bucket_match(h[r], kw[r], more);
-        if (more) {
-          uint64_t b = b0[r];
-          const uint64_t blo = pp[j], bhi = (uint64_t)pp[j] + pl[j];
-          do {
-            if (++b == bhi) b = blo;
-            q = bucket_match(ld_bucket(P.table, b), kw[r], more);
-          } while (more);
-        }
+        q = half_match(h[r], kw[r], more);
+        if (more) q = probe_rest(P0.table, b0[r], pp[0], (uint64_t)pp[0] + pl[0], kw[r]);
         if (q == kEmpty) {
           ++misses;
           live[r] = false;
         }
-        qv[r][j] = q;
       }
+      advance(0, live[r], base + r * 32 + lane, q);
     }
-    // survivors: one warp-aggregated atomic for the warp's R rounds
-    unsigned bal[R];
-    uint32_t tot = 0;
+    // later stages on full batches of 32 queued rows
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      bal[r] = __ballot_sync(0xffffffffu, live[r]);
-      tot += __popc(bal[r]);
-    }
-    if (tot == 0) continue;
-    uint32_t o = 0;
-    if (lane == 0) o = atomicAdd(&ctr->survivors, tot);
-    o = __shfl_sync(0xffffffffu, o, 0);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (live[r]) {
-        const uint32_t at = o + __popc(bal[r] & lt_mask);
-        const uint32_t pos = pos0 + (uint32_t)(base + r * 32 + lane);
-        uint64_t mult = mult0;
-        uint32_t chp[NP], chl[NP];
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          const KSub& P = N.sub[SP.s[j]];
-          const uint32_t ql = __ldg(P.cnt + qv[r][j]);
-          chp[j] = P.last ? 0u : qv[r][j];
-          chl[j] = P.last ? 0u : ql;
-          if (P.last) mult *= ql;
-        }
-#pragma unroll
-        for (int v = 0; v < W; ++v)
-          if ((N.out_vars >> v) & 1u) {
-            int32_t val = 0;
-            bool cov = false;
-#pragma unroll
-            for (int k = 0; k < MAXK; ++k)
-              if (k < S.nv && S.var[k] == v) {
-                val = __ldg(S.src[k] + pos);
-                cov = true;
-              }
-            N.out_var[v][at] = cov ? val : __ldg(N.in_var[v]);
-          }
-#pragma unroll
-        for (int a = 0; a < W; ++a)
-          if ((N.out_atoms >> a) & 1u) {
-            uint32_t pa = 0, la = 0;
-            bool here = false;
-            if (S.atom == a) {
-              pa = kSingleton;
-              la = 1u;
-              here = true;
-            }
-#pragma unroll
-            for (int j = 0; j < NP; ++j)
-              if (N.sub[SP.s[j]].atom == a) {
-                pa = chp[j];
-                la = chl[j];
-                here = true;
-              }
-            if (!here) {
-              pa = __ldg(N.in_p[a]);
-              la = __ldg(N.in_len[a]);
-            }
-            N.out_p[a][at] = pa;
-            N.out_len[a][at] = la;
-          }
-        if (N.out_mult) N.out_mult[at] = mult;
-      }
-      o += __popc(bal[r]);
-    }
+    for (int j = 1; j < NP; ++j)
+      while (qtail[j - 1] - qhead[j - 1] >= 32) stage(j, 32);
   }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  // drain the partial batches, stage by stage
+#pragma unroll
+  for (int j = 1; j < NP; ++j)
+    while (qtail[j - 1] != qhead[j - 1]) stage(j, min(32u, qtail[j - 1] - qhead[j - 1]));
+  const uint64_t tprobes = warp_sum((uint64_t)probes), tmisses = warp_sum((uint64_t)misses),
+                 tbody = warp_sum((uint64_t)body);
   if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    if (tprobes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)tprobes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)tprobes);
     }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (tmisses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)tmisses);
+    if (tbody) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)tbody);
   }
 }
 
