@@ -269,6 +269,7 @@ struct fjg_query {
   int gj_w[MAXN];  // per node: the GJ frontier-writing fast-path variable, or -1
   bool sw[MAXN];   // per node: the stream-cover frontier-writing fast path applies
   SProbe sprobe[MAXN];  // per node: probe plan of the single-binding stream kernel (np = 0: n/a)
+  std::vector<TailPlan> tails;  // per node: fused Cartesian tail from this node on (ntail = 0: n/a)
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   uint32_t* chunk_owner = nullptr;  // chunk -> owning entry (GJ last node)
@@ -542,6 +543,35 @@ static SProbe stream_probe_plan(const DevNode& N, bool sw) {
   return P;
 }
 
+// Fused Cartesian tail from node k (k_tail): every node k..K-1 has exactly one
+// subatom, a stream-iterated cover of fresh variables (SPEC.md:423-431's pure
+// Cartesian suffix), over distinct atoms whose subtrie at node k is in its
+// frontier or is the root.
+static TailPlan tail_plan(const fjg_query* q, int k) {
+  TailPlan T;
+  memset(&T, 0, sizeof(T));
+  const int K = (int)q->nodes.size();
+  if (K - k > MAXTAIL || q->width > 16) return T;
+  const DevNode& Nk = q->nodes[k];
+  uint32_t seen = 0;
+  for (int j = k; j < K; ++j) {
+    const DevNode& N = q->nodes[j];
+    if (N.nsub != 1 || N.ncov != 1) return TailPlan{};
+    const DevSub& D = N.sub[0];
+    if (!D.stream || D.bound_mask || !D.last || ((seen >> D.atom) & 1u)) return TailPlan{};
+    seen |= 1u << D.atom;
+    const int t = j - k;
+    T.node[t] = j;
+    T.open[t] = (Nk.in_atoms >> D.atom) & 1u;
+    if (!T.open[t] && D.depth != 0) return TailPlan{};
+    T.in_p[t] = T.open[t] ? Nk.in.p[D.atom] : nullptr;
+    T.in_len[t] = T.open[t] ? Nk.in.len[D.atom] : nullptr;
+    T.sub[t] = q->knodes[j].sub[0];
+  }
+  T.ntail = K - k;
+  return T;
+}
+
 static void build_knodes(fjg_query* q) {
   const size_t K = q->nodes.size();
   q->knodes.assign(K, KNode{});
@@ -610,6 +640,8 @@ static void build_knodes(fjg_query* q) {
     q->sw[k] = stream_write_ok(q->nodes[k], q->knodes[k]);
     q->sprobe[k] = stream_probe_plan(q->nodes[k], q->sw[k]);
   }
+  q->tails.assign(K, TailPlan{});
+  for (size_t k = 0; k < K; ++k) q->tails[k] = tail_plan(q, (int)k);
 }
 
 // Chain-suffix analysis for the memoised factorised count (mirrors the
@@ -975,10 +1007,42 @@ static void launch_stream_one(fjg_query* q, const KNode& KN, const SProbe& SP, u
   }
 }
 
+#ifndef FJG_TAIL
+#define FJG_TAIL 1
+#endif
+template <int MODE>
+static void launch_tail(fjg_query* q, int k, uint64_t F) {
+  fjg_engine* eng = q->eng;
+  const KNode& KN = q->knodes[k];
+  const TailPlan& T = q->tails[k];
+  const unsigned g = grid_for(F, TILE, eng->num_sms * 8);
+  if (q->width <= 4)
+    LAUNCH(eng, (k_tail<MODE, 4><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
+                                                              q->d_ctr)));
+  else if (q->width <= 8)
+    LAUNCH(eng, (k_tail<MODE, 8><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
+                                                              q->d_ctr)));
+  else
+    LAUNCH(eng, (k_tail<MODE, 16><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
+                                                               q->d_ctr)));
+}
+
 static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (F == 0) return;
   q->node_inputs[k] += F;
   fjg_engine* eng = q->eng;
+  if (FJG_TAIL && q->tails[k].ntail > 0 && (mode == EXPAND_COUNT || mode == EXPAND_ENUM) && q->stop_node < 0) {
+    // nodes k..K-1 in one kernel: no per-node select / scan / host sync
+    q->mark(eng->stream, -1);
+    if (mode == EXPAND_COUNT)
+      launch_tail<EXPAND_COUNT>(q, k, F);
+    else
+      launch_tail<EXPAND_ENUM>(q, k, F);
+    q->mark(eng->stream, 2);
+    q->last_launches += 1;
+    q->last_candidates += F;
+    return;
+  }
   const DevNode& N = q->nodes[k];
   const bool memo_top = mode == EXPAND_MEMO && k == q->stop_node;
   const KNode& KN = memo_top ? q->memo_top : q->knodes[k];
@@ -1520,7 +1584,7 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     for (int k = 0; k < MAXN && k < FJG_MAX_NODES; ++k) {
       r.node_body_entries[k] = H.body[k];
       r.node_probes[k] = H.node_probes[k];
-      r.node_inputs[k] = q->node_inputs[k];
+      r.node_inputs[k] = q->node_inputs[k] + H.tail_inputs[k];
     }
     r.maps_built = q->maps_built;
     r.keys_inserted = H.keys_inserted;

@@ -193,6 +193,20 @@ struct DevCounters {
   uint32_t root_need[MAXT];
   uint32_t root_region[MAXT];  // buckets of each trie's root slot region (rows, or distinct keys once sorted)
   uint32_t level_dup[MAXT * MAXL];  // some force of (trie, level) met a repeated key: child counts can exceed 1
+  uint64_t tail_inputs[MAXN];  // node inputs counted on the device (fused Cartesian tail nodes)
+};
+
+// Fused Cartesian tail (nodes k..K-1 each one stream-iterated subatom binding
+// only fresh variables: SPEC.md:423-431's pure Cartesian suffix): every
+// binding of node k's frontier expands to the product of its tail subtries.
+constexpr int MAXTAIL = 4;
+struct TailPlan {
+  int ntail;
+  int node[MAXTAIL];           // plan node of tail subatom j
+  int open[MAXTAIL];           // atom has a subtrie in node k's frontier (else: its root, depth 0)
+  const uint32_t* in_p[MAXTAIL];
+  const uint32_t* in_len[MAXTAIL];
+  KSub sub[MAXTAIL];
 };
 
 }  // namespace fjg

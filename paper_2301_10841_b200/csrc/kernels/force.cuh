@@ -79,6 +79,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
   for (int t = 0; t < MAXK; ++t) src[t] = t < nk ? level_src(T, lev, L.keycol[t]) : nullptr;
   __shared__ uint32_t s_cnt, s_base;
   const int lane = threadIdx.x & 31;
+  bool sawdup = false;  // a repeated key: flagged once per block at the end (one hot address)
   // block-uniform trip count: the new-slot append is aggregated per block
   for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < total; b0 += gridDim.x * blockDim.x) {
     const uint32_t i = b0 + threadIdx.x;
@@ -112,8 +113,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
         }
         if ((uint32_t)cur == kw) {
           if (!MULTI) {
-            ctr->dup = 1u;
-            ctr->level_dup[trie * MAXL + lev] = 1u;
+            sawdup = true;
             break;
           }
           uint32_t r;
@@ -124,8 +124,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
           for (int t = 0; t < MAXK; ++t)
             if (t < nk && src[t][r - 1] != vals[t]) eq = false;
           if (eq) {
-            ctr->dup = 1u;
-            ctr->level_dup[trie * MAXL + lev] = 1u;
+            sawdup = true;
             break;
           }
         }
@@ -150,6 +149,10 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
       newslots[o] = (uint32_t)h;
       newslot_p[o] = p;
     }
+  }
+  if (__syncthreads_or(sawdup) && threadIdx.x == 0) {
+    ctr->dup = 1u;
+    ctr->level_dup[trie * MAXL + lev] = 1u;
   }
 }
 
@@ -319,6 +322,7 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
                               DevCounters* ctr) {
   const DevLevel& L = tries[trie].lev[0];
   const uint32_t G = *ngroups;
+  bool sawdup = false;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
     const uint32_t q = starts[g];
     const uint32_t c = (g + 1 < G ? starts[g + 1] : n) - q;
@@ -333,8 +337,9 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
       if (++h == hi) h = lo;
     }
     L.cnt[q] = c;
-    if (c > 1) ctr->level_dup[trie * MAXL] = 1u;
+    sawdup |= c > 1;
   }
+  if (__any_sync(0xffffffffu, sawdup) && (threadIdx.x & 31) == 0) ctr->level_dup[trie * MAXL] = 1u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     L.nkeys[0] = G;
     L.state[0] = 2u;

@@ -707,10 +707,14 @@ __device__ __forceinline__ uint32_t probe_rest(const Slot* table, uint64_t b, ui
 
 // probe one key in a subtrie region (first half-bucket already loaded)
 __device__ __forceinline__ uint32_t probe_region_one(const Slot* table, uint32_t p, uint32_t len, uint32_t kw) {
-  const uint32_t b = (uint32_t)region_bucket(p, len, kw);
+  uint64_t b = (uint32_t)region_bucket(p, len, kw);
   bool more;
-  const uint32_t q = half_match(__ldg(reinterpret_cast<const uint4*>(table) + 2ull * b), kw, more);
-  return more ? probe_rest(table, b, p, (uint64_t)p + len, kw) : q;
+  uint32_t q = bucket_match(ld_bucket(table, b), kw, more);
+  while (more) {
+    if (++b == (uint64_t)p + len) b = p;
+    q = bucket_match(ld_bucket(table, b), kw, more);
+  }
+  return q;
 }
 
 template <int NP, int W>
@@ -791,7 +795,7 @@ __device__ __forceinline__ void stream_one_write(const KNode& N, const SProbe& S
 }
 
 template <int NP, int R, int W>
-__global__ void __launch_bounds__(TILE, R <= 4 ? 4 : 3) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
+__global__ void __launch_bounds__(TILE, 3) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
                                                         uint64_t c1, DevCounters* ctr) {
   constexpr int QC = StreamOneQC<NP, R>::QC;
   constexpr int NQ = NP > 1 ? NP - 1 : 1;
@@ -866,7 +870,6 @@ __global__ void __launch_bounds__(TILE, R <= 4 ? 4 : 3) k_stream_one(const __gri
   const uint32_t e1 = (uint32_t)c1;
   const int32_t* __restrict__ kcol0 = S.src[SP.kc[0]] + pos0;
   const KSub& P0 = N.sub[SP.s[0]];
-  const uint4* __restrict__ tb0 = reinterpret_cast<const uint4*>(P0.table);
   uint32_t base = (uint32_t)c0 + (blockIdx.x * (TILE / 32) + wi) * 32u * R;
   // software pipeline: the next chunk's first-probe keys stream into shared
   // memory (cp.async, double buffer) while this chunk probes; each lane copies
@@ -889,14 +892,14 @@ __global__ void __launch_bounds__(TILE, R <= 4 ? 4 : 3) k_stream_one(const __gri
     asm volatile("cp.async.wait_group 1;\n" ::);
     uint32_t kw[R], b0[R];
     bool live[R];
-    uint4 h[R];
+    Bucket8 h[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       live[r] = base + r * 32 + lane < e1;
       body += live[r] ? 1u : 0u;
       kw[r] = KB[buf][wi][r * 32 + lane];
       b0[r] = (uint32_t)region_bucket(pp[0], pl[0], kw[r]);
-      if (live[r]) h[r] = __ldg(tb0 + 2ull * b0[r]);
+      if (live[r]) h[r] = ld_bucket(P0.table, b0[r]);
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -904,8 +907,14 @@ __global__ void __launch_bounds__(TILE, R <= 4 ? 4 : 3) k_stream_one(const __gri
       if (live[r]) {
         ++probes;
         bool more;
-        q = half_match(h[r], kw[r], more);
-        if (more) q = probe_rest(P0.table, b0[r], pp[0], (uint64_t)pp[0] + pl[0], kw[r]);
+        q = bucket_match(h[r], kw[r], more);
+        if (more) {
+          uint64_t b = b0[r];
+          do {
+            if (++b == (uint64_t)pp[0] + pl[0]) b = pp[0];
+            q = bucket_match(ld_bucket(P0.table, b), kw[r], more);
+          } while (more);
+        }
         if (q == kEmpty) {
           ++misses;
           live[r] = false;
@@ -932,6 +941,154 @@ __global__ void __launch_bounds__(TILE, R <= 4 ? 4 : 3) k_stream_one(const __gri
     }
     if (tmisses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)tmisses);
     if (tbody) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)tbody);
+  }
+}
+
+// Fused Cartesian tail (TailPlan): thread per binding of node k's frontier;
+// a binding whose product exceeds 8 tuples is expanded by its whole warp
+// (lanes stride the product). Each output tuple = the binding's values plus one
+// row of every tail subtrie (mixed-radix index, last tail node fastest); counts,
+// checksum and MIN fold as in the last node, or tuples are written (ENUM).
+template <int MODE, int W>
+__device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, uint64_t e, uint64_t start,
+                                            uint32_t step, bool own, int min_var, int32_t* __restrict__ out_tuples,
+                                            uint64_t out_cap, DevCounters* ctr, uint64_t& acc_lo, uint64_t& acc_hi,
+                                            uint64_t& acc_sum, long long& acc_min, uint64_t (&inputs)[MAXTAIL],
+                                            uint64_t (&body)[MAXTAIL]) {
+  int32_t val[W];
+#pragma unroll
+  for (int v = 0; v < W; ++v) val[v] = ((N.in_vars >> v) & 1u) ? __ldg(N.in_var[v] + e) : 0;
+  const uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+  uint32_t tp[MAXTAIL], tl[MAXTAIL];
+  uint64_t prod = 1;
+#pragma unroll
+  for (int j = 0; j < MAXTAIL; ++j) {
+    if (j >= T.ntail) continue;
+    if (T.open[j]) {
+      tp[j] = __ldg(T.in_p[j] + e);
+      tl[j] = __ldg(T.in_len[j] + e);
+    } else {
+      tp[j] = 0;
+      tl[j] = T.sub[j].root_n;
+    }
+    const uint32_t c = tp[j] == kSingleton ? 1u : tl[j];
+    if (own) inputs[j] += prod;
+    prod *= c;
+    if (own) body[j] += prod;
+  }
+  const bool narrow = prod <= 0xFFFFFFFFull;
+  for (uint64_t idx = start; idx < prod; idx += step) {
+    uint64_t rest = idx;
+#pragma unroll
+    for (int j = MAXTAIL - 1; j >= 0; --j) {
+      if (j >= T.ntail) continue;
+      const uint32_t c = tp[j] == kSingleton ? 1u : tl[j];
+      uint32_t off;
+      if (j == 0) {  // outermost: the remaining index is the offset
+        off = (uint32_t)rest;
+      } else if (narrow) {
+        off = (uint32_t)rest % c;
+        rest = (uint32_t)rest / c;
+      } else {
+        off = (uint32_t)(rest % c);
+        rest /= c;
+      }
+      if (tp[j] == kSingleton) continue;
+      const KSub& S = T.sub[j];
+#pragma unroll
+      for (int t = 0; t < MAXK; ++t)
+        if (t < S.nv) put(val, S.var[t], __ldg(S.src[t] + tp[j] + off));
+    }
+    if (MODE == EXPAND_COUNT) {
+      uint64_t h = fj::kTupleHashSeed;
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if (v < N.nhead) h = fj::tuple_hash_step(h, (int64_t)val[v]);
+      acc_sum += mult * fj::checksum_word(h);
+      acc_lo += mult;
+      if (acc_lo < mult) ++acc_hi;
+      if (min_var >= 0) acc_min = min(acc_min, (long long)sel(val, min_var));
+    } else {
+      const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
+      for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+          if (v < N.nhead) out_tuples[(o + r) * N.nhead + v] = val[v];
+    }
+  }
+}
+
+template <int MODE, int W>
+__global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, const __grid_constant__ TailPlan T,
+                                               uint64_t F, int min_var, int32_t* __restrict__ out_tuples,
+                                               uint64_t out_cap, DevCounters* ctr) {
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0;
+  long long acc_min = LLONG_MAX;
+  uint64_t inputs[MAXTAIL], body[MAXTAIL];
+#pragma unroll
+  for (int j = 0; j < MAXTAIL; ++j) inputs[j] = body[j] = 0;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t b = (uint64_t)blockIdx.x * TILE; b < F; b += (uint64_t)gridDim.x * TILE) {
+    const uint64_t e = b + threadIdx.x;
+    bool big = false;
+    if (e < F) {
+      uint64_t prod = 1;
+#pragma unroll
+      for (int j = 0; j < MAXTAIL; ++j)
+        if (j < T.ntail) {
+          const uint32_t p = T.open[j] ? __ldg(T.in_p[j] + e) : 0u;
+          const uint32_t l = T.open[j] ? __ldg(T.in_len[j] + e) : T.sub[j].root_n;
+          prod *= p == kSingleton ? 1u : l;
+        }
+      big = prod > 8;
+      // small products: this thread alone (and it counts the binding's inputs/body)
+      tail_expand<MODE, W>(N, T, e, big ? ~0ull : 0ull, 1u, true, min_var, out_tuples, out_cap, ctr, acc_lo,
+                           acc_hi, acc_sum, acc_min, inputs, body);
+    }
+    unsigned bm = __ballot_sync(0xffffffffu, big);
+    uint64_t none[MAXTAIL], nb[MAXTAIL];
+    while (bm) {  // big products: the whole warp strides them
+      const int src = __ffs(bm) - 1;
+      bm &= bm - 1;
+      const uint64_t eb = __shfl_sync(0xffffffffu, e, src);
+      tail_expand<MODE, W>(N, T, eb, lane, 32u, false, min_var, out_tuples, out_cap, ctr, acc_lo, acc_hi, acc_sum,
+                           acc_min, none, nb);
+    }
+  }
+  uint64_t lo = acc_lo, hi = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    const uint64_t s = lo + l2;
+    hi += h2 + (s < lo ? 1 : 0);
+    lo = s;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+#pragma unroll
+  for (int j = 0; j < MAXTAIL; ++j) {
+    inputs[j] = warp_sum(inputs[j]);
+    body[j] = warp_sum(body[j]);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < MAXTAIL; ++j)
+      if (j < T.ntail) {
+        // node k's inputs are counted on the host (run_node)
+        if (j > 0 && inputs[j]) atomicAdd((unsigned long long*)&ctr->tail_inputs[T.node[j]], (unsigned long long)inputs[j]);
+        if (body[j]) atomicAdd((unsigned long long*)&ctr->body[T.node[j]], (unsigned long long)body[j]);
+      }
+    if (MODE == EXPAND_COUNT) {
+      if (lo) {
+        const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo);
+        if (old + lo < old) ++hi;
+      }
+      if (hi) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi);
+      if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+      if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+    }
   }
 }
 
