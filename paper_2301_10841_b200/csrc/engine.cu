@@ -905,14 +905,9 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     R.owner = q->owner_scratch;
   }
   q->mark(eng->stream, -1);
-  if (single) {
-    CK(cudaMemsetAsync(L.cursor + (l == 0 ? 0 : p0), 0, 4, eng->stream));
-    CK(cudaMemsetAsync(L.nkeys + (l == 0 ? 0 : p0), 0, 4, eng->stream));
-  }
-  CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, newslots), 0, 8, eng->stream));
-  static_assert(offsetof(DevCounters, dup) == offsetof(DevCounters, newslots) + 4, "newslots, dup adjacent");
   const unsigned g = grid_for(upper, 256, eng->num_sms * 16);
-  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R));
+  // (k_force_clear also resets this force's counters and the root's cursor / key count)
+  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->d_ctr));
   if (T.lev[l].multi)
     LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
                                                                   q->newslots, q->newslot_p, q->d_ctr));
@@ -927,9 +922,9 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, q->newslots,
                                                                    q->newslot_p, q->d_ctr));
   LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank, q->d_ctr));
-  LAUNCH(eng, k_force_unique<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->d_ctr));
-  LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R));
   // keys inserted accumulate on the device
+  LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R,
+                                                                                    q->d_ctr));
   q->mark(eng->stream, 0);
   q->forces += 1;
   q->maps_built += single ? 1 : count;
@@ -937,7 +932,6 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   T.lev[l].dirty = true;
 }
 
-__global__ void k_accum_keys(DevCounters* ctr) { ctr->keys_inserted += ctr->newslots; }
 
 static void run_node(fjg_query* q, int k, uint64_t F, int mode);
 
@@ -949,7 +943,6 @@ static void force_claims(fjg_query* q, int k) {
   for (size_t t = 0; t < q->tries.size(); ++t) {
     if (H.root_need[t] && !q->tries[t].root_forced) {
       force_level(q, (int)t, 0, true, 0, (uint32_t)q->tries[t].rel->nrows, 1);
-      LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
       q->tries[t].root_forced = true;
       any = true;
     }
@@ -957,7 +950,6 @@ static void force_claims(fjg_query* q, int k) {
       const uint32_t c = H.list_count[t * MAXL + l];
       if (c) {
         force_level(q, (int)t, l, false, 0, 0, c);
-        LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
         any = true;
       }
     }
@@ -1049,11 +1041,15 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   const bool is_last = N.is_last || memo_top;
   LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(KN, q->d_tries, F,
                                                                                     q->dynamic ? 1 : 0, q->d_ctr));
-  size_t bytes = q->cub_tmp_bytes;
-  CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, N.m, N.scan, (int64_t)F, eng->stream));
-  ++eng->launches;
-  CK(cudaMemcpyAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, total_m), N.scan + (F - 1), 8,
-                     cudaMemcpyDeviceToDevice, eng->stream));
+  if (F <= kSmallScan) {
+    LAUNCH(eng, k_scan_small<<<1, 1024, 0, eng->stream>>>(N.m, N.scan, (uint32_t)F, q->d_ctr));
+  } else {
+    size_t bytes = q->cub_tmp_bytes;
+    CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, N.m, N.scan, (int64_t)F, eng->stream));
+    ++eng->launches;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, total_m), N.scan + (F - 1), 8,
+                       cudaMemcpyDeviceToDevice, eng->stream));
+  }
   sync_counters(q);
   const uint64_t M = q->h_ctr->total_m;
   force_claims(q, k);
@@ -1193,7 +1189,6 @@ static void run_memo_passes(fjg_query* q) {
   for (int t : tries)
     if (!q->tries[t].root_forced) {
       force_level(q, t, 0, true, 0, (uint32_t)q->tries[t].rel->nrows, 1);
-      LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
       q->tries[t].root_forced = true;
     }
   for (auto& [t, own] : q->owner) {
@@ -1225,7 +1220,6 @@ static void eager_build(fjg_query* q) {
     if (T.map_levels < 1) continue;
     if (!T.root_forced) {
       force_level(q, (int)t, 0, true, 0, (uint32_t)T.rel->nrows, 1);
-      LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
       T.root_forced = true;
     }
     if (q->backend != FJG_BACKEND_SIMPLE) continue;
@@ -1243,7 +1237,6 @@ static void eager_build(fjg_query* q) {
       const uint32_t c = q->h_ctr->list_count[t * MAXL + l];
       if (c) {
         force_level(q, (int)t, l, false, 0, 0, c);
-        LAUNCH(eng, k_accum_keys<<<1, 1, 0, eng->stream>>>(q->d_ctr));
       }
       CK(cudaMemsetAsync(cntp, 0, 4, eng->stream));
     }

@@ -48,9 +48,18 @@ __global__ void k_force_marks(const uint32_t* __restrict__ list_scan, const uint
 
 // clear the slot regions (one 4-slot bucket per position) and child counts of
 // the claimed subtries
-__global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
+__global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                              DevCounters* ctr) {
   const DevLevel& L = tries[trie].lev[lev];
   const uint32_t total = force_total(R);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // this force's counters (read by the later kernels only)
+    ctr->newslots = 0;
+    ctr->dup = 0;
+    if (R.single) {
+      L.cursor[lev == 0 ? 0 : R.p0] = 0;
+      L.nkeys[lev == 0 ? 0 : R.p0] = 0;
+    }
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     uint32_t p, len, pos;
     force_locate(R, i, p, len, pos);
@@ -93,7 +102,8 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
 #pragma unroll
       for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
       const uint32_t kw = key_word_r(nk, vals);
-      const unsigned long long mine = ((unsigned long long)kPendBit << 32) | kw;
+      // the winner's CAS already counts it (rank 0); repeated keys add to the count
+      const unsigned long long mine = ((unsigned long long)(kPendBit | 1u) << 32) | kw;
       const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
       h = 4ull * region_bucket(p, len, kw);
       while (true) {
@@ -130,7 +140,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
         }
         if (++h == hi) h = lo;
       }
-      const uint32_t rank = atomicAdd(&L.table[h].q, 1u) & ~kPendBit;
+      const uint32_t rank = won ? 0u : (atomicAdd(&L.table[h].q, 1u) & ~kPendBit);
       tmp_slot[pos] = (uint32_t)h;
       tmp_rank[pos] = rank;
     }
@@ -222,10 +232,18 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int 
   }
 }
 
+__device__ void force_unique_body(const DevTrie* __restrict__ tries, int trie, int lev, const ForceRange& R,
+                                  const uint32_t* __restrict__ tmp_slot);
+
+// Scatter the clustered columns to their child ranges (repeated keys met), or
+// the identity grouping (k_force_unique's body) when every key was distinct.
 __global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
                                 const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank,
                                 const DevCounters* __restrict__ ctr) {
-  if (!ctr->dup) return;
+  if (!ctr->dup) {
+    force_unique_body(tries, trie, lev, R, tmp_slot);
+    return;
+  }
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[lev];
   const uint32_t total = force_total(R);
@@ -245,9 +263,8 @@ __global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int
 // own child group, so the grouping is the identity -- child start = the row's
 // position, count 1, clustered columns copied in place. Replaces assign +
 // scatter (a graph level of deduplicated edges always takes this path).
-__global__ void k_force_unique(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
-                               const uint32_t* __restrict__ tmp_slot, const DevCounters* __restrict__ ctr) {
-  if (ctr->dup) return;
+__device__ void force_unique_body(const DevTrie* __restrict__ tries, int trie, int lev, const ForceRange& R,
+                                  const uint32_t* __restrict__ tmp_slot) {
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[lev];
   const uint32_t total = force_total(R);
@@ -267,8 +284,10 @@ __global__ void k_force_unique(const DevTrie* __restrict__ tries, int trie, int 
   }
 }
 
-__global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R) {
+__global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+                                 DevCounters* ctr) {
   const DevLevel& L = tries[trie].lev[lev];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->keys_inserted += ctr->newslots;
   if (R.single) {
     if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
     return;
@@ -344,6 +363,7 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
     L.nkeys[0] = G;
     L.state[0] = 2u;
     ctr->newslots = G;
+    ctr->keys_inserted += G;
   }
 }
 
