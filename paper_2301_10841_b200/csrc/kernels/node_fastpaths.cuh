@@ -367,90 +367,121 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_
 
 // GJ-shaped frontier-writing node: every subatom is a one-variable cover of the
 // new variable x; atoms whose subatom is not their last continue with the
-// child of their cover (keys mode) or probe (q, cnt[q]). Survivors are
-// block-compacted into the next frontier.
+// child of their cover (keys mode) or probe (q, cnt[q]). Each thread takes
+// RW candidates per tile (rounds of 32-candidate warp chunks), and the
+// survivors of all rounds are block-compacted at once (one barrier pair and
+// one global atomic per RW*TILE candidates).
+#ifndef FJG_WRITE_RW
+#define FJG_WRITE_RW 4
+#endif
+template <int NS>
+__device__ __forceinline__ bool gj_write_cand(const KNode& N, uint64_t c0, uint64_t i,
+                                              const uint32_t* __restrict__ owner, uint32_t& e_out, int32_t& x,
+                                              uint64_t& mult, uint32_t (&chp)[NS], uint32_t (&chl)[NS],
+                                              uint32_t& probes, uint32_t& misses, uint32_t& body) {
+  const uint64_t* __restrict__ scan = N.scan;
+  const uint64_t t = (i - c0) / 32;  // this warp's 32-candidate chunk
+  const uint64_t e = upper_bound_u64(scan, __ldg(owner + t), __ldg(owner + t + 1), i);
+  e_out = (uint32_t)e;
+  const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+  const int ci = N.chosen[e];
+  uint32_t sp[NS], sl[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const KSub& P = N.sub[s];
+    if (P.in_p) {
+      sp[s] = __ldg(P.in_p + e);
+      sl[s] = __ldg(P.in_len + e);
+    } else {
+      sp[s] = 0;
+      sl[s] = *P.rregion;  // root: its probe region
+    }
+  }
+  mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+  bool alive = true;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (s == ci) {
+      const KSub& S = N.sub[s];
+      const uint32_t pos = sp[s] + (uint32_t)j;
+      if (!S.stream) {  // forced map: distinct keys are the child starts
+        const uint32_t c = __ldg(S.cnt + pos);
+        if (c == 0) alive = false;
+        chp[s] = pos;
+        chl[s] = c;
+      } else {
+        chp[s] = kSingleton;
+        chl[s] = 1;
+      }
+      x = alive ? __ldg(S.src[0] + pos) : 0;
+    }
+  if (!alive) return false;
+  ++body;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (s == ci) continue;
+    const KSub& P = N.sub[s];
+    ++probes;
+    const uint32_t kw = (uint32_t)x;
+    uint64_t b = region_bucket(sp[s], sl[s], kw);
+    const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+    bool more;
+    uint32_t q = bucket_match(ld_bucket(P.table, b), kw, more);
+    while (more) {
+      if (++b == bhi) b = blo;
+      q = bucket_match(ld_bucket(P.table, b), kw, more);
+    }
+    if (q == kEmpty) {
+      ++misses;
+      return false;
+    }
+    const uint32_t ql = __ldg(P.cnt + q);
+    if (P.last)
+      mult *= ql;
+    else {
+      chp[s] = q;
+      chl[s] = ql;
+    }
+  }
+  return true;
+}
+
 template <int NS, int W>
 __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
                                                    uint64_t F, const uint32_t* __restrict__ owner, int xvar,
                                                    DevCounters* ctr) {
+  constexpr int RW = FJG_WRITE_RW;
   __shared__ uint32_t s_warp[TILE / 32];
   __shared__ uint32_t s_base;
-  uint64_t probes = 0, misses = 0, body = 0;
+  uint32_t probes = 0, misses = 0, body = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t* __restrict__ scan = N.scan;
-  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE; base < c1; base += (uint64_t)gridDim.x * TILE) {
-    const uint64_t i = base + threadIdx.x;
-    bool alive = i < c1;
-    uint64_t e = 0, mult = 1;
-    int32_t x = 0;
-    uint32_t chp[NS], chl[NS];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * RW; base < c1; base += (uint64_t)gridDim.x * TILE * RW) {
+    bool alive[RW];
+    uint32_t e[RW];
+    int32_t x[RW];
+    uint64_t mult[RW];
+    uint32_t chp[RW][NS], chl[RW][NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) chp[s] = chl[s] = 0;
-    if (alive) {
-      const uint64_t t = (i - c0) / 32;  // this warp's 32-candidate chunk
-      e = upper_bound_u64(scan, __ldg(owner + t), __ldg(owner + t + 1), i);
-      const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
-      const int ci = N.chosen[e];
-      uint32_t sp[NS], sl[NS];
+    for (int r = 0; r < RW; ++r) {
+      // round r: warp w takes the 32-candidate chunk base + (r * TILE/32 + w) * 32
+      const uint64_t i = base + (uint64_t)r * TILE + threadIdx.x;
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const KSub& P = N.sub[s];
-        if (P.in_p) {
-          sp[s] = __ldg(P.in_p + e);
-          sl[s] = __ldg(P.in_len + e);
-        } else {
-          sp[s] = 0;
-          sl[s] = *P.rregion;  // root: its probe region
-        }
-      }
-      if (N.in_mult) mult = __ldg(N.in_mult + e);
-#pragma unroll
-      for (int s = 0; s < NS; ++s)
-        if (s == ci) {
-          const KSub& S = N.sub[s];
-          const uint32_t pos = sp[s] + (uint32_t)j;
-          if (!S.stream) {  // forced map: distinct keys are the child starts
-            const uint32_t c = __ldg(S.cnt + pos);
-            if (c == 0) alive = false;
-            chp[s] = pos;
-            chl[s] = c;
-          } else {
-            chp[s] = kSingleton;
-            chl[s] = 1;
-          }
-          if (alive) x = __ldg(S.src[0] + pos);
-        }
-      if (alive) ++body;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s == ci || !alive) continue;
-        const KSub& P = N.sub[s];
-        ++probes;
-        const uint32_t kw = (uint32_t)x;
-        uint64_t b = region_bucket(sp[s], sl[s], kw);
-        const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
-        bool more;
-        uint32_t q = bucket_match(ld_bucket(P.table, b), kw, more);
-        while (more) {
-          if (++b == bhi) b = blo;
-          q = bucket_match(ld_bucket(P.table, b), kw, more);
-        }
-        if (q == kEmpty) {
-          ++misses;
-          alive = false;
-        } else {
-          const uint32_t ql = __ldg(P.cnt + q);
-          if (P.last)
-            mult *= ql;
-          else {
-            chp[s] = q;
-            chl[s] = ql;
-          }
-        }
-      }
+      for (int s = 0; s < NS; ++s) chp[r][s] = chl[r][s] = 0;
+      e[r] = 0;
+      x[r] = 0;
+      mult[r] = 1;
+      alive[r] = i < c1 && gj_write_cand<NS>(N, c0, i, owner, e[r], x[r], mult[r], chp[r], chl[r], probes, misses,
+                                             body);
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, alive);
-    if (lane == 0) s_warp[warp] = __popc(bal);
+    unsigned bal[RW];
+    uint32_t wtot = 0;
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      bal[r] = __ballot_sync(0xffffffffu, alive[r]);
+      wtot += __popc(bal[r]);
+    }
+    if (lane == 0) s_warp[warp] = wtot;
     __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t tot = 0;
@@ -462,44 +493,47 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
       s_base = tot ? atomicAdd(&ctr->survivors, tot) : 0u;
     }
     __syncthreads();
-    if (alive) {
-      const uint32_t o = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1));
+    uint32_t o = s_base + s_warp[warp];
 #pragma unroll
-      for (int v = 0; v < W; ++v)
-        if ((N.out_vars >> v) & 1u) N.out_var[v][o] = (v == xvar) ? x : __ldg(N.in_var[v] + e);
+    for (int r = 0; r < RW; ++r) {
+      if (alive[r]) {
+        const uint32_t at = o + __popc(bal[r] & lt_mask);
 #pragma unroll
-      for (int a = 0; a < W; ++a)
-        if ((N.out_atoms >> a) & 1u) {
-          uint32_t pa = 0, la = 0;
-          bool here = false;
+        for (int v = 0; v < W; ++v)
+          if ((N.out_vars >> v) & 1u) N.out_var[v][at] = (v == xvar) ? x[r] : __ldg(N.in_var[v] + e[r]);
 #pragma unroll
-          for (int s = 0; s < NS; ++s)
-            if (N.sub[s].atom == a) {
-              pa = chp[s];
-              la = chl[s];
-              here = true;
+        for (int a = 0; a < W; ++a)
+          if ((N.out_atoms >> a) & 1u) {
+            uint32_t pa = 0, la = 0;
+            bool here = false;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (N.sub[s].atom == a) {
+                pa = chp[r][s];
+                la = chl[r][s];
+                here = true;
+              }
+            if (!here) {
+              pa = __ldg(N.in_p[a] + e[r]);
+              la = __ldg(N.in_len[a] + e[r]);
             }
-          if (!here) {
-            pa = __ldg(N.in_p[a] + e);
-            la = __ldg(N.in_len[a] + e);
+            N.out_p[a][at] = pa;
+            N.out_len[a][at] = la;
           }
-          N.out_p[a][o] = pa;
-          N.out_len[a][o] = la;
-        }
-      if (N.out_mult) N.out_mult[o] = mult;
+        if (N.out_mult) N.out_mult[at] = mult[r];
+      }
+      o += __popc(bal[r]);
     }
     __syncthreads();
   }
-  probes = warp_sum(probes);
-  misses = warp_sum(misses);
-  body = warp_sum(body);
+  const uint64_t tp = warp_sum((uint64_t)probes), tm = warp_sum((uint64_t)misses), tb = warp_sum((uint64_t)body);
   if (lane == 0) {
-    if (probes) {
-      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
-      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    if (tp) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)tp);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)tp);
     }
-    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
-    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (tm) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)tm);
+    if (tb) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)tb);
   }
 }
 
