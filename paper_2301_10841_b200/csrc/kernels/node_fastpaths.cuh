@@ -130,6 +130,9 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
 #ifndef FJG_GJ_BF_MINB
 #define FJG_GJ_BF_MINB 4
 #endif
+#ifndef FJG_GJ_BF_MINB3
+#define FJG_GJ_BF_MINB3 4  // 4 resident blocks (64 registers): C4 last node 107.7 -> 98.4 ms
+#endif
 // One 32-byte bucket (4 slots) in a single 256-bit load (LDG.E.ENL2.256).
 struct Bucket8 {
   uint32_t k0, q0, k1, q1, k2, q2, k3, q3;
@@ -176,7 +179,7 @@ struct HitQueue {  // per-warp ring buffers
 // priority select; survivors are folded from a per-warp queue (leaf
 // multiplicities, head-prefix hash, checksum, MIN) with every lane busy.
 template <int NS, int R, int W>
-__global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : 3) k_last_gj_bf(const __grid_constant__ KNode N, uint64_t c0,
+__global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MINB3) k_last_gj_bf(const __grid_constant__ KNode N, uint64_t c0,
                                                                      uint64_t c1, uint64_t F,
                                                                      const uint32_t* __restrict__ owner,
                                                                      int min_var, DevCounters* ctr) {
