@@ -426,3 +426,27 @@ def test_bucket_collisions_and_extreme_keys(engine):
         assert bag_equal(rows, ref["tuples"])
         qq.close()
     assert ref["count"] > 0
+
+
+@pytest.mark.parametrize("ndims", [1, 2, 3, 4])
+def test_stream_one_and_cartesian_tail(engine, ndims):
+    """Factored star plans: node 0 streams the fact table and probes every
+    dimension (k_stream_one: stage queues, NP = ndims); the per-dimension
+    suffix nodes form a Cartesian tail (k_tail) whose products exceed 8 rows
+    per binding (warp-strided expansion). Count, checksum, MIN and the
+    enumerated bag match the oracle for batch sizes that split node 0."""
+    rng = np.random.default_rng(900 + ndims)
+    nf = 3000
+    q = [{"rel": "F", "vars": ["r"] + [f"f{i + 1}" for i in range(ndims)]}]
+    cols = [[np.arange(nf, dtype=np.int32)] + [rng.integers(0, 40, nf).astype(np.int32) for _ in range(ndims)]]
+    for i in range(ndims):
+        keys = rng.integers(0, 60, 90).astype(np.int32)      # duplicate keys: tails of several rows
+        if i == 0:
+            keys = np.concatenate([keys, np.full(12, 7, np.int32)])  # one key with > 8 rows
+        q.append({"rel": f"D{i + 1}", "vars": [f"f{i + 1}", f"x{i + 1}"]})
+        cols.append([keys, rng.integers(-5, 5, len(keys)).astype(np.int32)])
+    plan = P.compile_plan({"query": q, "binary_plan": configs.left_deep([a["rel"] for a in q])}, "free")
+    assert len(plan) == ndims + 1 and all(len(node) == 1 for node in plan[1:])
+    for batch in (0, 1000, 777):
+        check(engine, q, plan, cols, min_var=0, batch_size=batch)
+    check(engine, q, plan, cols, enumerate=True, batch_size=777)
