@@ -104,6 +104,7 @@ typedef struct {
   double last_node_ms;        /* device time of the fused last-node kernel (if collect_timing) */
   uint64_t last_node_launches;
   uint64_t last_node_candidates; /* cover candidates expanded by the last node */
+  double first_node_ms;       /* device time of node 0's kernels when node 0 is not the last (if collect_timing) */
   uint32_t kernel_launches;   /* kernels this library launched for the call */
   uint32_t host_syncs;
 } fjg_result;

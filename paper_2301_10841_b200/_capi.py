@@ -56,6 +56,7 @@ class Result(C.Structure):
                 ("keys_inserted", C.c_uint64), ("forces", C.c_uint64), ("rows_forced", C.c_uint64),
                 ("build_ms", C.c_double), ("join_ms", C.c_double), ("last_node_ms", C.c_double),
                 ("last_node_launches", C.c_uint64), ("last_node_candidates", C.c_uint64),
+                ("first_node_ms", C.c_double),
                 ("kernel_launches", C.c_uint32),
                 ("host_syncs", C.c_uint32)]
 

@@ -278,8 +278,8 @@ struct fjg_query {
   std::vector<cudaEvent_t> events;
   std::vector<std::pair<int, int>> marks;  // (event index, phase) ; phase<0 = start
   size_t ev_used = 0;
-  double phase_ms[3] = {0, 0, 0};          // 0 force (build), 1 node kernels, 2 last node
-  double build_ms = 0, join_ms = 0, last_ms = 0;
+  double phase_ms[4] = {0, 0, 0, 0};       // 0 force (build), 1 node kernels, 2 last node, 3 node 0 (not last)
+  double build_ms = 0, join_ms = 0, last_ms = 0, first_ms = 0;
   uint64_t last_launches = 0, last_candidates = 0;
   uint64_t node_inputs[MAXN] = {0};
   bool timing = false;
@@ -1146,7 +1146,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       LAUNCH(eng, launch_expand<EXPAND_WRITE>(q->width, gw, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
                                               q->d_ctr));
     }
-    q->mark(eng->stream, 1);
+    q->mark(eng->stream, k == 0 ? 3 : 1);
     sync_counters(q);
     run_node(q, k + 1, q->h_ctr->survivors, mode);
   }
@@ -1173,7 +1173,7 @@ static void reset_query(fjg_query* q) {
   CK(cudaMemcpyAsync(q->d_ctr, q->h_ctr, sizeof(z), cudaMemcpyHostToDevice, eng->stream));
   q->maps_built = q->forces = q->rows_forced = 0;
   q->build_ms = q->join_ms = q->last_ms = 0;
-  q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = 0;
+  q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = q->phase_ms[3] = 0;
   q->last_launches = q->last_candidates = 0;
   for (int k = 0; k < MAXN; ++k) q->node_inputs[k] = 0;
   q->marks.clear();
@@ -1255,8 +1255,9 @@ static void execute_once(fjg_query* q, int mode) {
   sync_counters(q);
   q->resolve_marks();
   q->build_ms = q->phase_ms[0];
-  q->join_ms = q->phase_ms[1] + q->phase_ms[2];
+  q->join_ms = q->phase_ms[1] + q->phase_ms[2] + q->phase_ms[3];
   q->last_ms = q->phase_ms[2];
+  q->first_ms = q->phase_ms[3];
 }
 
 // ============================================================================
@@ -1588,6 +1589,7 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     r.last_node_ms = q->last_ms;
     r.last_node_launches = q->last_launches;
     r.last_node_candidates = q->last_candidates;
+    r.first_node_ms = q->first_ms;
     r.kernel_launches = eng->launches - l0;
     r.host_syncs = eng->syncs - s0;
     *out = r;

@@ -41,6 +41,7 @@ class ExecResult:
     last_node_ms: float
     last_node_launches: int
     last_node_candidates: int
+    first_node_ms: float
     kernel_launches: int
     host_syncs: int
     output_rows: int = 0
@@ -243,7 +244,7 @@ class Query:
                           maps_built=r.maps_built, keys_inserted=r.keys_inserted, forces=r.forces,
                           rows_forced=r.rows_forced, build_ms=r.build_ms, join_ms=r.join_ms,
                           last_node_ms=r.last_node_ms, last_node_launches=r.last_node_launches,
-                          last_node_candidates=r.last_node_candidates,
+                          last_node_candidates=r.last_node_candidates, first_node_ms=r.first_node_ms,
                           kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
 
     def enumerate(self, batch_size=0, dynamic_cover=True, min_var=None, backend="colt"):
