@@ -1002,21 +1002,28 @@ static void launch_stream_one(fjg_query* q, const KNode& KN, const SProbe& SP, u
 #ifndef FJG_TAIL
 #define FJG_TAIL 1
 #endif
-template <int MODE>
-static void launch_tail(fjg_query* q, int k, uint64_t F) {
+template <int MODE, int NT>
+static void launch_tail_nt(fjg_query* q, int k, uint64_t F) {
   fjg_engine* eng = q->eng;
   const KNode& KN = q->knodes[k];
   const TailPlan& T = q->tails[k];
   const unsigned g = grid_for(F, TILE, eng->num_sms * 8);
   if (q->width <= 4)
-    LAUNCH(eng, (k_tail<MODE, 4><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
-                                                              q->d_ctr)));
+    LAUNCH(eng, (k_tail<MODE, 4, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
+                                                                  q->d_ctr)));
   else if (q->width <= 8)
-    LAUNCH(eng, (k_tail<MODE, 8><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
-                                                              q->d_ctr)));
+    LAUNCH(eng, (k_tail<MODE, 8, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
+                                                                  q->d_ctr)));
   else
-    LAUNCH(eng, (k_tail<MODE, 16><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
-                                                               q->d_ctr)));
+    LAUNCH(eng, (k_tail<MODE, 16, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
+                                                                   q->d_ctr)));
+}
+template <int MODE>
+static void launch_tail(fjg_query* q, int k, uint64_t F) {
+  if (q->tails[k].ntail == 1)
+    launch_tail_nt<MODE, 1>(q, k, F);
+  else
+    launch_tail_nt<MODE, MAXTAIL>(q, k, F);
 }
 
 static void run_node(fjg_query* q, int k, uint64_t F, int mode) {

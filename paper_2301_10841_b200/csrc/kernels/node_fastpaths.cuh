@@ -986,20 +986,20 @@ __global__ void __launch_bounds__(TILE, 3) k_stream_one(const __grid_constant__ 
 // (lanes stride the product). Each output tuple = the binding's values plus one
 // row of every tail subtrie (mixed-radix index, last tail node fastest); counts,
 // checksum and MIN fold as in the last node, or tuples are written (ENUM).
-template <int MODE, int W>
+template <int MODE, int W, int NT>
 __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, uint64_t e, uint64_t start,
                                             uint32_t step, bool own, int min_var, int32_t* __restrict__ out_tuples,
                                             uint64_t out_cap, DevCounters* ctr, uint64_t& acc_lo, uint64_t& acc_hi,
-                                            uint64_t& acc_sum, long long& acc_min, uint64_t (&inputs)[MAXTAIL],
-                                            uint64_t (&body)[MAXTAIL]) {
+                                            uint64_t& acc_sum, long long& acc_min, uint64_t (&inputs)[NT],
+                                            uint64_t (&body)[NT]) {
   int32_t val[W];
 #pragma unroll
   for (int v = 0; v < W; ++v) val[v] = ((N.in_vars >> v) & 1u) ? __ldg(N.in_var[v] + e) : 0;
   const uint64_t mult = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
-  uint32_t tp[MAXTAIL], tl[MAXTAIL];
+  uint32_t tp[NT], tl[NT];
   uint64_t prod = 1;
 #pragma unroll
-  for (int j = 0; j < MAXTAIL; ++j) {
+  for (int j = 0; j < NT; ++j) {
     if (j >= T.ntail) continue;
     if (T.open[j]) {
       tp[j] = __ldg(T.in_p[j] + e);
@@ -1017,7 +1017,7 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
   for (uint64_t idx = start; idx < prod; idx += step) {
     uint64_t rest = idx;
 #pragma unroll
-    for (int j = MAXTAIL - 1; j >= 0; --j) {
+    for (int j = NT - 1; j >= 0; --j) {
       if (j >= T.ntail) continue;
       const uint32_t c = tp[j] == kSingleton ? 1u : tl[j];
       uint32_t off;
@@ -1055,15 +1055,15 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
   }
 }
 
-template <int MODE, int W>
+template <int MODE, int W, int NT>
 __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, const __grid_constant__ TailPlan T,
                                                uint64_t F, int min_var, int32_t* __restrict__ out_tuples,
                                                uint64_t out_cap, DevCounters* ctr) {
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0;
   long long acc_min = LLONG_MAX;
-  uint64_t inputs[MAXTAIL], body[MAXTAIL];
+  uint64_t inputs[NT], body[NT];
 #pragma unroll
-  for (int j = 0; j < MAXTAIL; ++j) inputs[j] = body[j] = 0;
+  for (int j = 0; j < NT; ++j) inputs[j] = body[j] = 0;
   const int lane = threadIdx.x & 31;
   for (uint64_t b = (uint64_t)blockIdx.x * TILE; b < F; b += (uint64_t)gridDim.x * TILE) {
     const uint64_t e = b + threadIdx.x;
@@ -1071,7 +1071,7 @@ __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, 
     if (e < F) {
       uint64_t prod = 1;
 #pragma unroll
-      for (int j = 0; j < MAXTAIL; ++j)
+      for (int j = 0; j < NT; ++j)
         if (j < T.ntail) {
           const uint32_t p = T.open[j] ? __ldg(T.in_p[j] + e) : 0u;
           const uint32_t l = T.open[j] ? __ldg(T.in_len[j] + e) : T.sub[j].root_n;
@@ -1079,16 +1079,16 @@ __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, 
         }
       big = prod > 8;
       // small products: this thread alone (and it counts the binding's inputs/body)
-      tail_expand<MODE, W>(N, T, e, big ? ~0ull : 0ull, 1u, true, min_var, out_tuples, out_cap, ctr, acc_lo,
+      tail_expand<MODE, W, NT>(N, T, e, big ? ~0ull : 0ull, 1u, true, min_var, out_tuples, out_cap, ctr, acc_lo,
                            acc_hi, acc_sum, acc_min, inputs, body);
     }
     unsigned bm = __ballot_sync(0xffffffffu, big);
-    uint64_t none[MAXTAIL], nb[MAXTAIL];
+    uint64_t none[NT], nb[NT];
     while (bm) {  // big products: the whole warp strides them
       const int src = __ffs(bm) - 1;
       bm &= bm - 1;
       const uint64_t eb = __shfl_sync(0xffffffffu, e, src);
-      tail_expand<MODE, W>(N, T, eb, lane, 32u, false, min_var, out_tuples, out_cap, ctr, acc_lo, acc_hi, acc_sum,
+      tail_expand<MODE, W, NT>(N, T, eb, lane, 32u, false, min_var, out_tuples, out_cap, ctr, acc_lo, acc_hi, acc_sum,
                            acc_min, none, nb);
     }
   }
@@ -1105,13 +1105,13 @@ __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
 #pragma unroll
-  for (int j = 0; j < MAXTAIL; ++j) {
+  for (int j = 0; j < NT; ++j) {
     inputs[j] = warp_sum(inputs[j]);
     body[j] = warp_sum(body[j]);
   }
   if (lane == 0) {
 #pragma unroll
-    for (int j = 0; j < MAXTAIL; ++j)
+    for (int j = 0; j < NT; ++j)
       if (j < T.ntail) {
         // node k's inputs are counted on the host (run_node)
         if (j > 0 && inputs[j]) atomicAdd((unsigned long long*)&ctr->tail_inputs[T.node[j]], (unsigned long long)inputs[j]);
