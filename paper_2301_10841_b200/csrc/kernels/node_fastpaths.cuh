@@ -377,16 +377,26 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
 #ifndef FJG_WRITE_RW
 #define FJG_WRITE_RW 4
 #endif
-template <int NS>
+template <int NS, bool ONE>
 __device__ __forceinline__ bool gj_write_cand(const KNode& N, uint64_t c0, uint64_t i,
                                               const uint32_t* __restrict__ owner, uint32_t& e_out, int32_t& x,
                                               uint64_t& mult, uint32_t (&chp)[NS], uint32_t (&chl)[NS],
                                               uint32_t& probes, uint32_t& misses, uint32_t& body) {
   const uint64_t* __restrict__ scan = N.scan;
-  const uint64_t t = (i - c0) / 32;  // this warp's 32-candidate chunk
-  const uint64_t e = upper_bound_u64(scan, __ldg(owner + t), __ldg(owner + t + 1), i);
+  uint64_t e = 0, j = i;  // ONE: a single binding (node 0), candidate = offset
+  if (!ONE) {
+    const uint64_t t = (i - c0) / 32;  // this warp's 32-candidate chunk
+    e = upper_bound_u64(scan, __ldg(owner + t), __ldg(owner + t + 1), i);
+    j = i - (e ? __ldg(scan + e - 1) : 0ull);
+  }
   e_out = (uint32_t)e;
-  const uint64_t j = i - (e ? __ldg(scan + e - 1) : 0ull);
+  if (ONE) {  // keys iteration over a forced map: most offsets are not child starts
+    const int ci = N.chosen[0];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == ci && !N.sub[s].stream && __ldg(N.sub[s].cnt + (N.sub[s].in_p ? __ldg(N.sub[s].in_p) : 0u) + (uint32_t)j) == 0)
+        return false;
+  }
   const int ci = N.chosen[e];
   uint32_t sp[NS], sl[NS];
 #pragma unroll
@@ -449,10 +459,23 @@ __device__ __forceinline__ bool gj_write_cand(const KNode& N, uint64_t c0, uint6
   return true;
 }
 
+template <int NS, int W, bool ONE>
+__device__ __forceinline__ void write_gj_body(const KNode& N, uint64_t c0, uint64_t c1,
+                                              const uint32_t* __restrict__ owner, int xvar, DevCounters* ctr);
+
 template <int NS, int W>
 __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode N, uint64_t c0, uint64_t c1,
                                                    uint64_t F, const uint32_t* __restrict__ owner, int xvar,
                                                    DevCounters* ctr) {
+  if (F == 1)
+    write_gj_body<NS, W, true>(N, c0, c1, owner, xvar, ctr);
+  else
+    write_gj_body<NS, W, false>(N, c0, c1, owner, xvar, ctr);
+}
+
+template <int NS, int W, bool ONE>
+__device__ __forceinline__ void write_gj_body(const KNode& N, uint64_t c0, uint64_t c1,
+                                              const uint32_t* __restrict__ owner, int xvar, DevCounters* ctr) {
   constexpr int RW = FJG_WRITE_RW;
   __shared__ uint32_t s_warp[TILE / 32];
   __shared__ uint32_t s_base;
@@ -474,7 +497,7 @@ __global__ void __launch_bounds__(TILE) k_write_gj(const __grid_constant__ KNode
       e[r] = 0;
       x[r] = 0;
       mult[r] = 1;
-      alive[r] = i < c1 && gj_write_cand<NS>(N, c0, i, owner, e[r], x[r], mult[r], chp[r], chl[r], probes, misses,
+      alive[r] = i < c1 && gj_write_cand<NS, ONE>(N, c0, i, owner, e[r], x[r], mult[r], chp[r], chl[r], probes, misses,
                                              body);
     }
     unsigned bal[RW];
