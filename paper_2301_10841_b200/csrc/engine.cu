@@ -1026,6 +1026,44 @@ static void launch_tail(fjg_query* q, int k, uint64_t F) {
     launch_tail_nt<MODE, MAXTAIL>(q, k, F);
 }
 
+__global__ void k_set_root_node(uint8_t* chosen, uint64_t* m, uint64_t* scan, int best, uint64_t mv) {
+  chosen[0] = (uint8_t)best;
+  m[0] = mv;
+  scan[0] = mv;
+}
+
+// k_select for the single empty binding entering node 0 when none of its
+// tries' roots is forced yet (every COLT execution): each subatom is a root
+// BaseScan, estimated_key_count = its cardinality, so the
+// host picks the cover (min estimate, ties to the lowest position,
+// SPEC.md:441) and the claims (every subatom but a stream-iterated cover)
+// exactly as the kernel would, with no device round trip.
+static bool host_select_root_node(fjg_query* q, int k, uint64_t F) {
+  if (k != 0 || F != 1) return false;
+  const DevNode& N = q->nodes[k];
+  for (int s = 0; s < N.nsub; ++s)
+    if (N.sub[s].depth != 0 || ((N.in_atoms >> N.sub[s].atom) & 1u) || q->tries[N.sub[s].trie].root_forced)
+      return false;
+  int best = N.cov[0];
+  uint64_t best_est = N.atom_n[N.sub[best].atom];
+  if (q->dynamic)
+    for (int ci = 1; ci < N.ncov; ++ci) {
+      const int s = N.cov[ci];
+      const uint64_t est = N.atom_n[N.sub[s].atom];
+      if (est < best_est) {
+        best_est = est;
+        best = s;
+      }
+    }
+  const uint64_t m = N.atom_n[N.sub[best].atom];
+  DevCounters& H = *q->h_ctr;
+  H.total_m = m;
+  for (int s = 0; s < N.nsub; ++s)
+    if (s != best || !N.sub[s].stream) H.root_need[N.sub[s].trie] = 1;
+  LAUNCH(q->eng, k_set_root_node<<<1, 1, 0, q->eng->stream>>>(N.chosen, N.m, N.scan, best, m));
+  return true;
+}
+
 static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (F == 0) return;
   q->node_inputs[k] += F;
@@ -1046,6 +1084,9 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   const bool memo_top = mode == EXPAND_MEMO && k == q->stop_node;
   const KNode& KN = memo_top ? q->memo_top : q->knodes[k];
   const bool is_last = N.is_last || memo_top;
+  if (!memo_top && host_select_root_node(q, k, F)) {
+    // node 0 of a fresh COLT execution: its cover choice and claims need no device round trip
+  } else {
   LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(KN, q->d_tries, F,
                                                                                     q->dynamic ? 1 : 0, q->d_ctr));
   if (F <= kSmallScan) {
@@ -1058,6 +1099,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
                        cudaMemcpyDeviceToDevice, eng->stream));
   }
   sync_counters(q);
+  }
   const uint64_t M = q->h_ctr->total_m;
   force_claims(q, k);
   if (M == 0) return;
