@@ -1201,25 +1201,61 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   }
 }
 
+// One launch resets an execution: the device counters (minv = +inf, root
+// probe regions = row counts) and the subtrie states of every level the last
+// execution forced (slot regions and child counts are cleared by the force
+// that claims them).
+struct ResetPlan {
+  int nz, ntries;
+  uint32_t* ptr[MAXT * MAXL];
+  uint32_t n[MAXT * MAXL];
+  uint32_t root_region[MAXT];
+};
+__global__ void k_reset(const __grid_constant__ ResetPlan P, DevCounters* ctr) {
+  if (blockIdx.y == 0) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(ctr);
+    constexpr uint32_t kMin = offsetof(DevCounters, minv) / 4, kReg = offsetof(DevCounters, root_region) / 4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < sizeof(DevCounters) / 4; i += gridDim.x * blockDim.x) {
+      uint32_t v = 0;
+      if (i == kMin) v = 0xFFFFFFFFu;      // minv = LLONG_MAX (little endian: low word all ones,
+      if (i == kMin + 1) v = 0x7FFFFFFFu;  // high word 0x7fffffff)
+      if (i >= kReg && i < kReg + (uint32_t)P.ntries) v = P.root_region[i - kReg];
+      w[i] = v;
+    }
+    return;
+  }
+  const int z = blockIdx.y - 1;
+  uint32_t* p = P.ptr[z];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n[z]; i += gridDim.x * blockDim.x) p[i] = 0;
+}
+
 static void reset_query(fjg_query* q) {
   fjg_engine* eng = q->eng;
+  ResetPlan P;
+  memset(&P, 0, sizeof(P));
+  uint32_t maxn = 1;
   for (auto& T : q->tries) {
     for (size_t l = 0; l < T.lev.size(); ++l) {
       auto& H = T.lev[l];
       DevLevel& L = T.dev.lev[l];
-      if (H.dirty) {  // slot regions and child counts are cleared by the force that claims them
-        CK(cudaMemsetAsync(L.state, 0, H.nsub * 4, eng->stream));
+      if (H.dirty) {
+        P.ptr[P.nz] = L.state;
+        P.n[P.nz] = (uint32_t)H.nsub;
+        maxn = std::max<uint32_t>(maxn, (uint32_t)H.nsub);
+        ++P.nz;
         H.dirty = false;
       }
     }
     T.root_forced = false;
   }
-  DevCounters z;
+  P.ntries = (int)q->tries.size();
+  for (size_t t = 0; t < q->tries.size(); ++t) P.root_region[t] = (uint32_t)std::max<uint64_t>(q->tries[t].rel->nrows, 1);
+  const dim3 grid(std::min<uint32_t>((maxn + 255) / 256, (uint32_t)eng->num_sms * 4), 1 + P.nz);
+  LAUNCH(eng, k_reset<<<grid, 256, 0, eng->stream>>>(P, q->d_ctr));
+  DevCounters& z = *q->h_ctr;
   memset(&z, 0, sizeof(z));
   z.minv = LLONG_MAX;
-  for (size_t t = 0; t < q->tries.size(); ++t) z.root_region[t] = (uint32_t)std::max<uint64_t>(q->tries[t].rel->nrows, 1);
-  memcpy(q->h_ctr, &z, sizeof(z));
-  CK(cudaMemcpyAsync(q->d_ctr, q->h_ctr, sizeof(z), cudaMemcpyHostToDevice, eng->stream));
+  for (size_t t = 0; t < q->tries.size(); ++t) z.root_region[t] = P.root_region[t];
   q->maps_built = q->forces = q->rows_forced = 0;
   q->build_ms = q->join_ms = q->last_ms = 0;
   q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = q->phase_ms[3] = 0;
