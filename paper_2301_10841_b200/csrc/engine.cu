@@ -859,7 +859,8 @@ static void chunk_owners(fjg_query* q, const uint64_t* scan, uint64_t F, uint64_
   fjg_engine* eng = q->eng;
   const uint64_t n = (c1 - c0 + chunk - 1) / chunk + 1;
   CK(cudaMemsetAsync(q->chunk_owner, 0, n * 4, eng->stream));
-  LAUNCH(eng, k_chunk_marks<<<grid_for(F), 256, 0, eng->stream>>>(scan, F, c0, c1, chunk, q->chunk_owner));
+  LAUNCH(eng, k_chunk_marks<<<grid_for(std::min<uint64_t>(F, (c1 - c0 + chunk - 1) / chunk + 1)), 256, 0,
+                              eng->stream>>>(scan, F, c0, c1, chunk, q->chunk_owner));
   size_t bytes = q->cub_tmp_bytes;
   CK(cub::DeviceScan::InclusiveScan(q->cub_tmp, bytes, q->chunk_owner, q->chunk_owner, MaxOp(), (int64_t)n,
                                     eng->stream));

@@ -25,7 +25,7 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__
 // [bounds[t], bounds[t+1]] instead of the whole scan.
 constexpr int TILE = 256;
 #ifndef FJG_LAST_CHUNK_LOG
-#define FJG_LAST_CHUNK_LOG 28
+#define FJG_LAST_CHUNK_LOG 27  // measured: 2^30 > 2^28 > 2^27 ~ 2^26 (C2 last node 3.49 > 3.42 > 3.31 ms)
 #endif
 constexpr uint64_t kLastChunk = 1ull << FJG_LAST_CHUNK_LOG;  // last-node candidates per launch
 __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1,
@@ -45,7 +45,10 @@ __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uin
 __global__ void k_chunk_marks(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk,
                               uint32_t* __restrict__ owner) {
   const uint64_t nch = (c1 - c0 + chunk - 1) / chunk;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < F; e += (uint64_t)gridDim.x * blockDim.x) {
+  // only the bindings whose candidates overlap [c0, c1): a contiguous range of the frontier
+  const uint64_t elo = upper_bound_u64(scan, 0, F - 1, c0), ehi = upper_bound_u64(scan, 0, F - 1, c1 - 1);
+  for (uint64_t e = elo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= ehi;
+       e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull, se = __ldg(scan + e);
     const uint64_t lo = max(prev, c0), hi = min(se, c1);
     if (lo >= hi) continue;
