@@ -1111,8 +1111,11 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
       const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
                            FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
-      if (gj_fast)
+      if (gj_fast) {
         chunk_owners(q, N.scan, F, c0, c1, 32 * FJG_GJ_R);
+        if (FJG_GJ_TICKET)
+          CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, ticket), 0, 8, eng->stream));
+      }
       else
         LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);

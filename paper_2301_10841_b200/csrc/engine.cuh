@@ -194,6 +194,7 @@ struct DevCounters {
   uint32_t root_region[MAXT];  // buckets of each trie's root slot region (rows, or distinct keys once sorted)
   uint32_t level_dup[MAXT * MAXL];  // some force of (trie, level) met a repeated key: child counts can exceed 1
   uint64_t tail_inputs[MAXN];  // node inputs counted on the device (fused Cartesian tail nodes)
+  unsigned long long ticket;   // last-node chunk tickets (FJG_GJ_TICKET)
 };
 
 // Fused Cartesian tail (nodes k..K-1 each one stream-iterated subatom binding

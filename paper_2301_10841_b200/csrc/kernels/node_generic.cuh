@@ -25,7 +25,7 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__
 // [bounds[t], bounds[t+1]] instead of the whole scan.
 constexpr int TILE = 256;
 #ifndef FJG_LAST_CHUNK_LOG
-#define FJG_LAST_CHUNK_LOG 27  // measured: 2^30 > 2^28 > 2^27 ~ 2^26 (C2 last node 3.49 > 3.42 > 3.31 ms)
+#define FJG_LAST_CHUNK_LOG 31  // with ticketed chunks one launch is best (C2 last node 3.20 ms at 2^27, 3.03 at 2^31)
 #endif
 constexpr uint64_t kLastChunk = 1ull << FJG_LAST_CHUNK_LOG;  // last-node candidates per launch
 __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1,
