@@ -1171,8 +1171,11 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
     const bool gj_write = q->gj_w[k] >= 0 && FJG_GJ_WRITE;
     const bool one = F == 1 && q->sprobe[k].np > 0 && FJG_STREAM_ONE;
-    if (gj_write)
+    if (gj_write) {
       chunk_owners(q, N.scan, F, c0, c1, 32);
+      if (FJG_WRITE_TICKET)
+        CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, ticket), 0, 8, eng->stream));
+    }
     else if (!one)
       LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
     const unsigned gw = grid_for(c1 - c0, TILE, eng->num_sms * 8);

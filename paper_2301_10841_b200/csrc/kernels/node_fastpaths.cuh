@@ -398,6 +398,9 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
 #ifndef FJG_WRITE_RW
 #define FJG_WRITE_RW 4
 #endif
+#ifndef FJG_WRITE_TICKET
+#define FJG_WRITE_TICKET 1  // C4 frontier node -2 ms
+#endif
 template <int NS, bool ONE>
 __device__ __forceinline__ bool gj_write_cand(const KNode& N, uint64_t c0, uint64_t i,
                                               const uint32_t* __restrict__ owner, uint32_t& e_out, int32_t& x,
@@ -503,7 +506,15 @@ __device__ __forceinline__ void write_gj_body(const KNode& N, uint64_t c0, uint6
   uint32_t probes = 0, misses = 0, body = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
+#if FJG_WRITE_TICKET
+  // blocks take their next tile from a device counter (one front, see k_last_gj_bf)
+  __shared__ uint64_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket, 1ull);
+  __syncthreads();
+  for (uint64_t base = c0 + s_tile * TILE * RW; base < c1;) {
+#else
   for (uint64_t base = c0 + (uint64_t)blockIdx.x * TILE * RW; base < c1; base += (uint64_t)gridDim.x * TILE * RW) {
+#endif
     bool alive[RW];
     uint32_t e[RW];
     int32_t x[RW];
@@ -571,7 +582,13 @@ __device__ __forceinline__ void write_gj_body(const KNode& N, uint64_t c0, uint6
       }
       o += __popc(bal[r]);
     }
+#if FJG_WRITE_TICKET
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket, 1ull);
     __syncthreads();
+    base = c0 + s_tile * TILE * RW;
+#else
+    __syncthreads();
+#endif
   }
   const uint64_t tp = warp_sum((uint64_t)probes), tm = warp_sum((uint64_t)misses), tb = warp_sum((uint64_t)body);
   if (lane == 0) {
