@@ -911,17 +911,17 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->d_ctr));
   if (T.lev[l].multi)
     LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
-                                                                  q->newslots, q->newslot_p, q->d_ctr));
-  else
-    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
-                                                                   q->newslots, q->newslot_p, q->d_ctr));
-  const unsigned ga = grid_for(upper, 256, eng->num_sms * 8);
-  if (single)
-    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, p0, q->newslots, q->newslot_p,
                                                                   q->d_ctr));
   else
-    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, q->newslots,
-                                                                   q->newslot_p, q->d_ctr));
+    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
+                                                                   q->d_ctr));
+  const unsigned ga = grid_for(upper, 256, eng->num_sms * 8);
+  if (single)
+    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, p0, R, q->tmp_slot, q->tmp_rank,
+                                                                  q->d_ctr));
+  else
+    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, R, q->tmp_slot,
+                                                                   q->tmp_rank, q->d_ctr));
   LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank, q->d_ctr));
   // keys inserted accumulate on the device
   LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R,

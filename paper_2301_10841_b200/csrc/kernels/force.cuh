@@ -77,7 +77,6 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int l
 template <bool MULTI>
 __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
                                uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
-                               uint32_t* __restrict__ newslots, uint32_t* __restrict__ newslot_p,
                                DevCounters* ctr) {
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[lev];
@@ -86,10 +85,9 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
   const int32_t* src[MAXK];
 #pragma unroll
   for (int t = 0; t < MAXK; ++t) src[t] = t < nk ? level_src(T, lev, L.keycol[t]) : nullptr;
-  __shared__ uint32_t s_cnt, s_base;
-  const int lane = threadIdx.x & 31;
   bool sawdup = false;  // a repeated key: flagged once per block at the end (one hot address)
-  // block-uniform trip count: the new-slot append is aggregated per block
+  uint32_t wins = 0;     // slots this thread claimed (new keys), summed once per block at the end
+  // block-uniform trip count (the end-of-kernel block reduction needs every thread)
   for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < total; b0 += gridDim.x * blockDim.x) {
     const uint32_t i = b0 + threadIdx.x;
     bool won = false;
@@ -144,22 +142,14 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
       tmp_slot[pos] = (uint32_t)h;
       tmp_rank[pos] = rank;
     }
-    // append the new slots: one global atomic per block iteration
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    const unsigned wmask = __ballot_sync(0xffffffffu, won);
-    uint32_t wbase = 0;
-    if (lane == 0 && wmask) wbase = atomicAdd(&s_cnt, (uint32_t)__popc(wmask));
-    wbase = __shfl_sync(0xffffffffu, wbase, 0);
-    __syncthreads();
-    if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(&ctr->newslots, s_cnt) : 0u;
-    __syncthreads();
-    if (won) {
-      const uint32_t o = s_base + wbase + __popc(wmask & ((1u << lane) - 1));
-      newslots[o] = (uint32_t)h;
-      newslot_p[o] = p;
-    }
+    wins += won ? 1u : 0u;
   }
+  // new keys and the repeated-key flag: one atomic per block (k_force_assign
+  // finds the new slots as the rank-0 offsets, so no slot list is appended)
+  typedef cub::BlockReduce<uint32_t, 256> BR;
+  __shared__ typename BR::TempStorage rtmp;
+  const uint32_t bw = BR(rtmp).Sum(wins);
+  if (threadIdx.x == 0 && bw) atomicAdd(&ctr->newslots, bw);
   if (__syncthreads_or(sawdup) && threadIdx.x == 0) {
     ctr->dup = 1u;
     ctr->level_dup[trie * MAXL + lev] = 1u;
@@ -168,12 +158,12 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
 
 // Child-range allocation: q = p + (running sum of child sizes of p).
 template <bool SINGLE>
-__global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0,
-                               const uint32_t* __restrict__ newslots, const uint32_t* __restrict__ newslot_p,
+__global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0, ForceRange R,
+                               const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank,
                                DevCounters* ctr) {
   if (!ctr->dup) return;  // k_force_unique handles the all-distinct case
   const DevLevel& L = tries[trie].lev[lev];
-  const uint32_t total = ctr->newslots;
+  const uint32_t total = force_total(R);
   typedef cub::BlockScan<uint32_t, 256> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ uint32_t s_base;
@@ -181,24 +171,26 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int 
   const uint32_t iters = (total + stride - 1) / stride;
   for (uint32_t it = 0; it < iters; ++it) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
-    const bool ok = i < total;
+    // the new slots are the rank-0 offsets (the winner of each key's CAS)
+    bool ok = false;
     uint32_t h = 0, c = 0, p = 0;
-    if (ok) {
-      h = newslots[i];
-      p = newslot_p[i];
-      c = L.table[h].q & ~kPendBit;
+    if (i < total) {
+      uint32_t len, pos;
+      force_locate(R, i, p, len, pos);
+      if (tmp_rank[pos] == 0) {
+        ok = true;
+        h = tmp_slot[pos];
+        c = L.table[h].q & ~kPendBit;
+      }
     }
     uint32_t q = 0;
     if (SINGLE) {
       uint32_t excl, blk_total;
       BS(tmp).ExclusiveSum(c, excl, blk_total);
-      if (threadIdx.x == 0) {
-        const uint32_t first = blockIdx.x * blockDim.x + it * stride;
-        if (first < total) {
-          const uint32_t nb = min((uint32_t)blockDim.x, total - first);
-          s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);
-          atomicAdd(&L.nkeys[p0], nb);
-        }
+      const uint32_t nb = __syncthreads_count(ok);
+      if (threadIdx.x == 0 && nb) {
+        s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);
+        atomicAdd(&L.nkeys[p0], nb);
       }
       __syncthreads();
       q = s_base + excl;
