@@ -833,7 +833,20 @@ static void force_root_sorted(fjg_query* q, int t) {
   uint32_t* starts = q->owner_scratch;
   uint8_t* flags = q->sort_flags;
   uint32_t* ng = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, survivors));
-  LAUNCH(eng, k_root_keys<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, keys, rows));
+  // two columns, one key column, both clustered at level 0: sort (key, other
+  // column) straight into the clustered columns (stable: the row order the
+  // (key, row) sort + gather would give), no gather pass
+  const DevLevel& L0 = T.dev.lev[0];
+  int pay = -1;
+  if (T.dev.ncols == 2 && T.levels[0].size() == 1) {
+    const int kc = L0.keycol[0], oc = 1 - kc;
+    if (L0.cval[kc] && L0.cval[oc]) {
+      pay = oc;
+      skeys = reinterpret_cast<uint32_t*>(L0.cval[kc]);
+      srows = reinterpret_cast<uint32_t*>(L0.cval[oc]);
+    }
+  }
+  LAUNCH(eng, k_root_keys<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, keys, rows, pay));
   size_t bytes = q->cub_tmp_bytes;
   const int kb = T.levels[0].empty() ? 1 : 32;
   CK(cub::DeviceRadixSort::SortPairs(q->cub_tmp, bytes, keys, skeys, rows, srows, (int64_t)n, 0, kb, eng->stream));
@@ -846,7 +859,7 @@ static void force_root_sorted(fjg_query* q, int t) {
   // the root's slot region shrinks to one bucket per distinct key (load <= 0.25)
   LAUNCH(eng, k_root_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, ng, q->d_ctr));
   LAUNCH(eng, k_root_insert<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, skeys, starts, ng, q->d_ctr));
-  LAUNCH(eng, k_root_gather<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, srows));
+  if (pay < 0) LAUNCH(eng, k_root_gather<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, srows));
   q->mark(eng->stream, 0);
   q->forces += 1;
   q->maps_built += 1;

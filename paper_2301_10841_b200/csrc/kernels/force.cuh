@@ -295,14 +295,17 @@ __global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, in
 // key of arity <= 1: radix-sort (key, row), mark group starts, insert one slot
 // per distinct key (no contention), gather the clustered columns. Produces the
 // same structure as the atomic path without per-row atomics on hot keys.
+// pay: the sort payload is this column's values (two-column relations: the
+// sort then lays out both clustered columns, no gather), else the row ids
 __global__ void k_root_keys(const DevTrie* __restrict__ tries, int trie, uint32_t n, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ rows) {
+                            uint32_t* __restrict__ rows, int pay) {
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[0];
   const int32_t* kc = L.nk ? T.base[L.keycol[0]] : nullptr;
+  const int32_t* pc = pay >= 0 ? T.base[pay] : nullptr;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     keys[i] = kc ? (uint32_t)kc[i] : 0u;
-    rows[i] = i;
+    rows[i] = pc ? (uint32_t)pc[i] : i;
   }
 }
 
