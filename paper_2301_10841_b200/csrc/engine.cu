@@ -993,7 +993,7 @@ static void launch_stream_one_rw(fjg_query* q, const KNode& KN, const SProbe& SP
 }
 template <int NP, int W>
 static void launch_stream_one_w(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
-  launch_stream_one_rw<NP, 4, W>(q, KN, SP, c0, c1);
+  launch_stream_one_rw<NP, FJG_STREAM_R, W>(q, KN, SP, c0, c1);
 }
 template <int NP>
 static void launch_stream_one_np(fjg_query* q, const KNode& KN, const SProbe& SP, uint64_t c0, uint64_t c1) {
