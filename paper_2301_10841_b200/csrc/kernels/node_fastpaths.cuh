@@ -130,6 +130,12 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
 #ifndef FJG_GJ_BF_MINB
 #define FJG_GJ_BF_MINB 4
 #endif
+#ifndef FJG_STREAM_MINB
+#define FJG_STREAM_MINB 4
+#endif
+#ifndef FJG_STREAM_R
+#define FJG_STREAM_R 2
+#endif
 #ifndef FJG_GJ_TICKET
 #define FJG_GJ_TICKET 16  // C2 last node 3.46 -> 3.20 ms, C5 1873 -> 1587 ms (vs static striding)
 #endif
@@ -893,7 +899,7 @@ __device__ __forceinline__ void stream_one_write(const KNode& N, const SProbe& S
 }
 
 template <int NP, int R, int W>
-__global__ void __launch_bounds__(TILE, 3) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
+__global__ void __launch_bounds__(TILE, FJG_STREAM_MINB) k_stream_one(const __grid_constant__ KNode N, const SProbe SP, uint64_t c0,
                                                         uint64_t c1, DevCounters* ctr) {
   constexpr int QC = StreamOneQC<NP, R>::QC;
   constexpr int NQ = NP > 1 ? NP - 1 : 1;
