@@ -880,22 +880,96 @@ static void chunk_owners(fjg_query* q, const uint64_t* scan, uint64_t F, uint64_
   ++eng->launches;
 }
 
+// Launch a force batch (clear -> insert -> assign -> scatter, blockIdx.y =
+// member); `upper` bounds every member's offset count, `single` says the
+// members are whole subtries (roots), `multi` the key arity >= 2 path.
+static void launch_force_batch(fjg_query* q, const ForceBatch& B, uint64_t upper, bool single, bool multi) {
+  fjg_engine* eng = q->eng;
+  q->mark(eng->stream, -1);
+  const dim3 g(grid_for(upper, 256, std::max(1, eng->num_sms * 16 / B.n)), B.n);
+  const dim3 ga(grid_for(upper, 256, std::max(1, eng->num_sms * 8 / B.n)), B.n);
+  // (k_force_clear also resets each member's counters and a root's cursor / key count)
+  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->d_ctr));
+  if (multi)
+    LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+  else
+    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+  if (single)
+    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+  else
+    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+  // (k_force_scatter also finalizes: states forced, keys inserted accumulated)
+  LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+  q->mark(eng->stream, 0);
+}
+
+static bool root_sorted_path(const fjg_query* q, int t) {
+  const auto& T = q->tries[t];
+  return T.levels[0].size() <= 1 && T.rel->nrows >= (1u << 21) && FJG_SORTED_ROOT;
+}
+
+// Force the roots of tries `ts` (all unforced): sorted roots one by one, the
+// atomic-path roots together in batches whose rows fit the scratch arrays.
+static void force_roots(fjg_query* q, const std::vector<int>& ts) {
+  fjg_engine* eng = q->eng;
+  for (int multi = 0; multi < 2; ++multi) {
+    ForceBatch B;
+    memset(&B, 0, sizeof(B));
+    uint64_t off = 0, upper = 0;
+    auto flush = [&]() {
+      if (!B.n) return;
+      launch_force_batch(q, B, upper, true, multi != 0);
+      memset(&B, 0, sizeof(B));
+      off = upper = 0;
+    };
+    for (int t : ts) {
+      auto& T = q->tries[t];
+      if ((int)T.lev[0].multi != multi) continue;
+      if (root_sorted_path(q, t)) {
+        if (!multi) force_root_sorted(q, t);
+        else continue;
+      } else {
+        const uint32_t n = (uint32_t)T.rel->nrows;
+        if (n == 0)  // empty root: probes read bucket 0 of a zero-length region and must see EMPTY
+          CK(cudaMemsetAsync(T.dev.lev[0].table, 0xFF, 4 * sizeof(Slot), eng->stream));
+        if (off + n > std::max<uint64_t>(q->max_n, 1)) flush();
+        ForceRange& R = B.R[B.n++];
+        R.single = 1;
+        R.p0 = 0;
+        R.len0 = n;
+        R.trie = t;
+        R.lev = 0;
+        R.slot_off = (uint32_t)off;
+        off += n;
+        upper = std::max<uint64_t>(upper, n);
+        q->forces += 1;
+        q->maps_built += 1;
+        q->rows_forced += n;
+        T.lev[0].dirty = true;
+      }
+      T.root_forced = true;
+    }
+    flush();
+  }
+}
+
 static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, uint32_t len0, uint32_t count) {
   fjg_engine* eng = q->eng;
   auto& T = q->tries[t];
   DevLevel& L = T.dev.lev[l];
-  if (single && l == 0 && T.levels[0].size() <= 1 && len0 >= (1u << 21) && FJG_SORTED_ROOT) {
-    force_root_sorted(q, t);
+  if (single && l == 0) {
+    force_roots(q, {t});
     return;
   }
-  if (single && len0 == 0) {
-    // empty root: probes read bucket p of a zero-length region and must see EMPTY
-    CK(cudaMemsetAsync(L.table + 4ull * p0, 0xFF, 4 * sizeof(Slot), eng->stream));
-  }
-  ForceRange R{};
+  ForceBatch B;
+  memset(&B, 0, sizeof(B));
+  B.n = 1;
+  ForceRange& R = B.R[0];
   R.single = single ? 1 : 0;
   R.p0 = p0;
   R.len0 = len0;
+  R.trie = t;
+  R.lev = l;
   uint64_t upper = len0;
   if (!single) {
     R.list_p = L.list_p;
@@ -918,28 +992,7 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     ++eng->launches;
     R.owner = q->owner_scratch;
   }
-  q->mark(eng->stream, -1);
-  const unsigned g = grid_for(upper, 256, eng->num_sms * 16);
-  // (k_force_clear also resets this force's counters and the root's cursor / key count)
-  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->d_ctr));
-  if (T.lev[l].multi)
-    LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
-                                                                  q->d_ctr));
-  else
-    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank,
-                                                                   q->d_ctr));
-  const unsigned ga = grid_for(upper, 256, eng->num_sms * 8);
-  if (single)
-    LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, p0, R, q->tmp_slot, q->tmp_rank,
-                                                                  q->d_ctr));
-  else
-    LAUNCH(eng, k_force_assign<false><<<ga, 256, 0, eng->stream>>>(q->d_tries, t, l, 0u, R, q->tmp_slot,
-                                                                   q->tmp_rank, q->d_ctr));
-  LAUNCH(eng, k_force_scatter<<<g, 256, 0, eng->stream>>>(q->d_tries, t, l, R, q->tmp_slot, q->tmp_rank, q->d_ctr));
-  // keys inserted accumulate on the device
-  LAUNCH(eng, k_force_finalize<<<single ? 1 : grid_for(count), 256, 0, eng->stream>>>(q->d_tries, t, l, R,
-                                                                                    q->d_ctr));
-  q->mark(eng->stream, 0);
+  launch_force_batch(q, B, upper, single, T.lev[l].multi);
   q->forces += 1;
   q->maps_built += single ? 1 : count;
   q->rows_forced += single ? len0 : 0;
@@ -954,12 +1007,14 @@ static void force_claims(fjg_query* q, int k) {
   fjg_engine* eng = q->eng;
   DevCounters& H = *q->h_ctr;
   bool any = false;
+  std::vector<int> roots;
+  for (size_t t = 0; t < q->tries.size(); ++t)
+    if (H.root_need[t] && !q->tries[t].root_forced) roots.push_back((int)t);
+  if (!roots.empty()) {
+    force_roots(q, roots);
+    any = true;
+  }
   for (size_t t = 0; t < q->tries.size(); ++t) {
-    if (H.root_need[t] && !q->tries[t].root_forced) {
-      force_level(q, (int)t, 0, true, 0, (uint32_t)q->tries[t].rel->nrows, 1);
-      q->tries[t].root_forced = true;
-      any = true;
-    }
     for (int l = 1; l < (int)q->tries[t].levels.size(); ++l) {
       const uint32_t c = H.list_count[t * MAXL + l];
       if (c) {
@@ -1291,11 +1346,10 @@ static void run_memo_passes(fjg_query* q) {
   std::set<int> tries;
   for (int j = q->chain_start; j < (int)q->nodes.size(); ++j)
     for (int i = 0; i < q->nodes[j].nsub; ++i) tries.insert(q->nodes[j].sub[i].trie);
+  std::vector<int> roots;
   for (int t : tries)
-    if (!q->tries[t].root_forced) {
-      force_level(q, t, 0, true, 0, (uint32_t)q->tries[t].rel->nrows, 1);
-      q->tries[t].root_forced = true;
-    }
+    if (!q->tries[t].root_forced) roots.push_back(t);
+  force_roots(q, roots);
   for (auto& [t, own] : q->owner) {
     const uint64_t n = q->tries[t].rel->nrows;
     if (!n) continue;
@@ -1320,13 +1374,13 @@ static void run_memo_passes(fjg_query* q) {
 // or every level of every trie (SIMPLE) before the join; COLT does neither.
 static void eager_build(fjg_query* q) {
   fjg_engine* eng = q->eng;
+  std::vector<int> roots;
+  for (size_t t = 0; t < q->tries.size(); ++t)
+    if (q->tries[t].map_levels >= 1 && !q->tries[t].root_forced) roots.push_back((int)t);
+  force_roots(q, roots);
   for (size_t t = 0; t < q->tries.size(); ++t) {
     auto& T = q->tries[t];
     if (T.map_levels < 1) continue;
-    if (!T.root_forced) {
-      force_level(q, (int)t, 0, true, 0, (uint32_t)T.rel->nrows, 1);
-      T.root_forced = true;
-    }
     if (q->backend != FJG_BACKEND_SIMPLE) continue;
     const uint64_t nslots = 4 * std::max<uint64_t>(T.rel->nrows, 1);
     for (int l = 1; l < T.map_levels; ++l) {

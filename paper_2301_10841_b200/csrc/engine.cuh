@@ -195,6 +195,8 @@ struct DevCounters {
   uint32_t level_dup[MAXT * MAXL];  // some force of (trie, level) met a repeated key: child counts can exceed 1
   uint64_t tail_inputs[MAXN];  // node inputs counted on the device (fused Cartesian tail nodes)
   unsigned long long ticket;   // last-node chunk tickets (FJG_GJ_TICKET)
+  uint32_t fnew[MAXT];         // per member of a force batch: new keys (slots claimed)
+  uint32_t fdup[MAXT];         // per member of a force batch: a repeated key was met
 };
 
 // Fused Cartesian tail (nodes k..K-1 each one stream-iterated subatom binding

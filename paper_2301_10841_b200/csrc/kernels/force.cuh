@@ -15,6 +15,15 @@ struct ForceRange {
   const uint32_t* owner;       // list entry of every forced offset index (max-scan of start markers)
   uint32_t p0, len0;
   int single;
+  int trie, lev;      // the (trie, level) this member forces
+  uint32_t slot_off;  // its offset into the tmp_slot / tmp_rank scratch
+};
+
+// Forces launched together (blockIdx.y = member): every root a node claims in
+// one set of launches; a level >= 1 force is a batch of one.
+struct ForceBatch {
+  int n;
+  ForceRange R[MAXT];
 };
 
 __device__ __forceinline__ uint32_t force_total(const ForceRange& R) {
@@ -48,13 +57,16 @@ __global__ void k_force_marks(const uint32_t* __restrict__ list_scan, const uint
 
 // clear the slot regions (one 4-slot bucket per position) and child counts of
 // the claimed subtries
-__global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+__global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                               DevCounters* ctr) {
-  const DevLevel& L = tries[trie].lev[lev];
+  const int y = blockIdx.y;
+  const ForceRange& R = B.R[y];
+  const int lev = R.lev;
+  const DevLevel& L = tries[R.trie].lev[lev];
   const uint32_t total = force_total(R);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // this force's counters (read by the later kernels only)
-    ctr->newslots = 0;
-    ctr->dup = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // this member's counters (read by the later kernels only)
+    ctr->fnew[y] = 0;
+    ctr->fdup[y] = 0;
     if (R.single) {
       L.cursor[lev == 0 ? 0 : R.p0] = 0;
       L.nkeys[lev == 0 ? 0 : R.p0] = 0;
@@ -75,9 +87,14 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, int trie, int l
 // on the 8-byte slot), then count it (the pending slot's q word is the group
 // counter; the returned value is the offset's rank inside its child group).
 template <bool MULTI>
-__global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+__global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                                uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
                                DevCounters* ctr) {
+  const int y = blockIdx.y;
+  const ForceRange& R = B.R[y];
+  const int trie = R.trie, lev = R.lev;
+  tmp_slot += R.slot_off;
+  tmp_rank += R.slot_off;
   const DevTrie& T = tries[trie];
   const DevLevel& L = T.lev[lev];
   const uint32_t total = force_total(R);
@@ -149,20 +166,25 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, int trie, int 
   typedef cub::BlockReduce<uint32_t, 256> BR;
   __shared__ typename BR::TempStorage rtmp;
   const uint32_t bw = BR(rtmp).Sum(wins);
-  if (threadIdx.x == 0 && bw) atomicAdd(&ctr->newslots, bw);
+  if (threadIdx.x == 0 && bw) atomicAdd(&ctr->fnew[y], bw);
   if (__syncthreads_or(sawdup) && threadIdx.x == 0) {
-    ctr->dup = 1u;
+    ctr->fdup[y] = 1u;
     ctr->level_dup[trie * MAXL + lev] = 1u;
   }
 }
 
 // Child-range allocation: q = p + (running sum of child sizes of p).
 template <bool SINGLE>
-__global__ void k_force_assign(const DevTrie* __restrict__ tries, int trie, int lev, uint32_t p0, ForceRange R,
+__global__ void k_force_assign(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                                const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank,
                                DevCounters* ctr) {
-  if (!ctr->dup) return;  // k_force_unique handles the all-distinct case
-  const DevLevel& L = tries[trie].lev[lev];
+  const int y = blockIdx.y;
+  const ForceRange& R = B.R[y];
+  if (!ctr->fdup[y]) return;  // the all-distinct case is k_force_scatter's identity grouping
+  const uint32_t p0 = R.p0;
+  tmp_slot += R.slot_off;
+  tmp_rank += R.slot_off;
+  const DevLevel& L = tries[R.trie].lev[R.lev];
   const uint32_t total = force_total(R);
   typedef cub::BlockScan<uint32_t, 256> BS;
   __shared__ typename BS::TempStorage tmp;
@@ -229,10 +251,29 @@ __device__ void force_unique_body(const DevTrie* __restrict__ tries, int trie, i
 
 // Scatter the clustered columns to their child ranges (repeated keys met), or
 // the identity grouping (k_force_unique's body) when every key was distinct.
-__global__ void k_force_scatter(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
+// Also finalizes the member (its subtries' state = forced, keys counted):
+// only later kernels read those, and they are stream-ordered after this one.
+__global__ void k_force_scatter(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                                 const uint32_t* __restrict__ tmp_slot, const uint32_t* __restrict__ tmp_rank,
-                                const DevCounters* __restrict__ ctr) {
-  if (!ctr->dup) {
+                                DevCounters* ctr) {
+  const int y = blockIdx.y;
+  const ForceRange& R = B.R[y];
+  const int trie = R.trie, lev = R.lev;
+  tmp_slot += R.slot_off;
+  tmp_rank += R.slot_off;
+  {
+    const DevLevel& L = tries[trie].lev[lev];
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // members of a batch finalize concurrently
+      atomicAdd((unsigned long long*)&ctr->keys_inserted, (unsigned long long)ctr->fnew[y]);
+    if (R.single) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
+    } else {
+      const uint32_t c = *R.list_count;
+      for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+        L.state[R.list_p[i]] = 2u;
+    }
+  }
+  if (!ctr->fdup[y]) {
     force_unique_body(tries, trie, lev, R, tmp_slot);
     return;
   }
@@ -276,18 +317,6 @@ __device__ void force_unique_body(const DevTrie* __restrict__ tries, int trie, i
   }
 }
 
-__global__ void k_force_finalize(const DevTrie* __restrict__ tries, int trie, int lev, ForceRange R,
-                                 DevCounters* ctr) {
-  const DevLevel& L = tries[trie].lev[lev];
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->keys_inserted += ctr->newslots;
-  if (R.single) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
-    return;
-  }
-  const uint32_t c = *R.list_count;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
-    L.state[R.list_p[i]] = 2u;
-}
 
 
 // ---------------------------------------------------------------------------
@@ -358,7 +387,7 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
     L.nkeys[0] = G;
     L.state[0] = 2u;
     ctr->newslots = G;
-    ctr->keys_inserted += G;
+    atomicAdd((unsigned long long*)&ctr->keys_inserted, (unsigned long long)G);
   }
 }
 

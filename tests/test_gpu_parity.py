@@ -450,3 +450,22 @@ def test_stream_one_and_cartesian_tail(engine, ndims):
     for batch in (0, 1000, 777):
         check(engine, q, plan, cols, min_var=0, batch_size=batch)
     check(engine, q, plan, cols, enumerate=True, batch_size=777)
+
+
+def test_batched_root_forces_count_keys(engine):
+    """Roots claimed together are forced in one batch (blockIdx.y = member):
+    every backend's keys_inserted equals the oracle's (SLT / SIMPLE force all
+    four dimension roots and the fact table's levels at once)."""
+    rng = np.random.default_rng(31)
+    q = [{"rel": "F", "vars": ["r", "f1", "f2", "f3"]}]
+    cols = [[np.arange(500, dtype=np.int32)] + [rng.integers(0, 30, 500).astype(np.int32) for _ in range(3)]]
+    for i in range(3):
+        q.append({"rel": f"D{i + 1}", "vars": [f"f{i + 1}", f"x{i + 1}"]})
+        keys = rng.integers(0, 40, 70).astype(np.int32)
+        cols.append([keys, rng.integers(0, 9, 70).astype(np.int32)])
+    plan = P.compile_plan({"query": q, "binary_plan": configs.left_deep([a["rel"] for a in q])}, "free")
+    for backend in ("colt", "slt", "simple"):
+        ref = oracle.execute(q, plan, cols, backend=backend)
+        r, _ = gpu_execute(engine, q, plan, cols, backend=backend)
+        assert (r.count, r.checksum) == (ref["count"], ref["checksum"])
+        assert r.keys_inserted == ref["keys_inserted"], (backend, r.keys_inserted, ref["keys_inserted"])
