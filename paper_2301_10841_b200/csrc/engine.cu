@@ -269,6 +269,7 @@ struct fjg_query {
   int gj_w[MAXN];  // per node: the GJ frontier-writing fast-path variable, or -1
   bool sw[MAXN];   // per node: the stream-cover frontier-writing fast path applies
   SProbe sprobe[MAXN];  // per node: probe plan of the single-binding stream kernel (np = 0: n/a)
+  int dev_tail_node = -1;  // a tail launched with its frontier size on the device (inputs counted there)
   std::vector<TailPlan> tails;  // per node: fused Cartesian tail from this node on (ntail = 0: n/a)
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
@@ -1072,27 +1073,28 @@ static void launch_stream_one(fjg_query* q, const KNode& KN, const SProbe& SP, u
 #define FJG_TAIL 1
 #endif
 template <int MODE, int NT>
-static void launch_tail_nt(fjg_query* q, int k, uint64_t F) {
+static void launch_tail_nt(fjg_query* q, int k, uint64_t F, const uint32_t* dF) {
   fjg_engine* eng = q->eng;
   const KNode& KN = q->knodes[k];
   const TailPlan& T = q->tails[k];
   const unsigned g = grid_for(F, TILE, eng->num_sms * 8);
   if (q->width <= 4)
-    LAUNCH(eng, (k_tail<MODE, 4, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
-                                                                  q->d_ctr)));
+    LAUNCH(eng, (k_tail<MODE, 4, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, dF, q->min_var, q->out_tuples,
+                                                                  q->out_cap, q->d_ctr)));
   else if (q->width <= 8)
-    LAUNCH(eng, (k_tail<MODE, 8, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
-                                                                  q->d_ctr)));
+    LAUNCH(eng, (k_tail<MODE, 8, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, dF, q->min_var, q->out_tuples,
+                                                                  q->out_cap, q->d_ctr)));
   else
-    LAUNCH(eng, (k_tail<MODE, 16, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, q->min_var, q->out_tuples, q->out_cap,
-                                                                   q->d_ctr)));
+    LAUNCH(eng, (k_tail<MODE, 16, NT><<<g, TILE, 0, eng->stream>>>(KN, T, F, dF, q->min_var, q->out_tuples,
+                                                                   q->out_cap, q->d_ctr)));
 }
+// F: the frontier size (host), or an upper bound when dF (device count) is given
 template <int MODE>
-static void launch_tail(fjg_query* q, int k, uint64_t F) {
+static void launch_tail(fjg_query* q, int k, uint64_t F, const uint32_t* dF = nullptr) {
   if (q->tails[k].ntail == 1)
-    launch_tail_nt<MODE, 1>(q, k, F);
+    launch_tail_nt<MODE, 1>(q, k, F, dF);
   else
-    launch_tail_nt<MODE, MAXTAIL>(q, k, F);
+    launch_tail_nt<MODE, MAXTAIL>(q, k, F, dF);
 }
 
 __global__ void k_set_root_node(uint8_t* chosen, uint64_t* m, uint64_t* scan, int best, uint64_t mv) {
@@ -1271,6 +1273,22 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
                                               q->d_ctr));
     }
     q->mark(eng->stream, k == 0 ? 3 : 1);
+    if (FJG_TAIL && k + 1 < (int)q->nodes.size() && q->tails[k + 1].ntail > 0 &&
+        (mode == EXPAND_COUNT || mode == EXPAND_ENUM) && q->stop_node < 0) {
+      // the next nodes are a Cartesian tail: it reads its frontier size on the
+      // device, so this batch needs no host round trip
+      const uint32_t* dF = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(q->d_ctr) +
+                                                             offsetof(DevCounters, survivors));
+      q->mark(eng->stream, -1);
+      if (mode == EXPAND_COUNT)
+        launch_tail<EXPAND_COUNT>(q, k + 1, c1 - c0, dF);
+      else
+        launch_tail<EXPAND_ENUM>(q, k + 1, c1 - c0, dF);
+      q->mark(eng->stream, 2);
+      q->last_launches += 1;
+      q->dev_tail_node = k + 1;
+      continue;
+    }
     sync_counters(q);
     run_node(q, k + 1, q->h_ctr->survivors, mode);
   }
@@ -1335,6 +1353,7 @@ static void reset_query(fjg_query* q) {
   q->build_ms = q->join_ms = q->last_ms = 0;
   q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = q->phase_ms[3] = 0;
   q->last_launches = q->last_candidates = 0;
+  q->dev_tail_node = -1;
   for (int k = 0; k < MAXN; ++k) q->node_inputs[k] = 0;
   q->marks.clear();
   q->ev_used = 0;
@@ -1412,6 +1431,7 @@ static void execute_once(fjg_query* q, int mode) {
   }
   run_node(q, 0, 1, mode);
   sync_counters(q);
+  if (q->dev_tail_node >= 0) q->last_candidates += q->h_ctr->tail_inputs[q->dev_tail_node];
   q->resolve_marks();
   q->build_ms = q->phase_ms[0];
   q->join_ms = q->phase_ms[1] + q->phase_ms[2] + q->phase_ms[3];

@@ -1122,10 +1122,18 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
   }
 }
 
+// dF (optional): the frontier size on the device (the previous node's
+// survivor count, no host round trip); node k's inputs are then counted here.
 template <int MODE, int W, int NT>
 __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, const __grid_constant__ TailPlan T,
-                                               uint64_t F, int min_var, int32_t* __restrict__ out_tuples,
-                                               uint64_t out_cap, DevCounters* ctr) {
+                                               uint64_t F, const uint32_t* __restrict__ dF, int min_var,
+                                               int32_t* __restrict__ out_tuples, uint64_t out_cap,
+                                               DevCounters* ctr) {
+  if (dF) {
+    F = *dF;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && F)
+      atomicAdd((unsigned long long*)&ctr->tail_inputs[T.node[0]], (unsigned long long)F);
+  }
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0;
   long long acc_min = LLONG_MAX;
   uint64_t inputs[NT], body[NT];
