@@ -213,6 +213,7 @@ struct PhysTrieHost {
   DevTrie dev{};
   bool root_forced = false;
   int map_levels = 0;  // levels that are maps in some sharing atom's GHT schema (SIMPLE / SLT eager builds)
+  int key_bits = 32;   // bits used by the root key column (sorted roots: radix-sort end bit)
 };
 
 struct AtomInfo {
@@ -511,6 +512,37 @@ static void prepare_query(fjg_query* q) {
   std::vector<DevTrie> dt;
   for (auto& T : q->tries) dt.push_back(T.dev);
   CK(cudaMemcpyAsync(q->d_tries, dt.data(), dt.size() * sizeof(DevTrie), cudaMemcpyHostToDevice, q->eng->stream));
+  // Roots forced by radix sort sort only the bits their key column uses (its
+  // largest value as uint32; negative keys use all 32): one reduction per such
+  // trie here, at query creation, instead of a fourth sort pass per execution.
+  std::vector<int> sorted;
+  for (size_t t = 0; t < q->tries.size(); ++t) {
+    const auto& T = q->tries[t];
+    if (T.levels[0].size() == 1 && T.rel->nrows >= (1u << 21)) sorted.push_back((int)t);
+  }
+  if (!sorted.empty()) {
+    fjg_engine* eng = q->eng;
+    uint32_t* dmax = (uint32_t*)eng->pool->alloc(sorted.size() * 4);
+    size_t need = 0;
+    CK(cub::DeviceReduce::Max(nullptr, need, (const uint32_t*)nullptr, dmax, (int64_t)q->max_n, eng->stream));
+    void* tmp = eng->pool->alloc(std::max<size_t>(need, 16));
+    for (size_t i = 0; i < sorted.size(); ++i) {
+      auto& T = q->tries[sorted[i]];
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(T.dev.base[T.dev.lev[0].keycol[0]]);
+      size_t bytes = need;
+      CK(cub::DeviceReduce::Max(tmp, bytes, col, dmax + i, (int64_t)T.rel->nrows, eng->stream));
+    }
+    std::vector<uint32_t> hmax(sorted.size());
+    CK(cudaMemcpyAsync(hmax.data(), dmax, sorted.size() * 4, cudaMemcpyDeviceToHost, eng->stream));
+    CK(cudaStreamSynchronize(eng->stream));
+    for (size_t i = 0; i < sorted.size(); ++i) {
+      int bits = 1;
+      while (bits < 32 && (hmax[i] >> bits)) ++bits;
+      q->tries[sorted[i]].key_bits = bits;
+    }
+    eng->pool->free(tmp);
+    eng->pool->free(dmax);
+  }
 }
 
 // Resolve each node's descriptor into the constant-bank kernel plan.
@@ -849,7 +881,7 @@ static void force_root_sorted(fjg_query* q, int t) {
   }
   LAUNCH(eng, k_root_keys<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, keys, rows, pay));
   size_t bytes = q->cub_tmp_bytes;
-  const int kb = T.levels[0].empty() ? 1 : 32;
+  const int kb = T.levels[0].empty() ? 1 : T.key_bits;
   CK(cub::DeviceRadixSort::SortPairs(q->cub_tmp, bytes, keys, skeys, rows, srows, (int64_t)n, 0, kb, eng->stream));
   ++eng->launches;
   LAUNCH(eng, k_root_starts<<<g, 256, 0, eng->stream>>>(skeys, n, flags));

@@ -176,8 +176,12 @@ class ShardedQuery:
         held = exchange(self.local, self.views, self.world, self.rank, self.ops, self.group, prev)
         torch.cuda.current_stream(self.ops.device).synchronize()
         same = prev is not None and all(h is p for v in held for h, p in zip(held[v], prev[v]))
+        # zero-copy relations over the exchanged buffers, bound once: every step
+        # exchanges the same local slices, so the buffers' contents never change
+        # under the bound query (relations are immutable; the query
+        # caches per-relation facts such as a sorted root's key width)
         if self._q is None or not same:
-            self._bind(held)  # zero-copy relations over the exchanged buffers, bound once
+            self._bind(held)
         r = self._q.execute(min_var=min_var, timing=timing, **kw)
         r.extra["local_count"] = r.count
         r.count, r.checksum, r.min_value = reduce_results(r.count, r.checksum, r.min_value, self.ops.device,
