@@ -469,3 +469,18 @@ def test_batched_root_forces_count_keys(engine):
         r, _ = gpu_execute(engine, q, plan, cols, backend=backend)
         assert (r.count, r.checksum) == (ref["count"], ref["checksum"])
         assert r.keys_inserted == ref["keys_inserted"], (backend, r.keys_inserted, ref["keys_inserted"])
+
+
+def test_sorted_root_key_widths(engine):
+    """Roots of >= 2^21 rows are forced by a radix sort over the key column's
+    used bits (its maximum, computed at query creation): narrow, wide and
+    negative keys (all 32 bits as uint32) give the oracle's results."""
+    rng = np.random.default_rng(5)
+    n = (1 << 21) + 77
+    q = [{"rel": "E", "vars": ["a", "b"]}, {"rel": "S", "vars": ["b", "c"]}]
+    for lo, hi in ((0, 1 << 20), (-(1 << 31), (1 << 31) - 1), (-(1 << 20), 1 << 20)):
+        E = [rng.integers(0, 50, n).astype(np.int32), rng.integers(lo, hi, n, dtype=np.int64).astype(np.int32)]
+        S = [np.concatenate([E[1][:3000], rng.integers(lo, hi, 100, dtype=np.int64).astype(np.int32)]),
+             rng.integers(0, 7, 3100).astype(np.int32)]
+        plan = P.compile_plan({"query": q, "binary_plan": configs.left_deep(["S", "E"])}, "free")
+        check(engine, q, plan, [E, S])
