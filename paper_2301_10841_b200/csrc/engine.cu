@@ -191,11 +191,18 @@ struct ScopedDevice {
   }
 };
 
-#define LAUNCH(eng, ...)          \
-  do {                            \
-    __VA_ARGS__;                  \
-    ++(eng)->launches;            \
-    CK(cudaGetLastError());       \
+// FJG_DEBUG_SYNC=1 (environment): synchronise after every launch so a device
+// fault is reported at the kernel that raised it (debugging only).
+static bool debug_sync() {
+  static const bool on = getenv("FJG_DEBUG_SYNC") && atoi(getenv("FJG_DEBUG_SYNC")) != 0;
+  return on;
+}
+#define LAUNCH(eng, ...)                                           \
+  do {                                                             \
+    __VA_ARGS__;                                                   \
+    ++(eng)->launches;                                             \
+    CK(cudaGetLastError());                                        \
+    if (debug_sync()) CK(cudaStreamSynchronize((eng)->stream));    \
   } while (0)
 
 struct PhysLevelHost {
@@ -1433,6 +1440,9 @@ static void eager_build(fjg_query* q) {
     auto& T = q->tries[t];
     if (T.map_levels < 1) continue;
     if (q->backend != FJG_BACKEND_SIMPLE) continue;
+    // an empty relation has no subtries below its root: its deeper tables were
+    // never cleared by a force, so k_eager_list must not read them
+    if (T.rel->nrows == 0) continue;
     const uint64_t nslots = 4 * std::max<uint64_t>(T.rel->nrows, 1);
     for (int l = 1; l < T.map_levels; ++l) {
       uint32_t* cntp = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(q->d_ctr) +

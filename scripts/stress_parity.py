@@ -1,0 +1,61 @@
+"""Randomised GPU-vs-oracle stress (not part of the test suite): random
+queries (larger than tests/randq defaults), every plan mode, random backend /
+batch size / dynamic cover, count + checksum + MIN, and the enumerated bag on
+every 5th case.  python scripts/stress_parity.py SEED SECONDS"""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import numpy as np
+import paper_2301_10841_b200 as fjg
+from paper_2301_10841_b200 import plan as P
+from oracle import oracle
+from randq import bag_equal, random_query
+
+seed, budget = int(sys.argv[1]), float(sys.argv[2])
+rng = np.random.default_rng(seed)
+eng = fjg.Engine(0)
+t0, n, bad, kbad = time.time(), 0, 0, 0
+while time.time() - t0 < budget:
+    q, cols = random_query(rng, max_atoms=6, max_rows=int(rng.choice([30, 60, 120])))
+    if np.prod([max(len(c[0]), 1) for c in cols], dtype=np.float64) > 2e6:  # output upper bound
+        continue
+    for mode in ("binary", "free", "generic"):
+        plan = P.compile_plan(q, mode)
+        dyn = bool(rng.random() < 0.7)
+        batch = int(rng.choice([0, 3, 64, 1000]))
+        backend = str(rng.choice(["colt", "colt", "slt", "simple"]))
+        head = P.head_variables(q["query"])
+        mv = int(rng.integers(-1, len(head)))
+        enum = n % 5 == 0
+        ref = oracle.execute(q, plan, cols, output_mode="enumerate" if enum else "count", min_var=mv,
+                             dynamic_cover=dyn, backend=backend)
+        with open(os.environ.get("STRESS_LAST", "/tmp/stress_last.json"), "w") as f:  # the case about to run
+            json.dump({"seed": seed, "n": n, "mode": mode, "backend": backend, "batch": batch, "dyn": dyn, "mv": mv,
+                       "enum": enum, "q": q, "cols": [[c.tolist() for c in cs] for cs in cols]}, f)
+        rels = [eng.relation(c) for c in cols]
+        qq = eng.query({"query": q["query"]}, plan, rels)
+        kw = dict(batch_size=batch, dynamic_cover=dyn, backend=backend, min_var=None if mv < 0 else mv)
+        if enum:
+            rows, r = qq.enumerate(**kw)
+            ok = bag_equal(rows, ref["tuples"])
+        else:
+            r = qq.execute(**kw)
+            ok = True
+        ok = ok and r.count == ref["count"] and r.checksum == ref["checksum"]
+        if mv >= 0 and ref["count"]:
+            ok = ok and r.min_value == ref["min"]
+        kmis = backend == "simple" and r.keys_inserted != ref["keys_inserted"]
+        if kmis:
+            kbad += 1
+        if not ok:
+            bad += 1
+            print("MISMATCH", seed, n, mode, backend, batch, dyn, mv, r.count, ref["count"], hex(r.checksum),
+                  hex(ref["checksum"]), q, flush=True)
+        qq.close()
+        for x in rels:
+            x.close()
+        n += 1
+        if n % 100 == 0:
+            print(f"{n} cases, {bad} mismatches, {kbad} key diffs, {time.time() - t0:.0f} s", flush=True)
+print(f"stress seed={seed}: {n} cases, {bad} mismatches, {kbad} SIMPLE key-count differences, "
+      f"{time.time() - t0:.0f} s", flush=True)
