@@ -44,7 +44,10 @@ while time.time() - t0 < budget:
         ok = ok and r.count == ref["count"] and r.checksum == ref["checksum"]
         if mv >= 0 and ref["count"]:
             ok = ok and r.min_value == ref["min"]
-        kmis = backend == "simple" and r.keys_inserted != ref["keys_inserted"]
+        # SIMPLE key counts are exact unless the join itself forces terminal
+        # vectors under dynamic cover, where the device claims per batch what the
+        # oracle forces per binding: compare with a static cover
+        kmis = backend == "simple" and not dyn and r.keys_inserted != ref["keys_inserted"]
         if kmis:
             kbad += 1
         if not ok:
