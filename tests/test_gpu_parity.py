@@ -484,3 +484,23 @@ def test_sorted_root_key_widths(engine):
              rng.integers(0, 7, 3100).astype(np.int32)]
         plan = P.compile_plan({"query": q, "binary_plan": configs.left_deep(["S", "E"])}, "free")
         check(engine, q, plan, [E, S])
+
+
+def test_simple_backend_empty_relation_after_pool_reuse(engine):
+    """SIMPLE forces every map level eagerly; an empty relation has no subtries
+    below its root, and its deeper tables (recycled device memory) must not be
+    read. The same query first runs with the relation non-empty so its freed
+    tables hold occupied slots when the empty one is bound."""
+    q = {"query": [{"rel": "A", "vars": ["x", "y", "z"]}, {"rel": "B", "vars": ["z", "x", "y"]},
+                   {"rel": "C", "vars": ["y", "z"]}]}
+    rng = np.random.default_rng(8)
+    full = [rng.integers(0, 4, 24).astype(np.int32) for _ in range(3)]
+    empty = [np.zeros(0, np.int32)] * 3
+    C = [rng.integers(0, 4, 10).astype(np.int32) for _ in range(2)]
+    for mode in ("generic", "free"):
+        plan = P.compile_plan(q, mode)
+        for b_cols in (full, empty, full, empty):
+            cols = [[c.copy() for c in full], [c.copy() for c in b_cols], C]
+            ref = oracle.execute(q, plan, cols, backend="simple", dynamic_cover=False)
+            r, _ = gpu_execute(engine, q, plan, cols, backend="simple", dynamic_cover=False)
+            assert (r.count, r.checksum, r.keys_inserted) == (ref["count"], ref["checksum"], ref["keys_inserted"])
