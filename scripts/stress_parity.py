@@ -12,17 +12,46 @@ from oracle import oracle
 from randq import bag_equal, random_query
 
 seed, budget = int(sys.argv[1]), float(sys.argv[2])
+WIDE = len(sys.argv) > 3 and sys.argv[3] == "wide"
+
+
+def wide_query(rng):
+    """Larger relations over wider domains (hundreds to thousands of rows)."""
+    nvars = int(rng.integers(2, 5))
+    pool = [f"v{i}" for i in range(nvars)]
+    natoms = int(rng.integers(2, 5))
+    atoms, cols = [], []
+    for a in range(natoms):
+        arity = int(rng.integers(1, min(3, nvars) + 1))
+        vs = list(rng.choice(pool, size=arity, replace=False))
+        atoms.append({"rel": f"A{a}", "vars": [str(v) for v in vs]})
+        n = int(rng.integers(0 if rng.random() < 0.03 else 20, 600))
+        dom = int(rng.integers(8, 80))
+        cols.append([np.floor(dom * rng.random(n) ** 2).astype(np.int32) for _ in range(arity)])
+    order = list(rng.permutation(natoms))
+    tree = atoms[order[0]]["rel"]
+    for i in order[1:]:
+        tree = ["join", tree, atoms[i]["rel"]]
+    return {"query": atoms, "binary_plan": tree}, cols
+
 rng = np.random.default_rng(seed)
 eng = fjg.Engine(0)
 t0, n, bad, kbad = time.time(), 0, 0, 0
 while time.time() - t0 < budget:
-    q, cols = random_query(rng, max_atoms=6, max_rows=int(rng.choice([30, 60, 120])))
-    if np.prod([max(len(c[0]), 1) for c in cols], dtype=np.float64) > 2e6:  # output upper bound
-        continue
+    if WIDE:
+        q, cols = wide_query(rng)
+        if np.prod([max(len(c[0]), 1) for c in cols], dtype=np.float64) > 1e8:
+            continue
+        if oracle.execute(q, P.compile_plan(q, "free"), cols)["count"] > 100000:
+            continue
+    else:
+        q, cols = random_query(rng, max_atoms=6, max_rows=int(rng.choice([30, 60, 120])))
+        if np.prod([max(len(c[0]), 1) for c in cols], dtype=np.float64) > 2e6:  # output upper bound
+            continue
     for mode in ("binary", "free", "generic"):
         plan = P.compile_plan(q, mode)
         dyn = bool(rng.random() < 0.7)
-        batch = int(rng.choice([0, 3, 64, 1000]))
+        batch = int(rng.choice([0, 3, 64, 1000, 4096]))
         backend = str(rng.choice(["colt", "colt", "slt", "simple"]))
         head = P.head_variables(q["query"])
         mv = int(rng.integers(-1, len(head)))
