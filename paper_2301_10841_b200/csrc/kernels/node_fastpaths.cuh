@@ -787,29 +787,7 @@ struct SProbe {
   int8_t kc[4];    // cover column (index into the cover's src[]) holding probe j's key
 };
 
-// First half of a bucket (slots 0-1) in one 128-bit load; slots fill in order,
-// so a free slot among them ends a miss, and only a full half without the key
-// reads the second half (rare at load <= 0.25).
-__device__ __forceinline__ uint32_t half_match(const uint4& a, uint32_t kw, bool& more) {
-  uint32_t q = (a.w != kEmpty && a.z == kw) ? a.w : kEmpty;
-  q = (a.y != kEmpty && a.x == kw) ? a.y : q;
-  more = a.w != kEmpty && q == kEmpty;
-  return q;
-}
-__device__ __forceinline__ uint32_t probe_rest(const Slot* table, uint64_t b, uint64_t blo, uint64_t bhi,
-                                               uint32_t kw) {
-  const uint4* tb = reinterpret_cast<const uint4*>(table);
-  bool more;
-  const uint4 h1 = __ldg(tb + 2 * b + 1);
-  uint32_t q = half_match(h1, kw, more);
-  while (more) {
-    if (++b == bhi) b = blo;
-    q = bucket_match(ld_bucket(table, b), kw, more);
-  }
-  return q;
-}
-
-// probe one key in a subtrie region (first half-bucket already loaded)
+// probe one key in a subtrie region: 256-bit bucket loads until a match or a free slot
 __device__ __forceinline__ uint32_t probe_region_one(const Slot* table, uint32_t p, uint32_t len, uint32_t kw) {
   uint64_t b = (uint32_t)region_bucket(p, len, kw);
   bool more;
@@ -821,10 +799,6 @@ __device__ __forceinline__ uint32_t probe_region_one(const Slot* table, uint32_t
   return q;
 }
 
-template <int NP, int W>
-struct StreamOneCtx {
-  static constexpr int QC = 256;  // per-warp ring capacity per stage (>= 32*R + 31)
-};
 template <int NP, int R>
 struct StreamOneQC {
   static constexpr int QC = R <= 7 ? 256 : 512;  // per-warp ring capacity per stage (>= 32*R + 31)
