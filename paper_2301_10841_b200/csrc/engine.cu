@@ -1021,7 +1021,9 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     size_t bytes = q->cub_tmp_bytes;
     CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, L.list_len, L.list_scan, (int64_t)count, eng->stream));
     ++eng->launches;
-    upper = T.rel->nrows;
+    // offsets to force: the claims' total when k_select counted it, else the level
+    const uint32_t claimed = q->h_ctr->list_total[t * MAXL + l];
+    upper = claimed ? std::min<uint64_t>(claimed, T.rel->nrows) : T.rel->nrows;
     // offset index -> list entry: marks at each entry's first index, then a max-scan
     CK(cudaMemsetAsync(q->owner_scratch, 0, std::max<uint64_t>(upper, 1) * 4, eng->stream));
     LAUNCH(eng, k_force_marks<<<grid_for(count), 256, 0, eng->stream>>>(L.list_scan, R.list_count,
@@ -1064,8 +1066,11 @@ static void force_claims(fjg_query* q, int k) {
     }
   }
   if (any) {
+    static_assert(offsetof(DevCounters, root_need) == offsetof(DevCounters, list_count) + sizeof(DevCounters::list_count) &&
+                      offsetof(DevCounters, list_total) == offsetof(DevCounters, root_need) + sizeof(DevCounters::root_need),
+                  "claim counters contiguous");
     CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, list_count), 0,
-                       sizeof(H.list_count) + sizeof(H.root_need), eng->stream));
+                       sizeof(H.list_count) + sizeof(H.root_need) + sizeof(H.list_total), eng->stream));
   }
   (void)k;
 }

@@ -191,6 +191,7 @@ struct DevCounters {
   uint32_t dup;  // the running force met a repeated key (else every child is a single row)
   uint32_t list_count[MAXT * MAXL];
   uint32_t root_need[MAXT];
+  uint32_t list_total[MAXT * MAXL];  // offsets of the claimed subtries (sum of their lengths)
   uint32_t root_region[MAXT];  // buckets of each trie's root slot region (rows, or distinct keys once sorted)
   uint32_t level_dup[MAXT * MAXL];  // some force of (trie, level) met a repeated key: child counts can exceed 1
   uint64_t tail_inputs[MAXN];  // node inputs counted on the device (fused Cartesian tail nodes)

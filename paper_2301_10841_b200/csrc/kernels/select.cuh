@@ -34,7 +34,12 @@ __device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters*
   if (!wm) return;
   const int first = __ffs(wm) - 1;
   uint32_t base = 0;
-  if (lane == first) base = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], (uint32_t)__popc(wm));
+  // the claimed offsets, so the force sizes its owner map by them, not by the level
+  const uint32_t tot = __reduce_add_sync(act, won ? len : 0u);
+  if (lane == first) {
+    base = atomicAdd(&ctr->list_count[S.trie * MAXL + S.depth], (uint32_t)__popc(wm));
+    atomicAdd(&ctr->list_total[S.trie * MAXL + S.depth], tot);
+  }
   base = __shfl_sync(act, base, first);
   if (won) {
     const uint32_t idx = base + __popc(wm & ((1u << lane) - 1u));
