@@ -1116,6 +1116,9 @@ static void launch_stream_one(fjg_query* q, const KNode& KN, const SProbe& SP, u
 #ifndef FJG_TAIL
 #define FJG_TAIL 1
 #endif
+#ifndef FJG_SELECT_NS
+#define FJG_SELECT_NS 1
+#endif
 template <int MODE, int NT>
 static void launch_tail_nt(fjg_query* q, int k, uint64_t F, const uint32_t* dF) {
   fjg_engine* eng = q->eng;
@@ -1202,8 +1205,15 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (!memo_top && host_select_root_node(q, k, F)) {
     // node 0 of a fresh COLT execution: its cover choice and claims need no device round trip
   } else {
-  LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(KN, q->d_tries, F,
-                                                                                    q->dynamic ? 1 : 0, q->d_ctr));
+  if (KN.nsub <= 2 && FJG_SELECT_NS)
+    LAUNCH(eng, k_select_ns<2><<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(
+                    KN, q->d_tries, F, q->dynamic ? 1 : 0, q->d_ctr));
+  else if (KN.nsub <= 3 && FJG_SELECT_NS)
+    LAUNCH(eng, k_select_ns<3><<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(
+                    KN, q->d_tries, F, q->dynamic ? 1 : 0, q->d_ctr));
+  else
+    LAUNCH(eng, k_select<<<grid_for(F, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(KN, q->d_tries, F,
+                                                                                      q->dynamic ? 1 : 0, q->d_ctr));
   if (F <= kSmallScan) {
     LAUNCH(eng, k_scan_small<<<1, 1024, 0, eng->stream>>>(N.m, N.scan, (uint32_t)F, q->d_ctr));
   } else {

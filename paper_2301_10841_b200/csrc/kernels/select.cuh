@@ -94,6 +94,73 @@ __global__ void k_select(const __grid_constant__ KNode N, const DevTrie* __restr
 }
 
 
+// k_select for nodes of at most NS subatoms: each subatom's subtrie and state
+// word are read once per binding and reused by the cover choice and the claims
+// (the generic kernel re-reads them for the claims).
+template <int NS>
+__global__ void k_select_ns(const __grid_constant__ KNode N, const DevTrie* __restrict__ tries, uint64_t F,
+                            int dynamic, DevCounters* ctr) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t iters = (F + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t e = start + it * stride;
+    const bool ok = e < F;
+    uint32_t p[NS], l[NS], st[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      p[s] = l[s] = 0;
+      st[s] = 1;
+      if (ok && s < N.nsub) {
+        const KSub& S = N.sub[s];
+        subtrie_of(S, e, p[s], l[s]);
+        if (p[s] != kSingleton) st[s] = *((volatile const uint32_t*)(S.state + (S.depth == 0 ? 0u : p[s])));
+      }
+    }
+    int best = N.cov[0];
+    if (ok) {
+      auto est = [&](int s) -> uint64_t {
+        uint64_t v = 0;
+#pragma unroll
+        for (int t = 0; t < NS; ++t)
+          if (t == s) {
+            const KSub& S = N.sub[t];
+            v = p[t] == kSingleton ? 1ull : (st[t] == 2u ? (uint64_t)S.nkeys[S.depth == 0 ? 0u : p[t]] : l[t]);
+          }
+        return v;
+      };
+      if (dynamic && N.ncov > 1) {
+        uint64_t best_est = est(best);
+        for (int ci = 1; ci < N.ncov; ++ci) {
+          const int s = N.cov[ci];
+          const uint64_t v = est(s);
+          if (v < best_est) {  // ties keep the lowest position
+            best_est = v;
+            best = s;
+          }
+        }
+      }
+      uint32_t bp = 0, bl = 0;
+#pragma unroll
+      for (int t = 0; t < NS; ++t)
+        if (t == best) {
+          bp = p[t];
+          bl = l[t];
+        }
+      N.chosen[e] = (uint8_t)best;
+      N.m[e] = (bp == kSingleton) ? 1ull : (uint64_t)bl;
+    }
+    // claims: the keys-iterated cover and every probed subatom must be forced
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s >= N.nsub) break;
+      const KSub& S = N.sub[s];
+      const bool need = ok && p[s] != kSingleton && (s != best || !S.stream) && st[s] == 0u;
+      claim_subtrie(tries, ctr, S, p[s], l[s], need);
+    }
+  }
+}
+
 // Inclusive scan of a small frontier's candidate counts in one block (F <=
 // kSmallScan), total written to DevCounters::total_m: one launch instead of
 // CUB's two plus a device-to-device copy.
