@@ -121,12 +121,18 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
       const unsigned long long mine = ((unsigned long long)(kPendBit | 1u) << 32) | kw;
       const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
       h = 4ull * region_bucket(p, len, kw);
+      bool first = R.single;  // roots: wide regions, the home slot is usually free
       while (true) {
         unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);
-        unsigned long long cur = *((volatile unsigned long long*)addr);
-        if ((uint32_t)(cur >> 32) == kEmpty) {
-          const unsigned long long old = atomicCAS(addr, cur, mine);
-          if (old == cur) {
+        // a root's home slot is tried with a CAS straight away (a cleared slot
+        // is all ones, so a free home slot costs one atomic and no load); other
+        // slots -- and every slot of a small subtrie region, where the keys
+        // crowd a few buckets -- are read first
+        unsigned long long cur = first ? kEmpty64 : *((volatile unsigned long long*)addr);
+        first = false;
+        if (cur == kEmpty64) {
+          const unsigned long long old = atomicCAS(addr, kEmpty64, mine);
+          if (old == kEmpty64) {
             won = true;
             if (MULTI) {
               *((volatile uint32_t*)(L.srep + h)) = pos + 1;
