@@ -353,8 +353,11 @@ def run_ours(args):
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
-        e2e = e2e_leg(fjg, eng, w, stream, mv, args.e2e_steps, flush)
+    if args.e2e_steps > 0:
+        if world > 1 or args.shard:
+            e2e = e2e_leg_sharded(sharded, w, mv, args.e2e_steps, flush, world, args.backend)
+        else:
+            e2e = e2e_leg(fjg, eng, w, stream, mv, args.e2e_steps, flush)
 
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None
@@ -438,6 +441,44 @@ def e2e_leg(fjg, eng, w, stream, mv, steps, flush):
             times.append(max(e0.elapsed_time(e1) / 1000.0, 0.0) or wall)
         units = w.input_tuples() + (res.count if w.output_mode == "count" else 0)
     t = statistics.median(times)
+    return {"value": units / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": 1000 * t, "steps": steps}
+
+
+def e2e_leg_sharded(sharded, w, mv, steps, flush, world, backend):
+    """N-rank end to end: every rank's pinned host slice of each base relation
+    -> H2D into its device slice -> partition + NCCL exchange -> query ->
+    result all-reduce read back to the host (ShardedQuery.execute). Device-timed
+    with CUDA events on the torch stream that issues the copies, the exchange and
+    the reduce (execute returns only after the reduced result is on the host),
+    max over ranks."""
+    import torch
+    dev_stream = torch.cuda.current_stream()
+    eng_stream = torch.cuda.ExternalStream(sharded.engine.stream_ptr, device=dev_stream.device)
+    host = {b: [c.cpu().pin_memory() for c in cols] for b, cols in sharded.local.items()}
+    h2d = sum(t.numel() * 4 for cols in host.values() for t in cols)
+    # result counters block + the reduced (count, checksum, min) words
+    d2h = 8 * 160 + 8 * 7
+    times = []
+    for i in range(steps + 1):
+        torch.cuda.synchronize()
+        barrier(world)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(dev_stream)
+        for b, cols in host.items():
+            for d, h in zip(sharded.local[b], cols):
+                d.copy_(h, non_blocking=True)
+        eng_stream.wait_stream(dev_stream)  # the partition kernel runs on the engine stream
+        res = sharded.execute(min_var=mv, output_mode=w.output_mode, backend=backend)
+        e1.record(dev_stream)
+        torch.cuda.synchronize()
+        flush.add_(1)
+        if i > 0:  # first iteration warms the exchange buffers
+            times.append(e0.elapsed_time(e1) / 1000.0)
+    t = allreduce_max(statistics.median(times), world)
+    out_local = res.extra.get("local_count", res.count)
+    units = allreduce_sum(sharded.input_tuples_local + (out_local if w.output_mode == "count" else 0), world)
     return {"value": units / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": 1000 * t, "steps": steps}
 
