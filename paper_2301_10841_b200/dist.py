@@ -54,27 +54,22 @@ def _reuse(out, i, n, ops):
     return ops.empty(n)
 
 
-def all_to_all_partitioned(cols, col, world, ops, group=None, out=None):
-    """Send each row to rank partition_of(row[col]); returns this rank's rows
+def all_to_all_partitioned(grouped, counts, recv_counts, ops, group=None, out=None):
+    """Rows already grouped by destination rank (partition_of(row[col]),
+    `counts` per destination) -> this rank's rows, `recv_counts` per source
     (written into `out` when its buffers have the right sizes)."""
-    grouped, counts = ops.partition(cols, col, world)
-    send = torch.tensor(counts, dtype=torch.int64, device=ops.device)
-    recv = torch.empty(world, dtype=torch.int64, device=ops.device)
-    dist.all_to_all_single(recv, send, group=group)
-    rc = [int(x) for x in recv.tolist()]
     res = []
     for i, g in enumerate(grouped):
-        o = _reuse(out, i, sum(rc), ops)
-        dist.all_to_all_single(o, g, output_split_sizes=rc, input_split_sizes=counts, group=group)
+        o = _reuse(out, i, sum(recv_counts), ops)
+        dist.all_to_all_single(o, g, output_split_sizes=recv_counts, input_split_sizes=counts, group=group)
         res.append(o)
     return res
 
 
-def all_gather_rows(cols, world, ops, group=None, out=None):
+def all_gather_rows(cols, sizes, world, ops, group=None, out=None):
+    """Every rank's rows of `cols` (`sizes` = each rank's row count),
+    concatenated in rank order."""
     n = cols[0].numel() if cols else 0
-    sizes = [torch.zeros(1, dtype=torch.int64, device=ops.device) for _ in range(world)]
-    dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=ops.device), group=group)
-    sizes = [int(s.item()) for s in sizes]
     m = max(sizes) if sizes else 0
     res = []
     for i, c in enumerate(cols):
@@ -98,32 +93,66 @@ def all_gather_rows(cols, world, ops, group=None, out=None):
 
 
 def reduce_results(count, checksum, minv, device, group=None):
-    """count (python int, < 2^127), checksum (u64), minv (int or None) -> global."""
+    """count (python int, < 2^127), checksum (u64), minv (int or None) -> global.
+    One all-gather of every rank's (count limbs, checksum halves, min) and a
+    host-side sum / min: one collective and one device->host read per step."""
     INT64_MAX = (1 << 63) - 1
     parts = [count & MASK32, (count >> 32) & MASK32, (count >> 64) & MASK32, count >> 96,
-             checksum & MASK32, checksum >> 32]
+             checksum & MASK32, checksum >> 32, INT64_MAX if minv is None else int(minv)]
     t = torch.tensor(parts, dtype=torch.int64, device=device)
-    dist.all_reduce(t, group=group)
-    v = [int(x) for x in t.tolist()]
+    world = dist.get_world_size(group)
+    if world == 1:
+        rows = [t.tolist()]
+    else:
+        allp = torch.empty(world * len(parts), dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(allp, t, group=group)
+        rows = allp.reshape(world, len(parts)).tolist()
+    v = [sum(int(r[i]) for r in rows) for i in range(6)]
     total = v[0] + (v[1] << 32) + (v[2] << 64) + (v[3] << 96)
     cs = (v[4] + (v[5] << 32)) & ((1 << 64) - 1)
-    m = torch.tensor([INT64_MAX if minv is None else int(minv)], dtype=torch.int64, device=device)
-    dist.all_reduce(m, op=dist.ReduceOp.MIN, group=group)
-    mv = int(m.item())
+    mv = min(int(r[6]) for r in rows)
     return total, cs, (None if mv == INT64_MAX else mv)
 
 
 def exchange(relations, views, world, rank, ops, group=None, bufs=None):
     """relations: base -> list of local-slice column tensors. Returns
     view -> list of column tensors held by this rank after the exchange
-    (reusing `bufs`, the previous step's result, when sizes match)."""
-    out = {}
-    for view in sorted(set(views), key=lambda v: (v[0], -1 if v[1] is None else v[1])):
+    (reusing `bufs`, the previous step's result, when sizes match).
+
+    Every partitioned view is grouped by destination first; then ONE
+    all-gather carries all size metadata (per partitioned view the counts
+    per destination, per replicated view the local row count), so a step
+    pays one metadata round trip however many views it exchanges."""
+    order = sorted(set(views), key=lambda v: (v[0], -1 if v[1] is None else v[1]))
+    meta, grouped = [], {}
+    for view in order:
         base, col = view
         cols = relations[base]
+        if col is None:
+            meta.append([cols[0].numel() if cols else 0] * world)
+        else:
+            g, counts = ops.partition(cols, col, world)
+            grouped[view] = (g, counts)
+            meta.append(list(counts))
+    nv = len(order)
+    mine = torch.tensor(meta, dtype=torch.int64, device=ops.device).reshape(-1)
+    if world == 1:
+        allm = mine
+    else:
+        allm = torch.empty(world * nv * world, dtype=torch.int64, device=ops.device)
+        dist.all_gather_into_tensor(allm, mine, group=group)
+    M = allm.reshape(world, nv, world).tolist()  # M[source rank][view][destination]
+    out = {}
+    for vi, view in enumerate(order):
+        base, col = view
         prev = bufs.get(view) if bufs else None
-        out[view] = all_gather_rows(cols, world, ops, group, prev) if col is None else \
-            all_to_all_partitioned(cols, col, world, ops, group, prev)
+        if col is None:
+            sizes = [int(M[r][vi][0]) for r in range(world)]
+            out[view] = all_gather_rows(relations[base], sizes, world, ops, group, prev)
+        else:
+            g, counts = grouped[view]
+            rc = [int(M[r][vi][rank]) for r in range(world)]
+            out[view] = all_to_all_partitioned(g, counts, rc, ops, group, prev)
     return out
 
 
