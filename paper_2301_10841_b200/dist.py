@@ -193,6 +193,7 @@ class ShardedQuery:
             self.local[base] = [torch.from_numpy(c[lo:hi].copy()).to(self.ops.device) for c in cols]
         self.input_tuples_local = sum(len(w.relations[b][0]) for b in w.atom_rel) / world
         self._q = None
+        self._eng_stream = torch.cuda.ExternalStream(engine.stream_ptr, device=self.ops.device)
 
     def _bind(self, held):
         rels = {v: self.engine.relation_from_torch(cols) for v, cols in held.items()}
@@ -203,7 +204,9 @@ class ShardedQuery:
     def execute(self, min_var=None, timing=False, **kw):
         prev = getattr(self, "_held", None)
         held = exchange(self.local, self.views, self.world, self.rank, self.ops, self.group, prev)
-        torch.cuda.current_stream(self.ops.device).synchronize()
+        # the executor runs on the engine stream: order it after the exchange
+        # on the device (no host synchronisation)
+        self._eng_stream.wait_stream(torch.cuda.current_stream(self.ops.device))
         same = prev is not None and all(h is p for v in held for h, p in zip(held[v], prev[v]))
         # zero-copy relations over the exchanged buffers, bound once: every step
         # exchanges the same local slices, so the buffers' contents never change
