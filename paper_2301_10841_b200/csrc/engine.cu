@@ -910,6 +910,7 @@ static void force_root_sorted(fjg_query* q, int t) {
 // Chunk owners for [c0, c1) at `chunk` candidates per chunk (k_chunk_marks + max-scan).
 static void chunk_owners(fjg_query* q, const uint64_t* scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk) {
   fjg_engine* eng = q->eng;
+  if ((chunk & (chunk - 1)) || c1 - c0 > kLastChunk) throw fj::EngineError("chunk_owners: chunk must be a power of two");
   const uint64_t n = (c1 - c0 + chunk - 1) / chunk + 1;
   CK(cudaMemsetAsync(q->chunk_owner, 0, n * 4, eng->stream));
   LAUNCH(eng, k_chunk_marks<<<grid_for(std::min<uint64_t>(F, (c1 - c0 + chunk - 1) / chunk + 1)), 256, 0,
@@ -1772,6 +1773,7 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     if (opts) o = *opts;
     if (o.min_var >= (int)q->head.size()) throw fj::ValidationError("min_var out of range");
     uint64_t batch = o.batch_size ? o.batch_size : (1ull << 25);
+    if (batch > kLastChunk) throw fj::ValidationError("batch_size must be <= 2^31");
     ensure_frontiers(q, batch);
     q->dynamic = o.dynamic_cover != 0;
     q->timing = o.collect_timing != 0;

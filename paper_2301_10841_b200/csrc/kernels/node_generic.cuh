@@ -44,16 +44,21 @@ __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uin
 // which is usually a single binding.
 __global__ void k_chunk_marks(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk,
                               uint32_t* __restrict__ owner) {
-  const uint64_t nch = (c1 - c0 + chunk - 1) / chunk;
-  // only the bindings whose candidates overlap [c0, c1): a contiguous range of the frontier
-  const uint64_t elo = upper_bound_u64(scan, 0, F - 1, c0), ehi = upper_bound_u64(scan, 0, F - 1, c1 - 1);
+  // chunk is a power of two and c1 - c0 <= kLastChunk (2^31): 32-bit shifts, no 64-bit division
+  const uint32_t sh = __ffs(chunk) - 1;
+  const uint32_t nch = (uint32_t)(c1 - c0 + chunk - 1) >> sh;
+  // only the bindings whose candidates overlap [c0, c1): a contiguous range of
+  // the frontier (a launch that starts at 0 / ends at the total skips the search;
+  // the zero-candidate bindings it then visits fall through lo >= hi)
+  const uint64_t elo = c0 == 0 ? 0 : upper_bound_u64(scan, 0, F - 1, c0);
+  const uint64_t ehi = c1 >= __ldg(scan + F - 1) ? F - 1 : upper_bound_u64(scan, 0, F - 1, c1 - 1);
   for (uint64_t e = elo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= ehi;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull, se = __ldg(scan + e);
     const uint64_t lo = max(prev, c0), hi = min(se, c1);
     if (lo >= hi) continue;
-    const uint64_t c = (lo - c0 + chunk - 1) / chunk;
-    if (c * chunk + c0 < hi) owner[c] = (uint32_t)e;
+    const uint32_t c = ((uint32_t)(lo - c0) + chunk - 1) >> sh;
+    if (((uint64_t)c << sh) + c0 < hi) owner[c] = (uint32_t)e;
     if (hi == c1) owner[nch] = (uint32_t)e;
   }
 }
