@@ -48,8 +48,11 @@ FJ_HD uint64_t slot_hash(uint32_t parent, uint32_t key) {
 
 // Hash-partition function for multi-GPU sharding on the first plan variable.
 FJ_HD uint32_t partition_of(int32_t v, uint32_t nparts) {
-  return static_cast<uint32_t>(fmix64(static_cast<uint64_t>(static_cast<int64_t>(v)) ^ 0x5bd1e995ULL) %
-                               nparts);
+  const uint64_t h = fmix64(static_cast<uint64_t>(static_cast<int64_t>(v)) ^ 0x5bd1e995ULL);
+  // power-of-two rank counts (1/2/4/8 GPUs): a mask, the same value as h % nparts
+  // without the 64-bit division subroutine on the device
+  if ((nparts & (nparts - 1)) == 0) return static_cast<uint32_t>(h & (nparts - 1));
+  return static_cast<uint32_t>(h % nparts);
 }
 
 }  // namespace fj

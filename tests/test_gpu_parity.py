@@ -173,15 +173,16 @@ def test_filter_and_partition_kernels(engine):
     assert (f[0] == c0[keep]).all() and (f[1] == c1[keep]).all()
     g = rel.filter([(0, "=", ("col", 1))]).download()
     assert (g[0] == c0[c0 == c1]).all()
-    part, counts = rel.partition(0, 4)
-    cols = part.download()
-    dest = np.array([oracle.partition_of(v, 4) for v in c0])
-    off = 0
-    for d in range(4):
-        assert counts[d] == int((dest == d).sum())
-        assert (cols[0][off:off + counts[d]] == c0[dest == d]).all()  # stable within a destination
-        assert (cols[1][off:off + counts[d]] == c1[dest == d]).all()
-        off += counts[d]
+    for G in (4, 3, 8, 1):  # the power-of-two mask path and the modulo path
+        part, counts = rel.partition(0, G)
+        cols = part.download()
+        dest = np.array([oracle.partition_of(v, G) for v in c0])
+        off = 0
+        for d in range(G):
+            assert counts[d] == int((dest == d).sum())
+            assert (cols[0][off:off + counts[d]] == c0[dest == d]).all()  # stable within a destination
+            assert (cols[1][off:off + counts[d]] == c1[dest == d]).all()
+            off += counts[d]
 
 
 def test_counters(engine):
