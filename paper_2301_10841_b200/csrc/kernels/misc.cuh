@@ -51,7 +51,7 @@ __global__ void k_compact_col(const int32_t* in, const uint32_t* flags, const ui
 // counting sort by destination. Block b owns rows [b*kPartChunk, ...); hist is
 // destination-major (d * nblocks + b) so its exclusive scan gives every
 // (destination, block) its output base.
-constexpr uint32_t kPartChunk = 8192;
+constexpr uint32_t kPartChunk = 2048;  // 8 rounds of 256 rows: more resident blocks hide the per-round latency
 constexpr int PART_WARPS = 8;
 
 struct DevPartCols {
