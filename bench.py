@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Benchmark: Free Join query throughput on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config triangle] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config scale_triangle] [--impl ours|reference]
+
+Default workload: C5 triangle (BASELINE configs[4]: R-MAT 2^27 vertices, 512M
+edges), the config BASELINE.json's 1/2/4/8-GPU metric is quoted on.
 
 A step = one full query execution (COLT build phase + join phase)
 over inputs already resident in HBM. `value` = (input tuples + output tuples)
@@ -11,7 +14,10 @@ For N>1 (torchrun), relations holding the first plan variable are
 hash-partitioned across ranks by an NCCL all-to-all and the rest all-gathered
 (paper_2301_10841_b200/dist.py); the exchange is inside the timed step.
 --impl reference times the CPU restatement of the reference path (oracle/)
-on all host cores over a bounded sample of the same workload.
+over a bounded sample of the same workload; it loads only oracle/ libraries
+(inputs from oracle/gen.cpp, plans from oracle/workload_plans.json).
+--gpus N without torchrun re-launches this script under torch.distributed.run
+with N ranks on 127.0.0.1.
 """
 import argparse
 import json
@@ -36,11 +42,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="triangle")
+    ap.add_argument("--config", default="scale_triangle")
+    ap.add_argument("--small", action="store_true", help="tiny sizes of the config (launcher / harness tests)")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="all-core CPU leg threads (0: every host thread)")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-target-s", type=float, default=30.0)
+    ap.add_argument("--cpu-target-s", type=float, default=20.0)
     ap.add_argument("--backend", default="colt", choices=["colt", "slt", "simple"],
                     help="GHT backend (SPEC.md:286-294): the §5.3 ablation ladder")
     ap.add_argument("--shard", action="store_true",
@@ -57,9 +65,60 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def workload(name):
+SMALL = {"chain": dict(n=20000, domain=30000), "triangle": dict(scale=12, m=30000),
+         "star": dict(nf=50000, dims=(500, 400, 300, 200)), "clique4": dict(scale=12, m=30000),
+         "path5": dict(scale=10, m=8000), "scale_triangle": dict(scale=14, m=100000),
+         "scale_path5": dict(scale=14, m=100000)}
+
+
+def workload(name, small=False):
     from paper_2301_10841_b200 import configs
-    return configs.CONFIGS[name]()
+    return configs.CONFIGS[name](**(SMALL[name] if small else {}))
+
+
+def oracle_workload(name, small=False):
+    """The same config restated on the oracle side (no product library)."""
+    from oracle import workloads as OW
+    return OW.CONFIGS[name](**(SMALL[name] if small else {}))
+
+
+def config_dict(name, params, mode, backend):
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": name, **params, "plan_mode": mode, "backend": backend}
+
+
+def host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    mem = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable"):
+                    mem = int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "mem_available_bytes": mem}
+
+
+def maybe_relaunch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run, N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 class Clocks:
@@ -194,73 +253,148 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------- CPU leg ---
-def _orc_run(w, plan, cols, min_var, T, P, backend="colt"):
+# The CPU restatement of the reference path (oracle/fj_oracle.cpp) on the
+# host cores. A sample = T threads, thread t running first-variable hash
+# partition t of P with its own trie set (one independent trie
+# instance per concurrent execution). The rows of the atoms that hold the
+# first variable are restricted to the sampled partitions before the timed
+# call (the host-side counterpart of the multi-GPU exchange; otherwise every
+# thread would force those atoms' whole roots); atoms without it are whole.
+# P starts large and shrinks 4x while the sample stays short, so a sample is
+# bounded by ~target_s unless one thread's fixed trie build alone exceeds it.
+
+def _np_partition_of(v, nparts):
+    """fj::partition_of (csrc/fj_hash.hpp): fmix64(v ^ 0x5bd1e995) mod nparts."""
+    import numpy as np
+    with np.errstate(over="ignore"):
+        k = v.astype(np.int64).astype(np.uint64) ^ np.uint64(0x5bd1e995)
+        k ^= k >> np.uint64(33)
+        k *= np.uint64(0xff51afd7ed558ccd)
+        k ^= k >> np.uint64(33)
+        k *= np.uint64(0xc4ceb9fe1a85ec53)
+        k ^= k >> np.uint64(33)
+    return k % np.uint64(nparts)
+
+
+def _first_var_atoms(ow):
+    plan = ow.plan
+    fv = plan[0][0][1][0]
+    return fv, [i for i, a in enumerate(ow.query) if fv in a["vars"]]
+
+
+def _restricted_columns(ow, cols, parts, P):
+    import numpy as np
+    fv, atoms = _first_var_atoms(ow)
+    out = list(cols)
+    cache = {}
+    for i in atoms:
+        c = ow.query[i]["vars"].index(fv)
+        key = (id(cols[i][0]), c)
+        if key not in cache:
+            keep = np.isin(_np_partition_of(cols[i][c], P), np.asarray(parts, dtype=np.uint64))
+            cache[key] = [x[keep] for x in cols[i]]
+        out[i] = cache[key]
+    return out
+
+
+def _thread_bytes(ow, cols, frac):
+    """Rough per-thread trie footprint of the oracle (bytes): ~100 B per row of
+    every whole atom (flat map + keys + nodes + offsets), less for restricted ones."""
+    _, atoms = _first_var_atoms(ow)
+    rows = sum(len(c[0]) * (frac if i in atoms else 1.0) for i, c in enumerate(cols))
+    return int(100 * rows) + (64 << 20)
+
+
+def cpu_sample(ow, T, P, cols=None):
+    """One timed oracle sample: T threads, partitions 0..T-1 of P."""
     from oracle import oracle
+    cols = cols if cols is not None else ow.atom_columns()
+    head = ow.head()
+    mv = head.index(ow.min_var) if ow.min_var else -1
+    rc = _restricted_columns(ow, cols, list(range(T)), P) if P > 1 else cols
     t0 = time.perf_counter()
-    r = oracle.execute(w.query, plan, cols, part=0, nparts=P, nthreads=T, min_var=min_var, backend=backend)
-    return time.perf_counter() - t0, r
-
-
-def cpu_plan(w, plan, min_var, T, backend="colt"):
-    """Two-point calibration of the oracle on T threads: t(P) = B + W/P for T of
-    P first-variable partitions (B: per-thread build, W: join work)."""
-    cols = w.atom_columns()
-    t16, _ = _orc_run(w, plan, cols, min_var, T, 16 * T, backend)
-    t4, _ = _orc_run(w, plan, cols, min_var, T, 4 * T, backend)
-    W = max(t4 - t16, 0.0) / (1.0 / (4 * T) - 1.0 / (16 * T))
-    B = max(t16 - W / (16 * T), 0.0)
-    return B, W
-
-
-def cpu_sample(w, plan, min_var, target_s, threads=None, calib=None, backend="colt"):
-    """Time the oracle (CPU restatement of the reference path) on all host
-    threads. Thread t runs first-variable hash partition t of P with its own
-    trie set; P = T is the whole query. P is the smallest
-    multiple of T whose predicted time fits target_s."""
-    T = threads or max(1, min(os.cpu_count() or 1, 64))
-    B, W = calib or cpu_plan(w, plan, min_var, T, backend)
-    P = T
-    while B + W / P > target_s and P < (1 << 16):
-        P *= 2
-    dt, r = _orc_run(w, plan, w.atom_columns(), min_var, T, P, backend)
+    r = oracle.execute(ow.query, ow.plan, rc, part=0, nparts=P, nthreads=T, min_var=mv,
+                       output_mode=ow.output_mode)
+    dt = time.perf_counter() - t0
     frac = T / P
-    tuples = w.input_tuples() * frac + r["count"]
-    what = "the whole query" if P == T else f"{T} of {P} first-variable hash partitions ({frac:.4f} of the query)"
-    return {"value": tuples / dt, "unit": UNIT, "cores": T, "kind": "port",
-            "sample": f"{what}; {T} threads, one independent trie set each"
-                      + ("" if P == T else "; input tuples scaled by the fraction"),
-            "seconds": dt, "sample_output_tuples": r["count"], "calib": (B, W)}
+    units = ow.input_tuples() * frac + (r["count"] if ow.output_mode == "count" else 0)
+    return {"value": units / dt, "seconds": dt, "threads": T, "P": P, "frac": frac, "count": r["count"],
+            "checksum": r["checksum"], "min": r["min"]}
+
+
+def cpu_leg(ow, T, target_s, cols=None):
+    """Adaptive bounded sample on T threads (see the block comment above)."""
+    cols = cols if cols is not None else ow.atom_columns()
+    P = T
+    while P < (1 << 14) and ow.input_tuples() * T / P > 4e6:  # start near 4M input rows per sample
+        P *= 2
+    s = cpu_sample(ow, T, P, cols)
+    while P > T and s["seconds"] < target_s / 5:
+        P //= 4 if P // 4 >= T else P // T
+        s = cpu_sample(ow, T, P, cols)
+    what = "the whole query" if P == T else f"{T} of {P} first-variable hash partitions ({s['frac']:.5f} of the query)"
+    s["sample"] = (f"{what}; {T} thread(s), one independent trie set each (SPEC.md:354); rows of the first-variable"
+                   f" atoms restricted to the sampled partitions before timing; input tuples scaled by the fraction")
+    return s
+
+
+def cpu_baseline(ow, target_s, threads=0, cols=None):
+    """Single-thread (the reference's concurrency model) and
+    all-core figures. The all-core thread count is capped by host memory (each
+    thread holds its own tries)."""
+    info = host_info()
+    cols = cols if cols is not None else ow.atom_columns()
+    one = cpu_leg(ow, 1, target_s, cols)
+    T = threads or max(1, min(os.cpu_count() or 1, 64))
+    capped = ""
+    if info["mem_available_bytes"]:
+        per = _thread_bytes(ow, cols, 1.0 / max(T, 1))
+        tmax = max(1, int(0.6 * info["mem_available_bytes"] // per))
+        if tmax < T:
+            T, capped = tmax, f" (capped from {os.cpu_count()} by host memory: ~{per / 2**30:.1f} GiB of tries per thread)"
+    allc = cpu_leg(ow, T, target_s, cols) if T > 1 else one
+    keep = ("value", "seconds", "threads", "P", "frac", "sample")
+    return {"value": allc["value"], "unit": UNIT, "cores": allc["threads"], "kind": "port",
+            "sample": allc["sample"] + capped,
+            "single_thread": {k: one[k] for k in keep},
+            "all_core": {k: allc[k] for k in keep},
+            "nproc": info["nproc"], "cpu_model": info["cpu_model"],
+            "compiler": "g++ -O3 -march=x86-64-v2, batch 1000, dynamic cover (SPEC.md:502)"}
 
 
 def run_reference(args):
+    """The reference arm: oracle only (inputs oracle/gen.cpp, plan
+    oracle/workload_plans.json); rank 0 runs, other ranks exit."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2301_10841_b200 import plan as P
-    w = workload(args.config)
-    plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
-    head = P.head_variables(w.query)
-    mv = head.index(w.min_var) if w.min_var else -1
-    T = max(1, min(os.cpu_count() or 1, 64))
-    calib = cpu_plan(w, plan, mv, T, args.backend)
-    target = max(1.0, min(60.0, 200.0 / max(1, args.steps + args.warmup)))
+    ow = oracle_workload(args.config, args.small)
+    cols = ow.atom_columns()
+    T = args.cpu_threads or max(1, min(os.cpu_count() or 1, 64))
+    info = host_info()
+    if info["mem_available_bytes"]:
+        T = max(1, min(T, int(0.6 * info["mem_available_bytes"] // _thread_bytes(ow, cols, 1.0 / T))))
+    steps = max(args.steps, 1)
+    target = max(2.0, min(60.0, 240.0 / (steps + args.warmup + 1)))
+    s0 = cpu_leg(ow, T, target, cols)  # fixes P for every step
     for _ in range(args.warmup):
-        cpu_sample(w, plan, mv, target, threads=T, calib=calib, backend=args.backend)
-    vals, secs, last = [], [], None
-    for _ in range(args.steps):
-        last = cpu_sample(w, plan, mv, target, threads=T, calib=calib, backend=args.backend)
-        vals.append(last["value"])
-        secs.append(last["seconds"])
-    v = statistics.median(vals)
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators)",
-            "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "backend": args.backend,
-                       "parallelism": "cpu-threads"},
+        cpu_sample(ow, T, s0["P"], cols)
+    runs = [cpu_sample(ow, T, s0["P"], cols) for _ in range(steps)]
+    v = statistics.median(r["value"] for r in runs)
+    last = runs[-1]
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(r["seconds"] for r in runs),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded generators)",
+            "config": config_dict(ow.name, ow.params, ow.mode, args.backend),
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port",
-                             "sample": last["sample"]},
+            "parallelism": f"cpu-threads x{T}",
+            "result": {"count": last["count"], "checksum": f"{last['checksum']:#018x}",
+                       "min": last["min"], "output_mode": ow.output_mode,
+                       "scope": "whole query" if last["P"] == T else f"partitions 0..{T - 1} of {last['P']}"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": T, "kind": "port", "sample": s0["sample"],
+                             "nproc": info["nproc"], "cpu_model": info["cpu_model"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -271,11 +405,13 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_setup(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     import paper_2301_10841_b200 as fjg
     from paper_2301_10841_b200 import plan as P
 
-    w = workload(args.config)
+    w = workload(args.config, args.small)
     plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
     head = P.head_variables(w.query)
     mv = w.min_var
@@ -357,15 +493,22 @@ def run_ours(args):
         if world > 1 or args.shard:
             e2e = e2e_leg_sharded(sharded, w, mv, args.e2e_steps, flush, world, args.backend)
         else:
+            # return the warm query's tries and relations to the pool first, so the
+            # e2e leg's query reuses that memory instead of holding a second trie set
+            q.close()
+            for r in rels.values():
+                r.close()
             e2e = e2e_leg(fjg, eng, w, stream, mv, args.e2e_steps, flush)
 
-    # ---- CPU baseline (rank 0, N=1) ----
+    # ---- CPU baseline (rank 0, N=1): the oracle on the same bytes ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_sample(w, plan, head.index(mv) if mv else -1, args.cpu_target_s, backend=args.backend)
-            for k in ("seconds", "sample_output_tuples", "calib"):
-                cpu.pop(k, None)
+            from oracle import workloads as OW
+            ow = OW.OWorkload(w.name, w.query, w.atom_rel, w.relations, filters=w.filters, min_var=w.min_var,
+                              params=w.params, output_mode=w.output_mode, mode=w.mode,
+                              plan_override=[[[r, list(vs)] for (r, vs) in node] for node in plan])
+            cpu = cpu_baseline(ow, args.cpu_target_s, args.cpu_threads)
         except Exception as ex:  # the CPU leg must not sink the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
 
@@ -374,11 +517,12 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generators, resident in HBM)",
-            "config": {"workload": w.name, **w.params, "plan_mode": w.mode, "backend": args.backend,
-                       "parallelism": f"hash-partition x{world}" if (world > 1 or args.shard) else "single-gpu",
-                       "l2": "flushed between timed steps (2x126MB write)",
-                       "input_tuples": w.input_tuples(), "output_tuples": out_local if world == 1 else None},
-            "result": {"count": res.count, "checksum": f"{res.checksum:#018x}", "output_mode": w.output_mode},
+            "config": config_dict(w.name, w.params, w.mode, args.backend),
+            "parallelism": f"hash-partition x{world}" if (world > 1 or args.shard) else "single-gpu",
+            "l2": "flushed between timed steps (2x126MB write)",
+            "tuples": {"input": w.input_tuples(), "output": res.count if w.output_mode == "count" else 0},
+            "result": {"count": res.count, "checksum": f"{res.checksum:#018x}", "min": res.min_value,
+                       "output_mode": w.output_mode, "scope": "whole query"},
             "phases_ms": {"build": statistics.mean(r.build_ms for r in results),
                           "join": statistics.mean(r.join_ms for r in results),
                           "last_node_total": statistics.mean(r.last_node_ms for r in results),
@@ -485,6 +629,7 @@ def e2e_leg_sharded(sharded, w, mv, steps, flush, world, backend):
 
 def main():
     args = parse()
+    maybe_relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -3,6 +3,8 @@
   libfjg.so    product: host plan compiler + sm_100a executor + C-ABI (include/fjg.h)
   libfjgen.so  seeded synthetic data generators (bench / tests input)
   oracle/liboracle.so  CPU restatement (test infrastructure only)
+  oracle/libxcheck.so  independent CSR graph counters (test infrastructure only)
+  oracle/libogen.so    independent config input generators (reference arm / tests only)
   oracle/_ref/ref_kat  TupleHash KAT tool compiled from the reference header
                         (only when /root/reference is present)
 """
@@ -19,6 +21,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIBFJG = os.path.join(HERE, "libfjg.so")
 LIBFJGEN = os.path.join(HERE, "libfjgen.so")
 LIBORACLE = os.path.join(ROOT, "oracle", "liboracle.so")
+LIBXCHECK = os.path.join(ROOT, "oracle", "libxcheck.so")
+LIBOGEN = os.path.join(ROOT, "oracle", "libogen.so")
 REF_KAT = os.path.join(ROOT, "oracle", "_ref", "ref_kat")
 
 
@@ -60,6 +64,14 @@ def build_oracle(force=False):
     if force or _stale(LIBORACLE, [src]):
         _run(["g++", "-std=c++17", "-O3", "-march=x86-64-v2", "-fPIC", "-shared", "-pthread", src,
               "-o", LIBORACLE])
+    xsrc = os.path.join(ROOT, "oracle", "xcheck.cpp")
+    if force or _stale(LIBXCHECK, [xsrc]):
+        _run(["g++", "-std=c++17", "-O3", "-march=x86-64-v2", "-fPIC", "-shared", "-pthread", xsrc,
+              "-o", LIBXCHECK])
+    gsrc = os.path.join(ROOT, "oracle", "gen.cpp")
+    if force or _stale(LIBOGEN, [gsrc]):
+        _run(["g++", "-std=c++17", "-O3", "-march=x86-64-v2", "-fPIC", "-shared", "-pthread", gsrc,
+              "-o", LIBOGEN])
     if os.path.isdir("/root/reference/proj/include"):
         kat = os.path.join(ROOT, "oracle", "ref_kat.cpp")
         if force or _stale(REF_KAT, [kat]):

@@ -910,7 +910,9 @@ static void force_root_sorted(fjg_query* q, int t) {
 // Chunk owners for [c0, c1) at `chunk` candidates per chunk (k_chunk_marks + max-scan).
 static void chunk_owners(fjg_query* q, const uint64_t* scan, uint64_t F, uint64_t c0, uint64_t c1, uint32_t chunk) {
   fjg_engine* eng = q->eng;
-  if ((chunk & (chunk - 1)) || c1 - c0 > kLastChunk) throw fj::EngineError("chunk_owners: chunk must be a power of two");
+  if (chunk == 0 || (chunk & (chunk - 1))) throw fj::EngineError("chunk_owners: chunk must be a nonzero power of two");
+  if (c1 < c0 || c1 - c0 > kLastChunk)
+    throw fj::EngineError("chunk_owners: launch range exceeds " + std::to_string(kLastChunk) + " candidates");
   const uint64_t n = (c1 - c0 + chunk - 1) / chunk + 1;
   CK(cudaMemsetAsync(q->chunk_owner, 0, n * 4, eng->stream));
   LAUNCH(eng, k_chunk_marks<<<grid_for(std::min<uint64_t>(F, (c1 - c0 + chunk - 1) / chunk + 1)), 256, 0,
@@ -1591,6 +1593,7 @@ int fjg_relation_from_device(fjg_engine* eng, const int32_t* const* dev_cols, in
       *out = r;
     } else {
       if (ncols <= 0 || ncols > MAXC) throw fj::ValidationError("relation must have 1..8 columns");
+      if (nrows >= (1ull << 32) - 16) throw fj::ValidationError("relations must have fewer than 2^32-16 rows");
       auto* r = new fjg_relation();
       r->eng = eng;
       r->nrows = nrows;
@@ -1654,6 +1657,8 @@ static void partition_into(const fjg_relation* in, int col, int nparts, int32_t*
   if (col < 0 || col >= in->ncols) throw fj::ValidationError("partition column out of range");
   if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
   const uint64_t n = in->nrows;
+  // k_part_count / k_part_scatter keep histograms and offsets in 32 bits
+  if (n >= (1ull << 32) - 16) throw fj::ValidationError("partition: relations must have fewer than 2^32-16 rows");
   if (n == 0) {
     for (int d = 0; d < nparts; ++d) counts[d] = 0;
     return;
@@ -1773,7 +1778,7 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     if (opts) o = *opts;
     if (o.min_var >= (int)q->head.size()) throw fj::ValidationError("min_var out of range");
     uint64_t batch = o.batch_size ? o.batch_size : (1ull << 25);
-    if (batch > kLastChunk) throw fj::ValidationError("batch_size must be <= 2^31");
+    if (batch > kLastChunk) throw fj::ValidationError("batch_size must be <= " + std::to_string(kLastChunk));
     ensure_frontiers(q, batch);
     q->dynamic = o.dynamic_cover != 0;
     q->timing = o.collect_timing != 0;

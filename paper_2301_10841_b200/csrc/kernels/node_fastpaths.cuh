@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
                                                                      uint64_t c1, uint64_t F,
                                                                      const uint32_t* __restrict__ owner,
                                                                      int min_var, DevCounters* ctr) {
+  // a warp leaves at most 31 unfolded survivors plus 32 per candidate of a run
+  static_assert(R >= 1 && (R & (R - 1)) == 0, "k_last_gj_bf: R must be a power of two (chunk_owners)");
+  static_assert(32 * R + 31 < HitQueue<NS>::QC, "k_last_gj_bf: survivor ring too small for R");
   __shared__ HitQueue<NS> Q;
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
   long long acc_min = LLONG_MAX;

@@ -27,6 +27,8 @@ constexpr int TILE = 256;
 #ifndef FJG_LAST_CHUNK_LOG
 #define FJG_LAST_CHUNK_LOG 31  // with ticketed chunks one launch is best (C2 last node 3.20 ms at 2^27, 3.03 at 2^31)
 #endif
+static_assert(FJG_LAST_CHUNK_LOG >= 12 && FJG_LAST_CHUNK_LOG <= 31,
+              "k_chunk_marks uses 32-bit candidate offsets within a launch: FJG_LAST_CHUNK_LOG must be <= 31");
 constexpr uint64_t kLastChunk = 1ull << FJG_LAST_CHUNK_LOG;  // last-node candidates per launch
 __global__ void k_tile_bounds(const uint64_t* __restrict__ scan, uint64_t F, uint64_t c0, uint64_t c1,
                               uint64_t* __restrict__ bounds) {
