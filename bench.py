@@ -210,6 +210,15 @@ def first_node_bytes(plan, query, res):
     return 32 * P + 32 * max(P - n, 0) + 32 * ((seq + 31) // 32)
 
 
+def memo_bytes(res):
+    """Sector model of the memoised chain passes (factorised count): a resolved
+    row streams its carrier value (4 B), probes one root (32 B) and writes its
+    child (4 B); a gathered row streams gid + child (8 B) and gathers one memo
+    entry (one 32 B sector); an initialising row streams cnt + gid (8 B)."""
+    rr, rg, ri = res.memo_rows
+    return 40 * rr + 40 * rg + 8 * ri
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -421,8 +430,9 @@ def run_ours(args):
 
     if world > 1 or args.shard:
         from paper_2301_10841_b200 import dist as D
-        sharded = D.ShardedQuery(eng, w, plan, world, rank)
-        step = lambda timing=False: sharded.execute(min_var=mv, timing=timing,  # noqa: E731
+        comm = D.Comm(eng, world, rank)  # fjg_comm: NCCL, bootstrapped over torch.distributed
+        sharded = D.ShardedQuery(eng, w, plan, comm)
+        step = lambda timing=False: sharded.execute(min_var=mv, timing=timing, batch_size=args.batch,  # noqa: E731
                                                     output_mode=w.output_mode, backend=args.backend)
         input_tuples_local = sharded.input_tuples_local
     else:
@@ -477,9 +487,18 @@ def run_ours(args):
     last_bytes = last_node_bytes(plan, w.query, r0) / max(r0.last_node_launches, 1)
     first_ms = statistics.mean(r.first_node_ms for r in results)
     kernel = "fused last node (k_last_gj_bf for GJ-shaped nodes, k_tail for a Cartesian tail, else k_expand<COUNT>)"
-    if world == 1 and first_ms > statistics.mean(r.last_node_ms for r in results):
+    memo_ms = statistics.mean(r.memo_ms for r in results)
+    cands = [(statistics.mean(r.last_node_ms for r in results), "last")]
+    if world == 1:
+        cands.append((first_ms, "first"))
+    cands.append((memo_ms, "memo"))
+    dom = max(cands)[1]
+    if dom == "first":
         last_ms, last_bytes = first_ms, first_node_bytes(plan, w.query, r0)
         kernel = "node 0 (k_stream_one: single-binding stream node)"
+    elif dom == "memo":
+        last_ms, last_bytes = memo_ms, memo_bytes(r0)
+        kernel = "memoised chain passes (k_memo_init / k_memo_resolve / k_memo_gather), one phase"
     achieved = last_bytes / (last_ms / 1000.0) / 1e9 if last_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
@@ -526,7 +545,7 @@ def run_ours(args):
             "phases_ms": {"build": statistics.mean(r.build_ms for r in results),
                           "join": statistics.mean(r.join_ms for r in results),
                           "last_node_total": statistics.mean(r.last_node_ms for r in results),
-                          "first_node": first_ms,
+                          "first_node": first_ms, "memo": memo_ms,
                           "last_node_per_launch": last_ms, "last_node_launches": r0.last_node_launches},
             "counters": {"probes": r0.probes, "node_probes": r0.node_probes, "node_inputs": r0.node_inputs,
                          "last_node_candidates": r0.last_node_candidates, "maps_built": r0.maps_built,
@@ -590,35 +609,35 @@ def e2e_leg(fjg, eng, w, stream, mv, steps, flush):
 
 
 def e2e_leg_sharded(sharded, w, mv, steps, flush, world, backend):
-    """N-rank end to end: every rank's pinned host slice of each base relation
-    -> H2D into its device slice -> partition + NCCL exchange -> query ->
-    result all-reduce read back to the host (ShardedQuery.execute). Device-timed
-    with CUDA events on the torch stream that issues the copies, the exchange and
-    the reduce (execute returns only after the reduced result is on the host),
-    max over ranks."""
+    """N-rank end to end through the C-ABI: every rank's pinned host slice of
+    each base relation -> fjg_relation_create (H2D) -> fjg_sharded_create ->
+    fjg_execute_multi (partition + NCCL exchange + query + all-reduce, result
+    on the host) -> destroy. Device-timed with CUDA events on the engine
+    stream every call runs on, max over ranks."""
+    import numpy as np
     import torch
-    dev_stream = torch.cuda.current_stream()
-    eng_stream = torch.cuda.ExternalStream(sharded.engine.stream_ptr, device=dev_stream.device)
-    host = {b: [c.cpu().pin_memory() for c in cols] for b, cols in sharded.local.items()}
+    from paper_2301_10841_b200 import dist as D
+    eng = sharded.engine
+    stream = torch.cuda.ExternalStream(eng.stream_ptr, device=torch.device("cuda", eng.device))
+    host = {b: [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in cols]
+            for b, cols in sharded.local.items()}
     h2d = sum(t.numel() * 4 for cols in host.values() for t in cols)
-    # result counters block + the reduced (count, checksum, min) words
-    d2h = 8 * 160 + 8 * 7
+    d2h = 8 * 7  # the reduced (count limbs, checksum halves, min) words
     times = []
     for i in range(steps + 1):
-        torch.cuda.synchronize()
+        eng.sync()
         barrier(world)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(dev_stream)
-        for b, cols in host.items():
-            for d, h in zip(sharded.local[b], cols):
-                d.copy_(h, non_blocking=True)
-        eng_stream.wait_stream(dev_stream)  # the partition kernel runs on the engine stream
-        res = sharded.execute(min_var=mv, output_mode=w.output_mode, backend=backend)
-        e1.record(dev_stream)
-        torch.cuda.synchronize()
-        flush.add_(1)
-        if i > 0:  # first iteration warms the exchange buffers
+        e0.record(stream)
+        sq = D.ShardedQuery(eng, w, sharded.plan, sharded.comm, local=host)
+        res = sq.execute(min_var=mv, output_mode=w.output_mode, backend=backend)
+        e1.record(stream)
+        eng.sync()
+        sq.close()
+        with torch.cuda.stream(stream):
+            flush.add_(1)
+        if i > 0:  # first iteration warms the memory pool
             times.append(e0.elapsed_time(e1) / 1000.0)
     t = allreduce_max(statistics.median(times), world)
     out_local = res.extra.get("local_count", res.count)

@@ -106,6 +106,10 @@ typedef struct {
   uint64_t last_node_launches;
   uint64_t last_node_candidates; /* cover candidates expanded by the last node */
   double first_node_ms;       /* device time of node 0's kernels when node 0 is not the last (if collect_timing) */
+  double memo_ms;             /* device time of the memoised chain passes (factorised count, if collect_timing) */
+  uint64_t memo_rows_resolved;/* rows whose fresh-atom roots were probed once (k_memo_resolve) */
+  uint64_t memo_rows_gathered;/* rows folded by the memo passes (k_memo_gather) */
+  uint64_t memo_rows_init;    /* level-0 positions scanned to initialise memo groups (k_memo_init) */
   uint32_t kernel_launches;   /* kernels this library launched for the call */
   uint32_t host_syncs;
 } fjg_result;
@@ -180,6 +184,54 @@ int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_rela
  * buffers of an NCCL all-to-all. */
 int fjg_relation_partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_dev_cols,
                                 uint64_t* counts);
+
+/* ---- multi-GPU execution (north_star (c)) ----
+ * The reference is single-threaded with reentrant, disjoint contexts
+ * (SPEC.md:354, :447); these calls run one such context per GPU and combine
+ * them. One fjg_engine + fjg_comm per rank (process or thread). NCCL is loaded
+ * on first use (dlopen of libnccl.so.2; FJG_NCCL_LIB overrides the path). */
+#define FJG_COMM_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+#define FJG_MAX_VIEWS 16
+typedef struct fjg_comm fjg_comm;
+typedef struct fjg_sharded fjg_sharded;
+/* ncclGetUniqueId: rank 0 creates the id; the caller ships the bytes to every
+ * rank over any channel (MPI, a TCP store, a file). */
+int fjg_comm_unique_id(void* id_out);
+/* ncclCommInitRank on the engine's device; collectives run on the engine's stream. */
+int fjg_comm_create(fjg_engine* eng, const void* id, int nranks, int rank, fjg_comm** out);
+int fjg_comm_size(const fjg_comm* comm);
+int fjg_comm_rank(const fjg_comm* comm);
+void fjg_comm_destroy(fjg_comm* comm);
+/* A query sharded on its plan's first variable. local_bases: this rank's slice
+ * of every base relation (filtered already; caller-owned, kept alive, contents
+ * may change between executions); atom_base[a]: base of query atom a (renamed
+ * self-joins share one); first_var_col[a]: column of the plan's first variable
+ * in atom a, or -1 when the atom does not hold it (then the base is replicated
+ * on every rank). query_json / plan_json as fjg_query_create. */
+int fjg_sharded_create(fjg_comm* comm, const char* query_json, const char* plan_json,
+                       fjg_relation* const* local_bases, int nbases, const int* atom_base,
+                       const int* first_var_col, int natoms, fjg_sharded** out);
+typedef struct {
+  uint64_t local_count_lo, local_count_hi, local_checksum; /* this rank's share */
+  uint64_t bytes_sent, bytes_received;                     /* NCCL payload, peers only */
+  uint64_t view_rows[FJG_MAX_VIEWS];                       /* rows held after the exchange */
+  int32_t nviews;
+  int32_t pad_;
+  double exchange_ms, reduce_ms;                           /* if collect_timing */
+} fjg_multi_info;
+/* fjg_execute across the communicator: partition kernel -> one metadata
+ * all-gather -> grouped ncclSend/ncclRecv (all-to-all of the partitioned
+ * views, all-gather of the replicated ones) -> local execution ->
+ * ncclAllReduce of (count, checksum, MIN). `out` holds the GLOBAL count /
+ * checksum / MIN and this rank's stats; `info` (optional) the local share and
+ * exchange figures. Collective: every rank must call it. Count and
+ * factorised-count modes (enumerate is single-GPU). */
+int fjg_execute_multi(fjg_sharded* sq, const fjg_exec_options* opts, fjg_result* out, fjg_multi_info* info);
+void fjg_sharded_destroy(fjg_sharded* sq);
+/* test hook: receive layout of an exchange from gathered metadata
+ * meta[src][view][dst]: recv_off[view][src], recv_rows[view]. */
+int fjg_exchange_layout(const uint64_t* meta, int nviews, int nranks, int rank, const int* partitioned,
+                        uint64_t* recv_off, uint64_t* recv_rows);
 
 /* ---- queries: build phase + join phase ----
  * query_json: {"query":[{"rel":..,"vars":[..]},..], "head": [..] (optional:

@@ -57,8 +57,21 @@ class Result(C.Structure):
                 ("build_ms", C.c_double), ("join_ms", C.c_double), ("last_node_ms", C.c_double),
                 ("last_node_launches", C.c_uint64), ("last_node_candidates", C.c_uint64),
                 ("first_node_ms", C.c_double),
+                ("memo_ms", C.c_double), ("memo_rows_resolved", C.c_uint64), ("memo_rows_gathered", C.c_uint64),
+                ("memo_rows_init", C.c_uint64),
                 ("kernel_launches", C.c_uint32),
                 ("host_syncs", C.c_uint32)]
+
+
+MAX_VIEWS = 16
+COMM_ID_BYTES = 128
+
+
+class MultiInfo(C.Structure):
+    _fields_ = [("local_count_lo", C.c_uint64), ("local_count_hi", C.c_uint64), ("local_checksum", C.c_uint64),
+                ("bytes_sent", C.c_uint64), ("bytes_received", C.c_uint64),
+                ("view_rows", C.c_uint64 * MAX_VIEWS), ("nviews", C.c_int32), ("pad_", C.c_int32),
+                ("exchange_ms", C.c_double), ("reduce_ms", C.c_double)]
 
 
 class Predicate(C.Structure):
@@ -99,6 +112,16 @@ def _load():
         "fjg_device_tuple_hash": (I, [P, P, I, U64, P]),
         "fjg_host_tuple_hash": (U64, [P, I]),
         "fjg_parse_csv": (I, [C.c_char_p, I, P, U64, C.POINTER(U64)]),
+        "fjg_comm_unique_id": (I, [P]),
+        "fjg_comm_create": (I, [P, P, I, I, C.POINTER(P)]),
+        "fjg_comm_size": (I, [P]),
+        "fjg_comm_rank": (I, [P]),
+        "fjg_comm_destroy": (None, [P]),
+        "fjg_sharded_create": (I, [P, C.c_char_p, C.c_char_p, C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I,
+                                   C.POINTER(P)]),
+        "fjg_execute_multi": (I, [P, C.POINTER(ExecOptions), C.POINTER(Result), C.POINTER(MultiInfo)]),
+        "fjg_sharded_destroy": (None, [P]),
+        "fjg_exchange_layout": (I, [P, I, I, I, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -116,7 +139,9 @@ EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_o
             "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition",
             "fjg_relation_partition_into", "fjg_query_create",
             "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_output_relation", "fjg_query_destroy",
-            "fjg_device_tuple_hash", "fjg_host_tuple_hash", "fjg_parse_csv"]
+            "fjg_device_tuple_hash", "fjg_host_tuple_hash", "fjg_parse_csv", "fjg_comm_unique_id", "fjg_comm_create",
+            "fjg_comm_size", "fjg_comm_rank", "fjg_comm_destroy", "fjg_sharded_create", "fjg_execute_multi",
+            "fjg_sharded_destroy", "fjg_exchange_layout"]
 
 
 def check(rc):

@@ -47,12 +47,12 @@ def _srcs(*names):
 def build_product(force=False):
     kdir = os.path.join(CSRC, "kernels")
     deps = _srcs("engine.cu", "engine.cuh", "capi.cpp", "fj_plan.cpp", "fj_plan.hpp", "fj_json.hpp",
-                 "fj_hash.hpp", "fj_errors.hpp") + [os.path.join(ROOT, "include", "fjg.h")] + \
+                 "fj_hash.hpp", "fj_errors.hpp", "multi.cuh") + [os.path.join(ROOT, "include", "fjg.h")] + \
         [os.path.join(kdir, f) for f in sorted(os.listdir(kdir)) if f.endswith(".cuh")]
     if force or _stale(LIBFJG, deps):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
               "-diag-suppress", "128",
-              *_srcs("engine.cu", "capi.cpp", "fj_plan.cpp"), "-o", LIBFJG])
+              *_srcs("engine.cu", "capi.cpp", "fj_plan.cpp"), "-ldl", "-o", LIBFJG])
     gdeps = _srcs("datagen.cpp", "datagen_dev.cu", "rmat.hpp")
     if force or _stale(LIBFJGEN, gdeps):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-Xcompiler", "-fPIC,-pthread,-march=x86-64-v2", "-shared",

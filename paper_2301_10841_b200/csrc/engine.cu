@@ -270,7 +270,8 @@ struct fjg_query {
   std::vector<MemoPass> memo_passes;    // for nodes K-1 .. k* (index j - k*)
   std::vector<unsigned long long*> memo;  // per chain node: 2n u64 (lo, hi)
   std::vector<uint64_t> memo_n;
-  std::map<int, uint32_t*> owner;       // per carrier trie: group start of each level-0 position
+  std::map<int, uint32_t*> gid;         // per chain trie: group index + 1 of each level-0 position
+  std::vector<int> memo_resolve_of;     // pass -> pass whose resolved child / coef arrays it reuses
   KNode memo_top{};                     // node k*-1 aggregating mult * memo[child]
   int stop_node = -1;
   int gj_x[MAXN];  // per node: the GJ fast-path variable, or -1
@@ -287,7 +288,8 @@ struct fjg_query {
   std::vector<cudaEvent_t> events;
   std::vector<std::pair<int, int>> marks;  // (event index, phase) ; phase<0 = start
   size_t ev_used = 0;
-  double phase_ms[4] = {0, 0, 0, 0};       // 0 force (build), 1 node kernels, 2 last node, 3 node 0 (not last)
+  double phase_ms[5] = {0, 0, 0, 0, 0};  // 0 force (build), 1 node kernels, 2 last node, 3 node 0 (not last), 4 memo
+  uint64_t memo_rows[3] = {0, 0, 0};     // rows resolved / gathered / initialised by the memo passes
   double build_ms = 0, join_ms = 0, last_ms = 0, first_ms = 0;
   uint64_t last_launches = 0, last_candidates = 0;
   uint64_t node_inputs[MAXN] = {0};
@@ -765,17 +767,55 @@ static void prepare_chain(fjg_query* q) {
   q->memo_passes = passes;
   q->memo.resize(passes.size());
   q->memo_n.resize(passes.size());
-  for (size_t i = 0; i < passes.size(); ++i) {
-    const int j = start + (int)i;
+  auto gid_of = [&](int trie) {
+    if (!q->gid.count(trie))
+      q->gid[trie] = (uint32_t*)q->alloc(std::max<uint64_t>(q->tries[trie].dev.n, 1) * 4);
+    return q->gid[trie];
+  };
+  std::vector<std::string> sig(passes.size());
+  q->memo_resolve_of.assign(passes.size(), -1);
+  // passes run from the last chain node down: the first to run resolves
+  for (int i = (int)passes.size() - 1; i >= 0; --i) {
+    const int j = start + i;
     int cidx, nx0;
     std::vector<int> fr0;
     device_chain_node(q, j, cidx, fr0, nx0);
     const KSub& C = q->knodes[j].sub[cidx];
-    q->memo_n[i] = passes[i].n;
-    q->memo[i] = (unsigned long long*)q->alloc(std::max<uint64_t>(passes[i].n, 1) * 16);
-    if (!q->owner.count(C.trie)) q->owner[C.trie] = (uint32_t*)q->alloc(std::max<uint64_t>(passes[i].n, 1) * 4);
-    q->memo_passes[i].owner = q->owner[C.trie];
-    q->memo_passes[i].memo_out = q->memo[i];
+    MemoPass& M = q->memo_passes[i];
+    q->memo_n[i] = M.n;
+    q->memo[i] = (unsigned long long*)q->alloc(std::max<uint64_t>(M.n, 1) * 16);
+    M.gid = gid_of(C.trie);
+    M.cnt = q->tries[C.trie].dev.lev[0].cnt;
+    M.memo_out = q->memo[i];
+    M.cont_x = -1;
+    M.has_coef = 0;
+    // rows resolve to the same children in every pass with the same carrier
+    // column(s) and fresh atoms (the C5 5-path: E2..E5 are one physical trie)
+    std::string sg = std::to_string(C.trie);
+    for (int t = 0; t < M.cnv; ++t) sg += ":" + std::to_string((uintptr_t)M.cvals[t]);
+    for (int x = 0; x < M.nfresh; ++x) {
+      const KSub& X = M.fresh[x];
+      if (M.cont[x]) {
+        M.cont_x = x;
+        M.gid_next = gid_of(X.trie);
+      } else {
+        M.has_coef = 1;
+      }
+      sg += "|" + std::to_string((uintptr_t)X.table) + "," + std::to_string(X.nv) + "," + std::to_string(M.cont[x]);
+      for (int t = 0; t < X.nv; ++t) sg += "," + std::to_string(M.cpos[x][t]);
+    }
+    sig[i] = sg;
+    for (int k = (int)passes.size() - 1; k > i; --k)
+      if (sig[k] == sg && q->memo_resolve_of[k] < 0 && q->memo_passes[k].nfresh > 0) {
+        q->memo_resolve_of[i] = k;
+        M.child = q->memo_passes[k].child;
+        M.coef = q->memo_passes[k].coef;
+        break;
+      }
+    if (q->memo_resolve_of[i] < 0 && M.nfresh > 0) {
+      if (M.cont_x >= 0) M.child = (uint32_t*)q->alloc(std::max<uint64_t>(M.n, 1) * 4);
+      if (M.has_coef) M.coef = (uint64_t*)q->alloc(std::max<uint64_t>(M.n, 1) * 8);
+    }
   }
   for (size_t i = 0; i + 1 < passes.size(); ++i) q->memo_passes[i].memo_next = q->memo[i + 1];
   // the aggregating top node
@@ -785,6 +825,7 @@ static void prepare_chain(fjg_query* q) {
   q->memo_top = q->knodes[start - 1];
   q->memo_top.memo = q->memo[0];
   q->memo_top.memo_atom = q->knodes[start].sub[c].atom;
+  q->memo_top.memo_gid = q->memo_passes[0].gid;
 }
 
 // (Re)allocate per-node frontier buffers for a candidate capacity `cap`.
@@ -845,6 +886,7 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
     q->memo_top = q->knodes[q->chain_start - 1];
     q->memo_top.memo = q->memo[0];
     q->memo_top.memo_atom = c;
+    q->memo_top.memo_gid = q->memo_passes[0].gid;
   }
 }
 
@@ -1408,7 +1450,8 @@ static void reset_query(fjg_query* q) {
   for (size_t t = 0; t < q->tries.size(); ++t) z.root_region[t] = P.root_region[t];
   q->maps_built = q->forces = q->rows_forced = 0;
   q->build_ms = q->join_ms = q->last_ms = 0;
-  q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = q->phase_ms[3] = 0;
+  q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = q->phase_ms[3] = q->phase_ms[4] = 0;
+  q->memo_rows[0] = q->memo_rows[1] = q->memo_rows[2] = 0;
   q->last_launches = q->last_candidates = 0;
   q->dev_tail_node = -1;
   for (int k = 0; k < MAXN; ++k) q->node_inputs[k] = 0;
@@ -1426,24 +1469,33 @@ static void run_memo_passes(fjg_query* q) {
   for (int t : tries)
     if (!q->tries[t].root_forced) roots.push_back(t);
   force_roots(q, roots);
-  for (auto& [t, own] : q->owner) {
+  for (auto& [t, gid] : q->gid) {
     const uint64_t n = q->tries[t].rel->nrows;
     if (!n) continue;
-    LAUNCH(eng, k_group_starts<<<grid_for(n), 256, 0, eng->stream>>>(q->tries[t].dev.lev[0].cnt, n, own));
+    LAUNCH(eng, k_start_flags<<<grid_for(n), 256, 0, eng->stream>>>(q->tries[t].dev.lev[0].cnt, n, gid));
     size_t bytes = 0;
-    CK(cub::DeviceScan::InclusiveScan(nullptr, bytes, own, own, MaxOp(), (int64_t)n));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, gid, gid, (int64_t)n));
     void* tmp = eng->pool->alloc(bytes);
-    CK(cub::DeviceScan::InclusiveScan(tmp, bytes, own, own, MaxOp(), (int64_t)n, eng->stream));
+    CK(cub::DeviceScan::InclusiveSum(tmp, bytes, gid, gid, (int64_t)n, eng->stream));
     ++eng->launches;
     eng->pool->free(tmp);
   }
   q->mark(eng->stream, -1);
+  const unsigned grid = grid_for(std::max<uint64_t>(q->max_n, 1), 256, eng->num_sms * 16);
   for (int i = (int)q->memo_passes.size() - 1; i >= 0; --i) {
     const MemoPass& M = q->memo_passes[i];
-    CK(cudaMemsetAsync(q->memo[i], 0, std::max<uint64_t>(M.n, 1) * 16, eng->stream));
-    if (M.n) LAUNCH(eng, k_memo_pass<<<grid_for(M.n, 256, eng->num_sms * 16), 256, 0, eng->stream>>>(M));
+    if (!M.n) continue;
+    LAUNCH(eng, k_memo_init<<<grid, 256, 0, eng->stream>>>(M));
+    q->memo_rows[2] += M.n;
+    if (M.nfresh == 0) continue;  // every row counts 1: the group sizes, written by k_memo_init
+    if (q->memo_resolve_of[i] < 0) {
+      LAUNCH(eng, k_memo_resolve<<<grid, 256, 0, eng->stream>>>(M));
+      q->memo_rows[0] += M.n;
+    }
+    LAUNCH(eng, k_memo_gather<<<grid, 256, 0, eng->stream>>>(M));
+    q->memo_rows[1] += M.n;
   }
-  q->mark(eng->stream, 1);
+  q->mark(eng->stream, 4);
 }
 
 // SLT / SIMPLE backends: force level 0 of every trie (SLT)
@@ -1494,7 +1546,7 @@ static void execute_once(fjg_query* q, int mode) {
   if (q->dev_tail_node >= 0) q->last_candidates += q->h_ctr->tail_inputs[q->dev_tail_node];
   q->resolve_marks();
   q->build_ms = q->phase_ms[0];
-  q->join_ms = q->phase_ms[1] + q->phase_ms[2] + q->phase_ms[3];
+  q->join_ms = q->phase_ms[1] + q->phase_ms[2] + q->phase_ms[3] + q->phase_ms[4];
   q->last_ms = q->phase_ms[2];
   q->first_ms = q->phase_ms[3];
 }
@@ -1652,7 +1704,10 @@ int fjg_relation_filter(const fjg_relation* in, const fjg_predicate* preds, int 
 // Stable hash-partition of `in` on column `col` (counting sort by destination,
 // one host sync): rows for destination d land in out_cols[c][base_d ...) in
 // their original order.
-static void partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_cols, uint64_t* counts) {
+// Hash-partition `in` on `col` into out_cols (grouped by destination, stable
+// within one), asynchronously on the engine stream: d_tot[0..nparts] receives
+// the cumulative row offsets of the destinations (u32, on the device).
+static void partition_async(const fjg_relation* in, int col, int nparts, int32_t* const* out_cols, uint32_t* d_tot) {
   fjg_engine* eng = in->eng;
   if (col < 0 || col >= in->ncols) throw fj::ValidationError("partition column out of range");
   if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
@@ -1660,14 +1715,13 @@ static void partition_into(const fjg_relation* in, int col, int nparts, int32_t*
   // k_part_count / k_part_scatter keep histograms and offsets in 32 bits
   if (n >= (1ull << 32) - 16) throw fj::ValidationError("partition: relations must have fewer than 2^32-16 rows");
   if (n == 0) {
-    for (int d = 0; d < nparts; ++d) counts[d] = 0;
+    CK(cudaMemsetAsync(d_tot, 0, (size_t)(nparts + 1) * 4, eng->stream));
     return;
   }
   const uint32_t nblocks = (uint32_t)((n + kPartChunk - 1) / kPartChunk);
   const uint64_t nh = (uint64_t)nparts * nblocks;
   uint32_t* hist = (uint32_t*)eng->pool->alloc((nh + 1) * 4);
   uint32_t* offs = (uint32_t*)eng->pool->alloc((nh + 1) * 4);
-  uint32_t* tot = (uint32_t*)eng->pool->alloc((nparts + 1) * 4);
   size_t bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, offs, (int64_t)(nh + 1)));
   void* tmp = eng->pool->alloc(bytes);
@@ -1684,16 +1738,24 @@ static void partition_into(const fjg_relation* in, int col, int nparts, int32_t*
     pc.out[c] = out_cols[c];
   }
   LAUNCH(eng, k_part_scatter<<<nblocks, 256, smem, eng->stream>>>(pc, col, n, nparts, nblocks, offs));
-  LAUNCH(eng, k_part_totals<<<grid_for(nparts + 1), 256, 0, eng->stream>>>(offs, nparts, nblocks, tot));
+  LAUNCH(eng, k_part_totals<<<grid_for(nparts + 1), 256, 0, eng->stream>>>(offs, nparts, nblocks, d_tot));
+  // stream-ordered pool: later allocations on this stream run after these kernels
+  eng->pool->free(hist);
+  eng->pool->free(offs);
+  eng->pool->free(tmp);
+}
+
+static void partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_cols, uint64_t* counts) {
+  fjg_engine* eng = in->eng;
+  if (nparts < 1 || nparts > 1024) throw fj::ValidationError("nparts must be 1..1024");
+  uint32_t* tot = (uint32_t*)eng->pool->alloc((nparts + 1) * 4);
+  partition_async(in, col, nparts, out_cols, tot);
   std::vector<uint32_t> h(nparts + 1);
   CK(cudaMemcpyAsync(h.data(), tot, (nparts + 1) * 4, cudaMemcpyDeviceToHost, eng->stream));
   CK(cudaStreamSynchronize(eng->stream));
   ++eng->syncs;
   for (int d = 0; d < nparts; ++d) counts[d] = h[d + 1] - h[d];
-  eng->pool->free(hist);
-  eng->pool->free(offs);
   eng->pool->free(tot);
-  eng->pool->free(tmp);
 }
 
 int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_relation** out_rel, uint64_t* counts) {
@@ -1833,6 +1895,10 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     r.last_node_launches = q->last_launches;
     r.last_node_candidates = q->last_candidates;
     r.first_node_ms = q->first_ms;
+    r.memo_ms = q->phase_ms[4];
+    r.memo_rows_resolved = q->memo_rows[0];
+    r.memo_rows_gathered = q->memo_rows[1];
+    r.memo_rows_init = q->memo_rows[2];
     r.kernel_launches = eng->launches - l0;
     r.host_syncs = eng->syncs - s0;
     *out = r;
@@ -1895,3 +1961,5 @@ int fjg_device_tuple_hash(fjg_engine* eng, const int64_t* host_vals, int arity, 
 }
 
 }  // extern "C"
+
+#include "multi.cuh"

@@ -155,27 +155,39 @@ struct KNode {
   uint8_t* chosen;
   uint64_t* m;
   uint64_t* scan;
-  const unsigned long long* memo;  // memoised chain count per child start (u128 as lo,hi), or null
+  const unsigned long long* memo;  // memoised chain count per level-0 group (u128 as lo,hi), or null
+  const uint32_t* memo_gid;        // group index + 1 of every level-0 position of memo_atom's trie
   int memo_atom;                   // atom whose child subtrie indexes `memo`
   KSub sub[MAXS];
 };
 
-// One bottom-up pass of the memoised chain count (DESIGN.md §3): for every
-// row of the carrier trie's level-0 domain, probe the fresh atoms' roots with
-// the row's values and add prod(leaf lengths) * memo_next[child] to the row's
-// group.
+// One bottom-up pass of the memoised chain count (DESIGN.md §5): for every
+// row of the carrier trie's level-0 domain, the fresh atoms' roots are probed
+// with the row's values (k_memo_resolve: the continuing atom's child group and
+// the product of the other atoms' leaf lengths, cached per row and shared by
+// every pass with the same carrier and fresh atoms), then k_memo_gather adds
+// coef * memo_next[child] into the row's group. Groups are numbered densely
+// (gid = inclusive count of group starts), so memo arrays hold one u128 per
+// level-0 key.
 struct MemoPass {
   uint64_t n;
-  const uint32_t* owner;       // group start of every position (level 0)
+  const uint32_t* gid;         // group index + 1 of every level-0 position (carrier trie)
+  const uint32_t* cnt;         // carrier trie level-0 cnt (nonzero at group starts)
   const int32_t* cvals[MAXK];  // carrier's variables at level-0 positions
   int cnv;
   int nfresh;
+  int cont_x;                  // index of the fresh atom continuing the chain, or -1
+  int has_coef;                // some fresh atom is a leaf (its length multiplies)
   int cont[MAXS];              // fresh atom continues the chain (uses memo_next)
   int8_t cpos[MAXS][MAXK];     // key var t of fresh x = carrier var cpos[x][t]
   KSub fresh[MAXS];
+  const uint32_t* gid_next;    // gid of the continuing atom's trie
+  uint32_t* child;             // per row: gid of the continuing atom's child, or kMemoMiss
+  uint64_t* coef;              // per row: product of leaf lengths (has_coef), 0 on a miss
   const unsigned long long* memo_next;
   unsigned long long* memo_out;
 };
+constexpr uint32_t kMemoMiss = 0xffffffffu;
 
 struct DevCounters {
   uint64_t count_lo, count_hi, checksum;

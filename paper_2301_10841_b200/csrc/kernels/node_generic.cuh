@@ -303,9 +303,9 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
         if (min_var >= 0) acc_min = min(acc_min, (long long)st.get(min_var));
       } else if (MODE == EXPAND_MEMO) {
         // memoised chain suffix: this binding contributes mult * count(child of the carrier)
-        const uint32_t q = st.cpd(N.memo_atom);
+        const uint64_t g = __ldg(N.memo_gid + st.cpd(N.memo_atom)) - 1u;
         const unsigned __int128 mv =
-            ((unsigned __int128)N.memo[2ull * q + 1] << 64) | (unsigned __int128)N.memo[2ull * q];
+            ((unsigned __int128)N.memo[2ull * g + 1] << 64) | (unsigned __int128)N.memo[2ull * g];
         const unsigned __int128 c = mv * mult + (((unsigned __int128)acc_hi << 64) | acc_lo);
         acc_lo = (uint64_t)c;
         acc_hi = (uint64_t)(c >> 64);

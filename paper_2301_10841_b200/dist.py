@@ -1,27 +1,25 @@
 """Multi-GPU Free Join: hash-partitioning on the first plan variable
-(BASELINE.json north_star (c)).
+(BASELINE.json north_star (c)), through the C-ABI (include/fjg.h
+fjg_comm_* / fjg_sharded_* / fjg_execute_multi, csrc/multi.cuh).
 
-One process per GPU (torch.distributed, NCCL over NVLink). Every rank starts
-with a contiguous 1/G slice of each base relation (the distributed-load model).
-Per step:
-  1. views whose atom holds the plan's first variable v are hash-partitioned
-     on v's column (fjg_relation_partition_into, fj::partition_of = fmix64 mod
-     G) and exchanged with an all-to-all (uneven splits, counts exchanged
-     first);
-  2. every other view is all-gathered (padded to the largest slice, then
-     compacted);
-  3. each rank runs the single-GPU executor on (its shard of v) x (replicas);
-     outputs are disjoint by v, so count = sum, checksum = sum mod 2^64,
-     MIN = min, reduced with one all-reduce.
-The exchange primitives take an `ops` object (array allocation + the
-partition function) so the same exchange logic runs on CPU tensors under gloo
-in tests/test_dist.py; the product path uses `DeviceOps` (the CUDA partition
-kernel, NCCL).
+One process per GPU. Every rank holds a contiguous 1/G slice of each base
+relation (the distributed-load model). fjg_execute_multi then, on the engine
+stream: hash-partitions the views holding the plan's first variable
+(fj::partition_of = fmix64 mod G), all-gathers the size metadata once,
+exchanges every view in one NCCL group (all-to-all of the partitioned views,
+all-gather of the replicated ones), runs the single-GPU executor on the rows
+it holds, and all-reduces (count, checksum, MIN): outputs are disjoint by the
+first variable. torch.distributed is used here only to ship the 128-byte NCCL
+id from rank 0 to the other ranks (any channel would do).
 """
-import torch
-import torch.distributed as dist
+import ctypes as C
+import json
 
-MASK32 = (1 << 32) - 1
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+from .engine import ExecResult, _OUT, _BACKEND
 
 
 def first_variable(plan):
@@ -47,175 +45,114 @@ def local_slice(n, world, rank):
     return lo, hi
 
 
-def _reuse(out, i, n, ops):
-    """out[i] if it exists with n rows (persistent exchange buffers), else a new buffer."""
-    if out is not None and i < len(out) and out[i].numel() == n:
-        return out[i]
-    return ops.empty(n)
+class Comm:
+    """fjg_comm: one NCCL communicator per rank on the engine's device."""
 
+    def __init__(self, engine, world, rank, uid=None, group=None):
+        if uid is None:
+            buf = C.create_string_buffer(_capi.COMM_ID_BYTES)
+            if rank == 0:
+                check(lib.fjg_comm_unique_id(buf))
+            if world > 1:
+                import torch.distributed as dist
+                obj = [bytes(buf.raw) if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                buf = C.create_string_buffer(obj[0], _capi.COMM_ID_BYTES)
+            uid = buf
+        h = C.c_void_p()
+        check(lib.fjg_comm_create(engine._h, uid, int(world), int(rank), C.byref(h)))
+        self._h, self.engine, self.world, self.rank = h, engine, world, rank
 
-def all_to_all_partitioned(grouped, counts, recv_counts, ops, group=None, out=None):
-    """Rows already grouped by destination rank (partition_of(row[col]),
-    `counts` per destination) -> this rank's rows, `recv_counts` per source
-    (written into `out` when its buffers have the right sizes)."""
-    res = []
-    for i, g in enumerate(grouped):
-        o = _reuse(out, i, sum(recv_counts), ops)
-        dist.all_to_all_single(o, g, output_split_sizes=recv_counts, input_split_sizes=counts, group=group)
-        res.append(o)
-    return res
+    def close(self):
+        if self._h:
+            lib.fjg_comm_destroy(self._h)
+            self._h = None
 
-
-def all_gather_rows(cols, sizes, world, ops, group=None, out=None):
-    """Every rank's rows of `cols` (`sizes` = each rank's row count),
-    concatenated in rank order."""
-    n = cols[0].numel() if cols else 0
-    m = max(sizes) if sizes else 0
-    res = []
-    for i, c in enumerate(cols):
-        if world == 1:
-            o = _reuse(out, i, n, ops)
-            o.copy_(c)
-            res.append(o)
-            continue
-        pad = ops.empty(m)
-        if n:
-            pad[:n].copy_(c)
-        buf = ops.empty(m * world)
-        dist.all_gather_into_tensor(buf, pad, group=group)
-        o = _reuse(out, i, sum(sizes), ops)
-        off = 0
-        for r in range(world):
-            o[off: off + sizes[r]].copy_(buf[r * m: r * m + sizes[r]])
-            off += sizes[r]
-        res.append(o)
-    return res
-
-
-def reduce_results(count, checksum, minv, device, group=None):
-    """count (python int, < 2^127), checksum (u64), minv (int or None) -> global.
-    One all-gather of every rank's (count limbs, checksum halves, min) and a
-    host-side sum / min: one collective and one device->host read per step."""
-    INT64_MAX = (1 << 63) - 1
-    parts = [count & MASK32, (count >> 32) & MASK32, (count >> 64) & MASK32, count >> 96,
-             checksum & MASK32, checksum >> 32, INT64_MAX if minv is None else int(minv)]
-    t = torch.tensor(parts, dtype=torch.int64, device=device)
-    world = dist.get_world_size(group)
-    if world == 1:
-        rows = [t.tolist()]
-    else:
-        allp = torch.empty(world * len(parts), dtype=torch.int64, device=device)
-        dist.all_gather_into_tensor(allp, t, group=group)
-        rows = allp.reshape(world, len(parts)).tolist()
-    v = [sum(int(r[i]) for r in rows) for i in range(6)]
-    total = v[0] + (v[1] << 32) + (v[2] << 64) + (v[3] << 96)
-    cs = (v[4] + (v[5] << 32)) & ((1 << 64) - 1)
-    mv = min(int(r[6]) for r in rows)
-    return total, cs, (None if mv == INT64_MAX else mv)
-
-
-def exchange(relations, views, world, rank, ops, group=None, bufs=None):
-    """relations: base -> list of local-slice column tensors. Returns
-    view -> list of column tensors held by this rank after the exchange
-    (reusing `bufs`, the previous step's result, when sizes match).
-
-    Every partitioned view is grouped by destination first; then ONE
-    all-gather carries all size metadata (per partitioned view the counts
-    per destination, per replicated view the local row count), so a step
-    pays one metadata round trip however many views it exchanges."""
-    order = sorted(set(views), key=lambda v: (v[0], -1 if v[1] is None else v[1]))
-    meta, grouped = [], {}
-    for view in order:
-        base, col = view
-        cols = relations[base]
-        if col is None:
-            meta.append([cols[0].numel() if cols else 0] * world)
-        else:
-            g, counts = ops.partition(cols, col, world)
-            grouped[view] = (g, counts)
-            meta.append(list(counts))
-    nv = len(order)
-    mine = torch.tensor(meta, dtype=torch.int64, device=ops.device).reshape(-1)
-    if world == 1:
-        allm = mine
-    else:
-        allm = torch.empty(world * nv * world, dtype=torch.int64, device=ops.device)
-        dist.all_gather_into_tensor(allm, mine, group=group)
-    M = allm.reshape(world, nv, world).tolist()  # M[source rank][view][destination]
-    out = {}
-    for vi, view in enumerate(order):
-        base, col = view
-        prev = bufs.get(view) if bufs else None
-        if col is None:
-            sizes = [int(M[r][vi][0]) for r in range(world)]
-            out[view] = all_gather_rows(relations[base], sizes, world, ops, group, prev)
-        else:
-            g, counts = grouped[view]
-            rc = [int(M[r][vi][rank]) for r in range(world)]
-            out[view] = all_to_all_partitioned(g, counts, rc, ops, group, prev)
-    return out
-
-
-class DeviceOps:
-    """Product ops: CUDA tensors, the libfjg partition kernel."""
-
-    def __init__(self, engine):
-        self.engine = engine
-        self.device = torch.device("cuda", engine.device)
-        self._send = {}  # (column pointers, key column) -> persistent send buffers
-
-    def empty(self, n):
-        return torch.empty(n, dtype=torch.int32, device=self.device)
-
-    def partition(self, cols, col, world):
-        key = (tuple(c.data_ptr() for c in cols), col)
-        if key not in self._send:
-            self._send[key] = (self.engine.relation_from_torch(cols), [self.empty(cols[0].numel()) for _ in cols])
-        rel, grouped = self._send[key]
-        counts = rel.partition_into(col, world, [g.data_ptr() for g in grouped])
-        return grouped, counts
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class ShardedQuery:
-    """A workload executed across `world` ranks (one GPU each)."""
+    """A workload executed across the ranks of `comm` (one GPU each)."""
 
-    def __init__(self, engine, w, plan, world, rank, group=None):
+    def __init__(self, engine, w, plan, comm, local=None):
+        """local: optional base -> this rank's columns (numpy arrays, or host
+        torch tensors copied from their pointers); default: slice w's relations."""
         from . import plan as P
-        self.engine, self.w, self.plan = engine, w, plan
-        self.world, self.rank, self.group = world, rank, group
-        self.ops = DeviceOps(engine)
+        self.engine, self.w, self.plan, self.comm = engine, w, plan, comm
+        world, rank = comm.world, comm.rank
         self.fv, self.views = atom_views(w.query, w.atom_rel, plan)
         self.head = P.head_variables(w.query)
+        bases = sorted(set(w.atom_rel))
         # this rank's slice of every (filtered) base relation, resident on the device
         self.local = {}
-        for base, cols in w.filtered().items():
-            lo, hi = local_slice(len(cols[0]), world, rank)
-            self.local[base] = [torch.from_numpy(c[lo:hi].copy()).to(self.ops.device) for c in cols]
+        self._rels = {}
+        for base in bases:
+            cols = (local or {}).get(base)
+            if cols is None:
+                full = w.filtered()[base]
+                lo, hi = local_slice(len(full[0]), world, rank)
+                cols = [np.ascontiguousarray(c[lo:hi]) for c in full]
+            if hasattr(cols[0], "data_ptr"):  # host tensors (e.g. pinned): H2D from their pointers
+                self._rels[base] = engine.relation_host_ptrs([c.data_ptr() for c in cols], cols[0].numel())
+            else:
+                self._rels[base] = engine.relation(cols)
+            self.local[base] = cols
         self.input_tuples_local = sum(len(w.relations[b][0]) for b in w.atom_rel) / world
-        self._q = None
-        self._eng_stream = torch.cuda.ExternalStream(engine.stream_ptr, device=self.ops.device)
+        arr = (C.c_void_p * len(bases))(*[self._rels[b]._h.value for b in bases])
+        ab = (C.c_int * len(w.atom_rel))(*[bases.index(b) for b in w.atom_rel])
+        fc = (C.c_int * len(w.atom_rel))(*[-1 if c is None else c for (_, c) in self.views])
+        h = C.c_void_p()
+        check(lib.fjg_sharded_create(comm._h, json.dumps({"query": w.query}).encode(),
+                                     json.dumps([[[r, list(v)] for (r, v) in n] for n in plan]).encode(),
+                                     arr, len(bases), ab, fc, len(w.atom_rel), C.byref(h)))
+        self._h = h
 
-    def _bind(self, held):
-        rels = {v: self.engine.relation_from_torch(cols) for v, cols in held.items()}
-        self._held = held
-        self._rels = rels
-        self._q = self.engine.query({"query": self.w.query}, self.plan, [rels[v] for v in self.views])
+    def execute(self, min_var=None, timing=False, batch_size=0, dynamic_cover=True, output_mode="count",
+                backend="colt"):
+        o = _capi.ExecOptions()
+        o.batch_size = int(batch_size)
+        o.dynamic_cover = int(bool(dynamic_cover))
+        o.output_mode = _OUT[output_mode]
+        o.min_var = self.head.index(min_var) if isinstance(min_var, str) else (-1 if min_var is None else min_var)
+        o.collect_timing = int(bool(timing))
+        o.backend = _BACKEND[backend]
+        r = _capi.Result()
+        info = _capi.MultiInfo()
+        check(lib.fjg_execute_multi(self._h, C.byref(o), C.byref(r), C.byref(info)))
+        n = r.num_nodes
+        res = ExecResult(
+            count=(r.count_hi << 64) | r.count_lo, checksum=r.checksum,
+            min_value=r.min_value if r.has_min else None, probes=r.probes, probe_misses=r.probe_misses,
+            node_body_entries=list(r.node_body_entries[:n]), node_probes=list(r.node_probes[:n]),
+            node_inputs=list(r.node_inputs[:n]), maps_built=r.maps_built, keys_inserted=r.keys_inserted,
+            forces=r.forces, rows_forced=r.rows_forced, build_ms=r.build_ms, join_ms=r.join_ms,
+            last_node_ms=r.last_node_ms, last_node_launches=r.last_node_launches,
+            last_node_candidates=r.last_node_candidates, first_node_ms=r.first_node_ms,
+            memo_ms=r.memo_ms, memo_rows=(r.memo_rows_resolved, r.memo_rows_gathered, r.memo_rows_init),
+            kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
+        res.extra["local_count"] = (info.local_count_hi << 64) | info.local_count_lo
+        res.extra["local_checksum"] = info.local_checksum
+        res.extra["bytes_sent"] = info.bytes_sent
+        res.extra["bytes_received"] = info.bytes_received
+        res.extra["view_rows"] = list(info.view_rows[:info.nviews])
+        res.extra["exchange_ms"] = info.exchange_ms
+        res.extra["reduce_ms"] = info.reduce_ms
+        return res
 
-    def execute(self, min_var=None, timing=False, **kw):
-        prev = getattr(self, "_held", None)
-        held = exchange(self.local, self.views, self.world, self.rank, self.ops, self.group, prev)
-        # the executor runs on the engine stream: order it after the exchange
-        # on the device (no host synchronisation)
-        self._eng_stream.wait_stream(torch.cuda.current_stream(self.ops.device))
-        same = prev is not None and all(h is p for v in held for h, p in zip(held[v], prev[v]))
-        # zero-copy relations over the exchanged buffers, bound once: every step
-        # exchanges the same local slices, so the buffers' contents never change
-        # under the bound query (relations are immutable, SPEC.md:86; the query
-        # caches per-relation facts such as a sorted root's key width)
-        if self._q is None or not same:
-            self._bind(held)
-        r = self._q.execute(min_var=min_var, timing=timing, **kw)
-        r.extra["local_count"] = r.count
-        r.count, r.checksum, r.min_value = reduce_results(r.count, r.checksum, r.min_value, self.ops.device,
-                                                          self.group)
-        return r
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.fjg_sharded_destroy(self._h)
+            self._h = None
+        for r in self._rels.values():
+            r.close()
+        self._rels = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -45,6 +45,8 @@ class ExecResult:
     kernel_launches: int
     host_syncs: int
     output_rows: int = 0
+    memo_ms: float = 0.0
+    memo_rows: tuple = (0, 0, 0)  # resolved / gathered / initialised rows of the memo passes
     extra: dict = field(default_factory=dict)
 
 
@@ -245,6 +247,8 @@ class Query:
                           rows_forced=r.rows_forced, build_ms=r.build_ms, join_ms=r.join_ms,
                           last_node_ms=r.last_node_ms, last_node_launches=r.last_node_launches,
                           last_node_candidates=r.last_node_candidates, first_node_ms=r.first_node_ms,
+                          memo_ms=r.memo_ms, memo_rows=(r.memo_rows_resolved, r.memo_rows_gathered,
+                                                        r.memo_rows_init),
                           kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
 
     def enumerate(self, batch_size=0, dynamic_cover=True, min_var=None, backend="colt"):

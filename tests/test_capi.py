@@ -31,11 +31,12 @@ def test_struct_sizes_match_header():
     # fjg_result / fjg_exec_options layouts are mirrored in _capi.py
     assert C.sizeof(_capi.ExecOptions) == 32
     assert C.sizeof(_capi.Predicate) == 24
-    assert C.sizeof(_capi.Result) == 8 * 3 + 8 + 4 + 4 + 8 * 3 + 8 * 32 * 3 + 8 * 4 + 8 * 3 + 8 * 2 + 8 + 4 * 2
+    assert C.sizeof(_capi.Result) == 8 * 3 + 8 + 4 + 4 + 8 * 3 + 8 * 32 * 3 + 8 * 4 + 8 * 3 + 8 * 2 + 8 + 8 * 4 + 4 * 2
+    assert C.sizeof(_capi.MultiInfo) == 8 * 5 + 8 * 16 + 4 * 2 + 8 * 2
 
 
 def test_error_codes():
-    assert _capi.lib.fjg_abi_version() == 3
+    assert _capi.lib.fjg_abi_version() == 4
     with pytest.raises(_capi.ParseError):
         P.compile_plan("{not json", "free")
     with pytest.raises(_capi.ValidationError):

@@ -1,8 +1,11 @@
-"""Multi-GPU exchange logic (paper_2301_10841_b200/dist.py) on CPU: world_size
-2 and 3 over gloo. Each rank starts with a contiguous slice of every base
-relation, runs the first-variable partition all-to-all + all-gather, executes
-its shard with the oracle, and the all-reduced result must equal the
-single-process oracle (count, checksum, MIN)."""
+"""Multi-GPU exchange protocol on CPU: world_size 2 and 3 over gloo with the
+protocol model (tests/dist_model.py, the steps of fjg_execute_multi). Each rank
+starts with a contiguous slice of every base relation, runs the first-variable
+partition all-to-all + all-gather, executes its shard with the oracle, and the
+reduced result must equal the single-process oracle (count, checksum, MIN).
+The product's C++ receive layout (fjg_exchange_layout) is checked against the
+model; the product path itself (NCCL) runs at world 1 on the GPU, through
+ctypes and from a compiled C++ caller."""
 import os
 import socket
 
@@ -12,8 +15,10 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import dist_model as D
 from oracle import oracle
-from paper_2301_10841_b200 import configs, dist as D, plan as P
+from paper_2301_10841_b200 import configs, plan as P
+from paper_2301_10841_b200 import dist as PD
 
 
 def np_partition_of(v, nparts):
@@ -59,10 +64,10 @@ def _worker(rank, world, port, name, q):
              "star": lambda: configs.star(nf=60000, dims=(2000, 3000, 800, 100)),
              "clique4": lambda: configs.clique4(scale=10, m=6000)}[name]()
         plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
-        fv, views = D.atom_views(w.query, w.atom_rel, plan)
+        fv, views = PD.atom_views(w.query, w.atom_rel, plan)
         local = {}
         for base, cols in w.filtered().items():
-            lo, hi = D.local_slice(len(cols[0]), world, rank)
+            lo, hi = PD.local_slice(len(cols[0]), world, rank)
             local[base] = [torch.from_numpy(c[lo:hi].copy()) for c in cols]
         held = D.exchange(local, views, world, rank, CpuOps())
         cols = [[c.numpy() for c in held[v]] for v in views]
@@ -110,51 +115,90 @@ def test_np_partition_matches_oracle():
         assert np_partition_of(v, n).tolist() == [oracle.partition_of(int(x), n) for x in v]
 
 
+def _gloo_one_rank(fn):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        return fn()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_reduce_results_carries():
-    # 128-bit count and u64 checksum recombination without a process group
+    """The model's reduction at one rank: a count above 2^64 survives the 32-bit
+    limb split, the checksum wraps mod 2^64, a missing MIN stays None."""
     big = (1 << 70) + 12345
-    parts = [big & D.MASK32, (big >> 32) & D.MASK32, (big >> 64) & D.MASK32, big >> 96]
-    assert parts[0] + (parts[1] << 32) + (parts[2] << 64) + (parts[3] << 96) == big
+    total, cs, mn = _gloo_one_rank(lambda: D.reduce_results(big, (1 << 64) - 3, None, torch.device("cpu")))
+    assert total == big and cs == (1 << 64) - 3 and mn is None
+    total, cs, mn = _gloo_one_rank(lambda: D.reduce_results(7, 5, -9, torch.device("cpu")))
+    assert (total, cs, mn) == (7, 5, -9)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_exchange_layout_matches_model(world):
+    """The C++ receive layout of fjg_execute_multi (fjg_exchange_layout) equals
+    the protocol model's for random metadata, every rank, mixed view kinds."""
+    import ctypes as C
+    from paper_2301_10841_b200 import _capi
+    rng = np.random.default_rng(world)
+    nviews = 3
+    part = [1, 0, 1]
+    M = rng.integers(0, 1000, size=(world, nviews, world)).astype(np.uint64)
+    for src in range(world):
+        M[src, 1, :] = M[src, 1, 0]  # a replicated view repeats its row count
+    for rank in range(world):
+        off = np.zeros(nviews * world, dtype=np.uint64)
+        rows = np.zeros(nviews, dtype=np.uint64)
+        pv = (C.c_int * nviews)(*part)
+        _capi.check(_capi.lib.fjg_exchange_layout(M.ctypes.data, nviews, world, rank, pv, off.ctypes.data,
+                                                  rows.ctypes.data))
+        moff, mrows = D.recv_layout(M.tolist(), part, rank)
+        assert off.reshape(nviews, world).tolist() == moff and rows.tolist() == mrows
 
 
 _NCCL_SCRIPT = r'''
 import json, os, sys
 sys.path.insert(0, os.getcwd())
-import torch, torch.distributed as dist
+import torch
 import paper_2301_10841_b200 as fjg
 from paper_2301_10841_b200 import configs, dist as D, plan as P
-torch.cuda.set_device(0)
-dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
 out = {}
+eng = fjg.Engine(0)
+comm = D.Comm(eng, 1, 0)
 for name, w in (("triangle", configs.triangle(scale=11, m=8000, seed=5)),
-                ("star", configs.star(nf=60000, dims=(2000, 3000, 800, 100)))):
+                ("star", configs.star(nf=60000, dims=(2000, 3000, 800, 100))),
+                ("path5", configs.path5(scale=10, m=6000))):
     plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
-    eng = fjg.Engine(0)
-    sq = D.ShardedQuery(eng, w, plan, 1, 0)
-    rs = [sq.execute(min_var=w.min_var, output_mode=w.output_mode) for _ in range(2)]
-    out[name] = [[r.count, r.checksum, r.min_value] for r in rs]
-dist.destroy_process_group()
+    sq = D.ShardedQuery(eng, w, plan, comm)
+    rs = [sq.execute(min_var=w.min_var, output_mode=w.output_mode, timing=True) for _ in range(2)]
+    out[name] = [[r.count, r.checksum, r.min_value, r.extra["local_count"]] for r in rs]
+    sq.close()
+comm.close()
 print(json.dumps(out))
 '''
 
 
 @pytest.mark.gpu
 def test_sharded_nccl_one_rank_matches_oracle(tmp_path):
-    """The product exchange (CUDA partition kernel + NCCL all-to-all /
-    all-gather, one all-gather of the size metadata, all-gathered result
-    reduction) at world 1, run twice (persistent buffers reused), vs the oracle."""
+    """The product multi-GPU path (fjg_execute_multi: CUDA partition kernel,
+    NCCL metadata all-gather, grouped send/recv, all-reduce) at world 1, run
+    twice (persistent buffers reused), vs the oracle."""
     import subprocess
     import sys
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    p = subprocess.run([sys.executable, "-c", _NCCL_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+    p = subprocess.run([sys.executable, "-c", _NCCL_SCRIPT], cwd=root, capture_output=True, text=True,
                        timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     got = __import__("json").loads(p.stdout.strip().splitlines()[-1])
     for name, w in (("triangle", configs.triangle(scale=11, m=8000, seed=5)),
-                    ("star", configs.star(nf=60000, dims=(2000, 3000, 800, 100)))):
+                    ("star", configs.star(nf=60000, dims=(2000, 3000, 800, 100))),
+                    ("path5", configs.path5(scale=10, m=6000))):
         plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
         head = P.head_variables(w.query)
-        ref = oracle.execute(w.query, plan, w.atom_columns(), min_var=head.index(w.min_var) if w.min_var else -1)
-        for c, cs, mn in got[name]:
-            assert (c, cs, mn) == (ref["count"], ref["checksum"], ref["min"]), name
+        ref = oracle.execute(w.query, plan, w.atom_columns(), min_var=head.index(w.min_var) if w.min_var else -1,
+                             output_mode=w.output_mode)
+        for c, cs, mn, lc in got[name]:
+            assert (c, mn) == (ref["count"], ref["min"]) and lc == c, name
+            if w.output_mode == "count":
+                assert cs == ref["checksum"], name

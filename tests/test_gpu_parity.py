@@ -258,6 +258,31 @@ def test_path5_memoised_count(engine, scale, m):
         assert fjg.run_workload(engine, w)[0].count == res.count
 
 
+def test_scale_triangle_full_vs_golden(own_engine):
+    """C5 triangle at full size (R-MAT 2^27, 512M edges, ~4.1e9 triangles):
+    count and checksum vs tests/golden/configs_full.json["scale_triangle"]
+    (tests/golden/make_xcheck_goldens.py: the independent CSR counter, which
+    agrees with the oracle on C2, C4 and on C5 partition 0 of 256)."""
+    g = _golden("scale_triangle")
+    w = configs.scale_triangle()
+    assert w.params == g["params"]
+    res, q, plan, rels = fjg.run_workload(own_engine, w)
+    assert [[[r, list(v)] for (r, v) in n] for n in plan] == g["plan"]
+    assert res.count == g["count"]
+    assert f"{res.checksum:#018x}" == g["checksum"]
+
+
+def test_scale_path5_exact_vs_golden(own_engine):
+    """C5 5-path at full size: the device memoised count equals the exact walk
+    count 1^T A^5 1 (xcheck SpMV residues mod 2^64 and two 61-bit primes,
+    combined by CRT) committed in configs_full.json["scale_path5"]."""
+    g = _golden("scale_path5")
+    w = configs.scale_path5()
+    assert w.params == g["params"]
+    res, q, plan, rels = fjg.run_workload(own_engine, w)
+    assert res.count == g["count"]
+
+
 def test_scale_path5_residues(own_engine):
     """C5 5-path at full size (~4.9e21 walks, > 2^64): the device memoised count
     agrees with 1^T A^5 1 computed independently by torch index_add SpMV,
