@@ -307,11 +307,12 @@ def _restricted_columns(ow, cols, parts, P):
 
 
 def _thread_bytes(ow, cols, frac):
-    """Rough per-thread trie footprint of the oracle (bytes): ~100 B per row of
-    every whole atom (flat map + keys + nodes + offsets), less for restricted ones."""
+    """Per-thread trie footprint of the oracle (bytes): measured ~64 B per row of
+    every whole atom (C5: 33 GB for the 512M-row E2 trie, one thread, maxrss
+    41.7 GB with the inputs), the restricted atoms scaled by the fraction."""
     _, atoms = _first_var_atoms(ow)
     rows = sum(len(c[0]) * (frac if i in atoms else 1.0) for i, c in enumerate(cols))
-    return int(100 * rows) + (64 << 20)
+    return int(64 * rows) + (256 << 20)
 
 
 def cpu_sample(ow, T, P, cols=None):
@@ -332,16 +333,17 @@ def cpu_sample(ow, T, P, cols=None):
 
 
 def cpu_leg(ow, T, target_s, cols=None):
-    """Adaptive bounded sample on T threads (see the block comment above)."""
+    """Adaptive bounded sample on T threads: P starts at 4096*T first-variable
+    partitions and shrinks 4x while a sample takes < target_s/5, so the final
+    sample is ~target_s unless one thread's fixed trie build alone is longer
+    (C5: ~150 s to build the 512M-row E2 trie on one core)."""
     cols = cols if cols is not None else ow.atom_columns()
-    P = T
-    while P < (1 << 14) and ow.input_tuples() * T / P > 4e6:  # start near 4M input rows per sample
-        P *= 2
+    P = 4096 * T
     s = cpu_sample(ow, T, P, cols)
     while P > T and s["seconds"] < target_s / 5:
-        P //= 4 if P // 4 >= T else P // T
+        P = max(T, P // 4)
         s = cpu_sample(ow, T, P, cols)
-    what = "the whole query" if P == T else f"{T} of {P} first-variable hash partitions ({s['frac']:.5f} of the query)"
+    what = "the whole query" if P == T else f"{T} of {P} first-variable hash partitions ({s['frac']:.6f} of the query)"
     s["sample"] = (f"{what}; {T} thread(s), one independent trie set each (SPEC.md:354); rows of the first-variable"
                    f" atoms restricted to the sampled partitions before timing; input tuples scaled by the fraction")
     return s
@@ -385,15 +387,21 @@ def run_reference(args):
     if info["mem_available_bytes"]:
         T = max(1, min(T, int(0.6 * info["mem_available_bytes"] // _thread_bytes(ow, cols, 1.0 / T))))
     steps = max(args.steps, 1)
-    target = max(2.0, min(60.0, 240.0 / (steps + args.warmup + 1)))
-    s0 = cpu_leg(ow, T, target, cols)  # fixes P for every step
-    for _ in range(args.warmup):
+    budget = 300.0  # seconds for the whole arm
+    target = max(2.0, min(60.0, budget / (steps + args.warmup + 2)))
+    s0 = cpu_leg(ow, T, target, cols)  # fixes P for every step (and warms the host caches)
+    # a sample cannot be shorter than one thread's trie build: when K + W samples
+    # of that size exceed the budget, run as many as fit (at least one)
+    warm = args.warmup if s0["seconds"] * (steps + args.warmup) <= budget else 0
+    steps = steps if s0["seconds"] * (steps + warm) <= budget else max(1, int(budget // max(s0["seconds"], 1e-9)))
+    for _ in range(warm):
         cpu_sample(ow, T, s0["P"], cols)
     runs = [cpu_sample(ow, T, s0["P"], cols) for _ in range(steps)]
     v = statistics.median(r["value"] for r in runs)
     last = runs[-1]
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(r["seconds"] for r in runs),
+            "warmup": warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": 1000 * statistics.median(r["seconds"] for r in runs),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (seeded generators)",
             "config": config_dict(ow.name, ow.params, ow.mode, args.backend),

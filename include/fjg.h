@@ -55,6 +55,7 @@ extern "C" {
 #define FJG_CMP_GE 5
 
 #define FJG_MAX_NODES 32
+#define FJG_MAX_ATOMS 16
 
 typedef struct fjg_engine fjg_engine;
 typedef struct fjg_relation fjg_relation;
@@ -110,6 +111,11 @@ typedef struct {
   uint64_t memo_rows_resolved;/* rows whose fresh-atom roots were probed once (k_memo_resolve) */
   uint64_t memo_rows_gathered;/* rows folded by the memo passes (k_memo_gather) */
   uint64_t memo_rows_init;    /* level-0 positions scanned to initialise memo groups (k_memo_init) */
+  /* TrieStats of each atom's physical trie (renamed
+   * self-join atoms that share one report the same values): subtries forced
+   * into maps, and bit l set iff some map was built at schema level l. */
+  uint64_t atom_maps_built[FJG_MAX_ATOMS];
+  uint32_t atom_levels_forced[FJG_MAX_ATOMS];
   uint32_t kernel_launches;   /* kernels this library launched for the call */
   uint32_t host_syncs;
 } fjg_result;

@@ -12,6 +12,7 @@ LIB_PATH = os.environ.get("FJG_LIB") or os.path.join(_HERE, "libfjg.so")
 
 FJG_OK, FJG_E_IO, FJG_E_PARSE, FJG_E_VALIDATION, FJG_E_RESOURCE, FJG_E_ENGINE = range(6)
 MAX_NODES = 32
+MAX_ATOMS = 16
 
 
 # error.hpp:9-33 categories, mirrored as Python exceptions
@@ -59,6 +60,7 @@ class Result(C.Structure):
                 ("first_node_ms", C.c_double),
                 ("memo_ms", C.c_double), ("memo_rows_resolved", C.c_uint64), ("memo_rows_gathered", C.c_uint64),
                 ("memo_rows_init", C.c_uint64),
+                ("atom_maps_built", C.c_uint64 * MAX_ATOMS), ("atom_levels_forced", C.c_uint32 * MAX_ATOMS),
                 ("kernel_launches", C.c_uint32),
                 ("host_syncs", C.c_uint32)]
 

@@ -261,6 +261,16 @@ struct fjg_query {
   uint64_t out_rows = 0;
   // per-execute stats
   uint64_t maps_built = 0, forces = 0, rows_forced = 0;
+  // TrieStats per physical trie: subtries forced, levels with a forced map
+  uint64_t trie_maps[MAXA] = {};
+  uint32_t trie_levels[MAXA] = {};
+  void count_maps(int t, int l, uint64_t n) {
+    maps_built += n;
+    if (t >= 0 && t < MAXA) {
+      trie_maps[t] += n;
+      if (n) trie_levels[t] |= 1u << l;
+    }
+  }
   bool dynamic = true;
   uint64_t batch = 0;
   int min_var = -1;
@@ -283,6 +293,12 @@ struct fjg_query {
   uint64_t* bounds = nullptr;  // tile -> first entry (load-balanced search)
   uint64_t bounds_cap = 0;
   uint32_t* chunk_owner = nullptr;  // chunk -> owning entry (GJ last node)
+  // GJ last node in probe-region order (FJG_GJ_SORT): keys, binding permutation, permuted m / scan
+  uint32_t *sort_keys = nullptr, *sort_keys2 = nullptr, *sort_vals = nullptr, *perm = nullptr;
+  uint64_t *m_perm = nullptr, *scan_perm = nullptr;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  uint64_t sort_cap = 0;
   int backend = FJG_BACKEND_COLT;
   // non-blocking phase timer: event pairs resolved after the final sync
   std::vector<cudaEvent_t> events;
@@ -944,7 +960,7 @@ static void force_root_sorted(fjg_query* q, int t) {
   if (pay < 0) LAUNCH(eng, k_root_gather<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, srows));
   q->mark(eng->stream, 0);
   q->forces += 1;
-  q->maps_built += 1;
+  q->count_maps(t, 0, 1);
   q->rows_forced += n;
   T.lev[0].dirty = true;
 }
@@ -1028,7 +1044,7 @@ static void force_roots(fjg_query* q, const std::vector<int>& ts) {
         off += n;
         upper = std::max<uint64_t>(upper, n);
         q->forces += 1;
-        q->maps_built += 1;
+        q->count_maps(t, 0, 1);
         q->rows_forced += n;
         T.lev[0].dirty = true;
       }
@@ -1081,11 +1097,59 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
   }
   launch_force_batch(q, B, upper, single, T.lev[l].multi);
   q->forces += 1;
-  q->maps_built += single ? 1 : count;
+  q->count_maps(t, l, single ? 1 : count);
   q->rows_forced += single ? len0 : 0;
   T.lev[l].dirty = true;
 }
 
+
+#ifndef FJG_GJ_SORT
+#define FJG_GJ_SORT 1
+#endif
+// Order the F bindings entering GJ last node k by the region their probed
+// subatom is probed in (k_probe_keys + radix sort), and build the permuted
+// candidate scan. Returns the permutation (null when not worth it: the probed
+// trie fits in L2, so probes hit L2 in any order).
+static const uint32_t* probe_region_order(fjg_query* q, int k, const KNode& KN, uint64_t F, uint64_t*& scan_out) {
+  fjg_engine* eng = q->eng;
+  const DevNode& N = q->nodes[k];
+  if (!FJG_GJ_SORT || N.nsub != 2 || F < 2) return nullptr;
+  uint64_t rows = 0;
+  for (int s = 0; s < 2; ++s) rows = std::max<uint64_t>(rows, q->tries[KN.sub[s].trie].dev.n);
+  // probed tables (32 B / row) that fit in L2 gain nothing; FJG_GJ_SORT_MIN_ROWS
+  // (environment) moves the threshold (tests force the path on small inputs)
+  static const char* env = getenv("FJG_GJ_SORT_MIN_ROWS");
+  const uint64_t min_rows = env ? strtoull(env, nullptr, 10) : 2ull * 126 * (1ull << 20) / 32;
+  if (rows < min_rows) return nullptr;
+  if (F > q->sort_cap) {
+    q->sort_keys = (uint32_t*)q->alloc(F * 4);
+    q->sort_keys2 = (uint32_t*)q->alloc(F * 4);
+    q->sort_vals = (uint32_t*)q->alloc(F * 4);
+    q->perm = (uint32_t*)q->alloc(F * 4);
+    q->m_perm = (uint64_t*)q->alloc(F * 8);
+    q->scan_perm = (uint64_t*)q->alloc(F * 8);
+    size_t b1 = 0, b2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, q->sort_keys, q->sort_keys2, q->sort_vals, q->perm, (int64_t)F));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, b2, q->m_perm, q->scan_perm, (int64_t)F));
+    q->sort_tmp_bytes = std::max(b1, b2);
+    q->sort_tmp = q->alloc(q->sort_tmp_bytes);
+    q->sort_cap = F;
+  }
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < rows) ++bits;
+  const unsigned g = grid_for(F, 256, eng->num_sms * 16);
+  LAUNCH(eng, k_probe_keys<2><<<g, 256, 0, eng->stream>>>(KN, F, q->sort_keys, q->sort_vals));
+  size_t bytes = q->sort_tmp_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(q->sort_tmp, bytes, q->sort_keys, q->sort_keys2, q->sort_vals, q->perm,
+                                     (int64_t)F, 0, bits, eng->stream));
+  ++eng->launches;
+  LAUNCH(eng, k_gather_m<<<g, 256, 0, eng->stream>>>(N.m, q->perm, F, q->m_perm));
+  bytes = q->sort_tmp_bytes;
+  CK(cub::DeviceScan::InclusiveSum(q->sort_tmp, bytes, q->m_perm, q->scan_perm, (int64_t)F, eng->stream));
+  ++eng->launches;
+  scan_out = q->scan_perm;
+  return q->perm;
+}
 
 static void run_node(fjg_query* q, int k, uint64_t F, int mode);
 
@@ -1275,13 +1339,19 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (M == 0) return;
   if (is_last) {
     q->mark(eng->stream, -1);
+    const bool gj_any = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
+                        FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
+    uint64_t* gscan = N.scan;
+    const uint32_t* perm = gj_any ? probe_region_order(q, k, KN, F, gscan) : nullptr;
+    KNode KP = KN;
+    KP.scan = gscan;
     for (uint64_t c0 = 0; c0 < M; c0 += kLastChunk) {
       const uint64_t c1 = std::min(M, c0 + kLastChunk);
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
       const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
                            FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
       if (gj_fast) {
-        chunk_owners(q, N.scan, F, c0, c1, 32 * FJG_GJ_R);
+        chunk_owners(q, gscan, F, c0, c1, 32 * FJG_GJ_R);
         if (FJG_GJ_TICKET)
           CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, ticket), 0, 8, eng->stream));
       }
@@ -1298,17 +1368,17 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const unsigned gi = grid_for(c1 - c0, TILE * FJG_GJ_R, eng->num_sms * 8);
         if (N.nsub == 2 && W8 == 4)
-          LAUNCH(eng, (k_last_gj_bf<2, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
-                                                                                q->min_var, q->d_ctr)));
+          LAUNCH(eng, (k_last_gj_bf<2, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                perm, q->min_var, q->d_ctr)));
         else if (N.nsub == 2)
-          LAUNCH(eng, (k_last_gj_bf<2, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
-                                                                                q->min_var, q->d_ctr)));
+          LAUNCH(eng, (k_last_gj_bf<2, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                perm, q->min_var, q->d_ctr)));
         else if (W8 == 4)
-          LAUNCH(eng, (k_last_gj_bf<3, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
-                                                                                q->min_var, q->d_ctr)));
+          LAUNCH(eng, (k_last_gj_bf<3, FJG_GJ_R, 4><<<gi, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                perm, q->min_var, q->d_ctr)));
         else
-          LAUNCH(eng, (k_last_gj_bf<3, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KN, c0, c1, F, q->chunk_owner,
-                                                                                q->min_var, q->d_ctr)));
+          LAUNCH(eng, (k_last_gj_bf<3, FJG_GJ_R, 8><<<gi, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                perm, q->min_var, q->d_ctr)));
       } else if (q->gj_x[k] >= 0 && mode == EXPAND_COUNT) {
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const int ns = N.nsub;
@@ -1449,6 +1519,10 @@ static void reset_query(fjg_query* q) {
   z.minv = LLONG_MAX;
   for (size_t t = 0; t < q->tries.size(); ++t) z.root_region[t] = P.root_region[t];
   q->maps_built = q->forces = q->rows_forced = 0;
+  for (int t = 0; t < MAXA; ++t) {
+    q->trie_maps[t] = 0;
+    q->trie_levels[t] = 0;
+  }
   q->build_ms = q->join_ms = q->last_ms = 0;
   q->phase_ms[0] = q->phase_ms[1] = q->phase_ms[2] = q->phase_ms[3] = q->phase_ms[4] = 0;
   q->memo_rows[0] = q->memo_rows[1] = q->memo_rows[2] = 0;
@@ -1899,6 +1973,11 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     r.memo_rows_resolved = q->memo_rows[0];
     r.memo_rows_gathered = q->memo_rows[1];
     r.memo_rows_init = q->memo_rows[2];
+    for (size_t a = 0; a < q->atoms.size() && a < FJG_MAX_ATOMS; ++a) {
+      const int t = q->atoms[a].trie;
+      r.atom_maps_built[a] = (t >= 0 && t < MAXA) ? q->trie_maps[t] : 0;
+      r.atom_levels_forced[a] = (t >= 0 && t < MAXA) ? q->trie_levels[t] : 0;
+    }
     r.kernel_launches = eng->launches - l0;
     r.host_syncs = eng->syncs - s0;
     *out = r;

@@ -168,9 +168,12 @@ __device__ __forceinline__ uint32_t bucket_match(const Bucket8& a, uint32_t kw, 
 // Per-warp queue of surviving candidates (binding, cover value, probe
 // results): the checksum / multiplicity fold runs on full batches of 32 with
 // every lane busy instead of on the ~7% of lanes that hit (C2).
+#ifndef FJG_GJ_QC
+#define FJG_GJ_QC 128  // survivor ring slots per warp (power of two, > 32 * FJG_GJ_R + 31)
+#endif
 template <int NS>
 struct HitQueue {  // per-warp ring buffers
-  static constexpr int NW = TILE / 32, QC = 128;
+  static constexpr int NW = TILE / 32, QC = FJG_GJ_QC;
   int32_t x[NW][QC];
   uint32_t e[NW][QC];
   uint32_t q[NS - 1][NW][QC];
@@ -191,6 +194,7 @@ template <int NS, int R, int W>
 __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MINB3) k_last_gj_bf(const __grid_constant__ KNode N, uint64_t c0,
                                                                      uint64_t c1, uint64_t F,
                                                                      const uint32_t* __restrict__ owner,
+                                                                     const uint32_t* __restrict__ perm,
                                                                      int min_var, DevCounters* ctr) {
   // a warp leaves at most 31 unfolded survivors plus 32 per candidate of a run
   static_assert(R >= 1 && (R & (R - 1)) == 0, "k_last_gj_bf: R must be a power of two (chunk_owners)");
@@ -265,14 +269,17 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
         const uint64_t se = __ldg(scan + e);
         const uint64_t prev = e ? __ldg(scan + e - 1) : 0ull;
         const uint64_t bend = min(iend, se);
-        const int ci = N.chosen[e];
+        // bindings may be visited in probe-region order: scan is then over the
+        // permuted sequence and perm maps a position to the binding
+        const uint32_t eb = perm ? __ldg(perm + e) : (uint32_t)e;
+        const int ci = N.chosen[eb];
         uint32_t sp[NS], sl[NS];
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           const KSub& P = N.sub[s];
           if (P.in_p) {
-            sp[s] = __ldg(P.in_p + e);
-            sl[s] = __ldg(P.in_len + e);
+            sp[s] = __ldg(P.in_p + eb);
+            sl[s] = __ldg(P.in_len + eb);
           } else {
             sp[s] = 0;
             sl[s] = *P.rregion;  // root: its probe region
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
           if (!live[r]) continue;
           const uint32_t slot = atomicAdd(&Q.tail[wi], 1u) & (HitQueue<NS>::QC - 1);
           Q.x[wi][slot] = x[r];
-          Q.e[wi][slot] = (uint32_t)e;
+          Q.e[wi][slot] = eb;
           Q.c[wi][slot] = (uint8_t)ci;
 #pragma unroll
           for (int j = 0; j < NS - 1; ++j) Q.q[j][wi][slot] = qv[r][j];
@@ -386,6 +393,28 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
     if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
     if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
   }
+}
+
+// Sort key of every binding entering a GJ last node: the start of the subtrie
+// region its (first) probed subatom will be probed in. Visiting bindings in
+// this order makes consecutive bindings probe the same region, so a region is
+// read from HBM about once per batch instead of once per probing binding.
+template <int NS>
+__global__ void k_probe_keys(const __grid_constant__ KNode N, uint64_t F, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < F; e += (uint64_t)gridDim.x * blockDim.x) {
+    const int ci = N.chosen[e];
+    const int s = ci == 0 ? 1 : 0;
+    const KSub& P = N.sub[s];
+    keys[e] = P.in_p ? __ldg(P.in_p + e) : 0u;
+    vals[e] = (uint32_t)e;
+  }
+}
+
+__global__ void k_gather_m(const uint64_t* __restrict__ m, const uint32_t* __restrict__ perm, uint64_t F,
+                           uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = __ldg(m + __ldg(perm + i));
 }
 
 #ifndef FJG_GJ_R

@@ -47,6 +47,8 @@ class ExecResult:
     output_rows: int = 0
     memo_ms: float = 0.0
     memo_rows: tuple = (0, 0, 0)  # resolved / gathered / initialised rows of the memo passes
+    atom_maps_built: list = field(default_factory=list)     # TrieStats per atom (its physical trie)
+    atom_levels_forced: list = field(default_factory=list)
     extra: dict = field(default_factory=dict)
 
 
@@ -249,6 +251,8 @@ class Query:
                           last_node_candidates=r.last_node_candidates, first_node_ms=r.first_node_ms,
                           memo_ms=r.memo_ms, memo_rows=(r.memo_rows_resolved, r.memo_rows_gathered,
                                                         r.memo_rows_init),
+                          atom_maps_built=list(r.atom_maps_built[:len(self.atoms)]),
+                          atom_levels_forced=list(r.atom_levels_forced[:len(self.atoms)]),
                           kernel_launches=r.kernel_launches, host_syncs=r.host_syncs, output_rows=r.output_rows)
 
     def enumerate(self, batch_size=0, dynamic_cover=True, min_var=None, backend="colt"):

@@ -31,7 +31,7 @@ def test_struct_sizes_match_header():
     # fjg_result / fjg_exec_options layouts are mirrored in _capi.py
     assert C.sizeof(_capi.ExecOptions) == 32
     assert C.sizeof(_capi.Predicate) == 24
-    assert C.sizeof(_capi.Result) == 8 * 3 + 8 + 4 + 4 + 8 * 3 + 8 * 32 * 3 + 8 * 4 + 8 * 3 + 8 * 2 + 8 + 8 * 4 + 4 * 2
+    assert C.sizeof(_capi.Result) == 8 * 3 + 8 + 4 + 4 + 8 * 3 + 8 * 32 * 3 + 8 * 4 + 8 * 3 + 8 * 2 + 8 + 8 * 4 + 8 * 16 + 4 * 16 + 4 * 2
     assert C.sizeof(_capi.MultiInfo) == 8 * 5 + 8 * 16 + 4 * 2 + 8 * 2
 
 

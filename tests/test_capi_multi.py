@@ -64,11 +64,11 @@ def test_compiled_caller_world1(tmp_path, name):
     data = os.path.join(str(tmp_path), "w.bin")
     write_workload(data, w, plan)
     p = subprocess.run([exe, data], capture_output=True, text=True, timeout=300)
-    assert p.returncode == 0, p.stderr
+    assert p.returncode == 0, p.stderr + p.stdout
     head = P.head_variables(w.query)
     ref = oracle.execute(w.query, plan, w.atom_columns(), min_var=head.index(w.min_var) if w.min_var else -1,
                          output_mode=w.output_mode)
-    lines = [json.loads(x) for x in p.stdout.splitlines()]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 2
     for r in lines:
         assert (r["count_hi"] << 64 | r["count_lo"]) == ref["count"]

@@ -530,3 +530,88 @@ def test_simple_backend_empty_relation_after_pool_reuse(engine):
             ref = oracle.execute(q, plan, cols, backend="simple", dynamic_cover=False)
             r, _ = gpu_execute(engine, q, plan, cols, backend="simple", dynamic_cover=False)
             assert (r.count, r.checksum, r.keys_inserted) == (ref["count"], ref["checksum"], ref["keys_inserted"])
+
+
+def test_acceptance4_device_colt_laziness(engine):
+    """SPEC acceptance #4 on the device: on the factored clover
+    with COLT, R (the cover, BaseScan) builds no map and S / T force at most
+    one level each; the extended clover with S(b) as cover builds no level-1
+    map for S (Example 4.4)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_oracle_acceptance import clover
+    for n in (20, 2000):
+        q, cols = clover(n)
+        plan = P.compile_plan(q, "free")
+        r, _ = gpu_execute(engine, q, plan, cols)
+        ref = oracle.execute(q, plan, cols)
+        assert r.count == ref["count"] == 1
+        assert r.atom_maps_built[0] == 0 and r.atom_levels_forced[0] == 0  # R: BaseScan only
+        for a in (1, 2):
+            assert bin(r.atom_levels_forced[a]).count("1") <= 1
+    q, cols = clover(20)
+    q2 = q + [{"rel": "U", "vars": ["b"]}]
+    U = [np.array([200, 3001, 3002], np.int32)]
+    plan = [[("R", ["x", "a"]), ("S", ["x"]), ("T", ["x"])], [("S", ["b"]), ("U", ["b"])], [("T", ["c"])]]
+    r, _ = gpu_execute(engine, q2, plan, cols + [U], dynamic_cover=False)
+    assert r.count == 1
+    assert not (r.atom_levels_forced[1] >> 1) & 1
+
+
+def test_acceptance6_device_probe_counters_batch_invariant(engine):
+    """SPEC acceptance #6 on the device: under a static cover the
+    output bag and the probe counters do not depend on the batch size
+    (1, 2, 7, 1000), and equal the oracle's."""
+    rng = np.random.default_rng(66)
+    done = 0
+    while done < 12:
+        q, cols = random_query(rng, max_atoms=4, max_rows=40)
+        plan = P.compile_plan(q, "free")
+        ref = oracle.execute(q, plan, cols, dynamic_cover=False, output_mode="enumerate")
+        if ref["count"] > 5000:
+            continue
+        done += 1
+        seen = None
+        for b in (1, 2, 7, 1000):
+            r, rows = gpu_execute(engine, q, plan, cols, batch_size=b, dynamic_cover=False, enumerate=True)
+            assert bag_equal(rows, ref["tuples"])
+            key = (r.probes, r.probe_misses, tuple(r.node_probes))
+            seen = seen or key
+            assert key == seen, (b, key, seen)
+        assert seen[0] == ref["probes"]
+
+
+_SORTED_SCRIPT = r'''
+import json, os, sys
+sys.path.insert(0, os.getcwd())
+import paper_2301_10841_b200 as fjg
+from paper_2301_10841_b200 import configs
+eng = fjg.Engine(0)
+out = []
+for w in (configs.triangle(scale=12, m=40000, seed=4), configs.triangle(scale=14, m=200000, seed=8)):
+    for batch in (0, 5000):
+        res, q, plan, rels = fjg.run_workload(eng, w, batch_size=batch)
+        out.append([res.count, res.checksum])
+print(json.dumps(out))
+'''
+
+
+def test_gj_last_node_probe_region_order():
+    """The GJ last node visiting bindings in probe-region order (the path C5
+    takes, forced here on small inputs with FJG_GJ_SORT_MIN_ROWS=0) gives the
+    oracle's count and checksum, for one and several frontier batches."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FJG_GJ_SORT_MIN_ROWS="0")
+    p = subprocess.run([sys.executable, "-c", _SORTED_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    got = json.loads(p.stdout.strip().splitlines()[-1])
+    i = 0
+    for w in (configs.triangle(scale=12, m=40000, seed=4), configs.triangle(scale=14, m=200000, seed=8)):
+        plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+        ref = oracle.execute(w.query, plan, w.atom_columns())
+        for _ in range(2):
+            assert got[i] == [ref["count"], ref["checksum"]]
+            i += 1
