@@ -1607,6 +1607,42 @@ static void eager_build(fjg_query* q) {
   }
 }
 
+// The chain's top node 0 as one reduction over pass 0's resolved children
+// (k_memo_total) when node 0 = [A(u,v) stream cover, B(v) root probe], A is a
+// single-subatom atom over the same relation and column as pass 0's carrier,
+// and B's root is the table pass 0 probed: node 0's rows are then the carrier
+// relation's rows and child(row) is exactly what pass 0 resolved per position.
+static bool memo_top_is_total(const fjg_query* q) {
+  if (q->chain_start != 1 || q->min_var >= 0 || q->memo_passes.empty()) return false;
+  const MemoPass& M0 = q->memo_passes[0];
+  if (M0.nfresh != 1 || M0.cont_x != 0 || M0.has_coef || !M0.child || M0.cnv != 1) return false;
+  const DevNode& N0 = q->nodes[0];
+  const KNode& K0 = q->knodes[0];
+  if (N0.nsub != 2) return false;
+  int c = -1, x = -1;
+  for (int i = 0; i < 2; ++i) {
+    if (N0.sub[i].nv == 2 && N0.sub[i].depth == 0) c = i;
+    if (N0.sub[i].nv == 1 && N0.sub[i].depth == 0 && !K0.sub[i].in_p) x = i;
+  }
+  if (c < 0 || x < 0 || c == x) return false;
+  if (K0.sub[x].table != M0.fresh[0].table) return false;
+  const int A = N0.sub[c].atom;
+  if (q->atoms[A].subs.size() != 1) return false;
+  const int v = N0.sub[x].var[0];
+  if (N0.sub[c].var[0] != v && N0.sub[c].var[1] != v) return false;
+  int carrier, next;
+  std::vector<int> fresh;
+  if (!device_chain_node(q, 1, carrier, fresh, next)) return false;
+  const int C = q->nodes[1].sub[carrier].atom;
+  const int cv = q->nodes[1].sub[carrier].var[0];
+  if (q->atoms[A].rel_index != q->atoms[C].rel_index) return false;
+  const auto& av = q->atoms[A].vars;
+  const auto& cvs = q->atoms[C].vars;
+  const int acol = (int)(std::find(av.begin(), av.end(), v) - av.begin());
+  const int ccol = (int)(std::find(cvs.begin(), cvs.end(), cv) - cvs.begin());
+  return acol == ccol && acol < (int)av.size();
+}
+
 static void execute_once(fjg_query* q, int mode) {
   reset_query(q);
   if (q->backend != FJG_BACKEND_COLT) eager_build(q);
@@ -1615,7 +1651,19 @@ static void execute_once(fjg_query* q, int mode) {
     run_memo_passes(q);
     q->stop_node = q->chain_start - 1;
   }
-  run_node(q, 0, 1, mode);
+  if (mode == EXPAND_MEMO && memo_top_is_total(q)) {
+    fjg_engine* eng = q->eng;
+    const MemoPass& M0 = q->memo_passes[0];
+    q->mark(eng->stream, -1);
+    LAUNCH(eng, k_memo_total<<<grid_for(M0.n, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(M0.child, M0.n,
+                                                                                         q->memo[0], 0, q->d_ctr));
+    q->mark(eng->stream, 2);
+    q->last_launches += 1;
+    q->last_candidates += M0.n;
+    q->node_inputs[0] = 1;
+  } else {
+    run_node(q, 0, 1, mode);
+  }
   sync_counters(q);
   if (q->dev_tail_node >= 0) q->last_candidates += q->h_ctr->tail_inputs[q->dev_tail_node];
   q->resolve_marks();

@@ -50,6 +50,7 @@ __device__ __forceinline__ uint32_t probe_region(const KSub& S, uint32_t len) {
 // earlier kernel of this node, so this is a pure lookup in its slot region:
 // read a bucket (one sector, as two 16-byte halves), stop at a match or at the
 // first free slot.
+template <bool WANT_LEN = true>
 __device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len, const int32_t (&key)[MAXK],
                                          uint32_t& q, uint32_t& ql) {
   const int nk = P.nv;
@@ -76,7 +77,7 @@ __device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len
           }
           if (eq) {
             q = sq;
-            ql = __ldg(P.cnt + sq);
+            ql = WANT_LEN ? __ldg(P.cnt + sq) : 0u;  // the child length costs a random read
             return true;
           }
         }
