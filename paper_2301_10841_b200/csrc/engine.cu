@@ -1351,7 +1351,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
                            FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
       if (gj_fast) {
-        chunk_owners(q, gscan, F, c0, c1, 32 * FJG_GJ_R);
+        chunk_owners(q, gscan, F, c0, c1, FJG_GJW ? 64 * FJG_GJW_RR : 32 * FJG_GJ_R);
         if (FJG_GJ_TICKET)
           CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, ticket), 0, 8, eng->stream));
       }
@@ -1364,7 +1364,24 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       else if (mode == EXPAND_MEMO)
         LAUNCH(eng, launch_expand<EXPAND_MEMO>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
                                                q->d_ctr));
-      else if (gj_fast) {  // k_last_gj_bf: x is the last head variable
+      else if (gj_fast && FJG_GJW) {  // k_last_gj_warp: x is the last head variable
+        const int W8 = q->head.size() <= 4 ? 4 : 8;
+        const uint64_t nch = (c1 - c0 + 64 * FJG_GJW_RR - 1) / (64 * FJG_GJW_RR);
+        const unsigned gw = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * FJG_GJW_MINB));
+        if (N.nsub == 2 && W8 == 4)
+          LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                      perm, q->min_var, q->d_ctr)));
+        else if (N.nsub == 2)
+          LAUNCH(eng, (k_last_gj_warp<2, 8, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                      perm, q->min_var, q->d_ctr)));
+        else if (W8 == 4)
+          LAUNCH(eng, (k_last_gj_warp<3, 4, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                      perm, q->min_var, q->d_ctr)));
+        else
+          LAUNCH(eng, (k_last_gj_warp<3, 8, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+                                                                                      perm, q->min_var, q->d_ctr)));
+      } else if (gj_fast) {  // k_last_gj_bf: x is the last head variable
         const int W8 = q->head.size() <= 4 ? 4 : 8;
         const unsigned gi = grid_for(c1 - c0, TILE * FJG_GJ_R, eng->num_sms * 8);
         if (N.nsub == 2 && W8 == 4)

@@ -417,6 +417,269 @@ __global__ void k_gather_m(const uint64_t* __restrict__ m, const uint32_t* __res
     out[i] = __ldg(m + __ldg(perm + i));
 }
 
+#ifndef FJG_GJW_RR
+#define FJG_GJW_RR 4  // 64-candidate double steps per warp chunk (chunk = 64 * RR candidates)
+#endif
+#ifndef FJG_GJW_MINB
+#define FJG_GJW_MINB 5  // 48 registers: C5 last node 1017 -> 973 ms vs 6 blocks (40 registers + spills)
+#endif
+#ifndef FJG_GJW
+#define FJG_GJW 1  // k_last_gj_warp instead of k_last_gj_bf for the GJ last node
+#endif
+
+// Binding state of a GJ last node (one frontier entry), loaded once per
+// binding by the whole warp (uniform addresses, broadcast loads).
+template <int NS>
+struct GjBind {
+  uint64_t prev, end;   // candidate range [prev, end) of the binding
+  uint32_t eb;          // binding index (after the probe-region permutation)
+  int ci;               // chosen cover
+  uint32_t cb;          // cover subtrie start
+  uint32_t p[NS - 1], len[NS - 1];  // probed subtrie regions, probe order
+};
+
+template <int NS>
+__device__ __forceinline__ void gj_load_bind(const KNode& N, const uint64_t* __restrict__ scan,
+                                             const uint32_t* __restrict__ perm, uint64_t e, GjBind<NS>& B) {
+  B.end = __ldg(scan + e);
+  B.prev = e ? __ldg(scan + e - 1) : 0ull;
+  B.eb = perm ? __ldg(perm + e) : (uint32_t)e;
+  B.ci = N.chosen[B.eb];
+  uint32_t sp[NS], sl[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const KSub& P = N.sub[s];
+    if (P.in_p) {
+      sp[s] = __ldg(P.in_p + B.eb);
+      sl[s] = __ldg(P.in_len + B.eb);
+    } else {
+      sp[s] = 0;
+      sl[s] = *P.rregion;
+    }
+  }
+  B.cb = sp[0];
+#pragma unroll
+  for (int s = 1; s < NS; ++s)
+    if (s == B.ci) B.cb = sp[s];
+#pragma unroll
+  for (int j = 0; j < NS - 1; ++j) {
+    B.p[j] = j >= B.ci ? sp[j + 1] : sp[j];
+    B.len[j] = j >= B.ci ? sl[j + 1] : sl[j];
+  }
+}
+
+// GJ-shaped last node, warp-uniform bindings: a warp walks chunks of 64 * RR
+// consecutive candidates (tickets from a device counter, as k_last_gj_bf) in
+// double steps of 64 (lane l takes candidates base + l and base + 32 + l, so
+// cover reads are two coalesced loads and two 256-bit bucket loads are in
+// flight per lane). A double step inside one binding -- the common case, a
+// binding has 300 candidates on C5 -- uses the warp's binding state held in
+// registers and costs no per-lane bookkeeping; a step crossing binding ends
+// walks each lane to its own binding. Survivors are folded from the per-warp
+// ring exactly as in k_last_gj_bf.
+template <int NS, int W, int RR>
+__global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __grid_constant__ KNode N, uint64_t c0,
+                                                                    uint64_t c1, uint64_t F,
+                                                                    const uint32_t* __restrict__ owner,
+                                                                    const uint32_t* __restrict__ perm, int min_var,
+                                                                    DevCounters* ctr) {
+  static_assert(64 + 63 < HitQueue<NS>::QC, "k_last_gj_warp: survivor ring too small");
+  __shared__ HitQueue<NS> Q;
+  uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
+  long long acc_min = LLONG_MAX;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint64_t* __restrict__ scan = N.scan;
+  const int nhead = N.nhead;
+  uint32_t head = 0;
+  if (lane == 0) Q.tail[wi] = 0;
+  __syncwarp();
+
+  auto fold = [&](uint32_t h0, uint32_t n) {
+    if ((uint32_t)lane < n) {
+      const uint32_t slot = (h0 + lane) & (HitQueue<NS>::QC - 1);
+      const int32_t x = Q.x[wi][slot];
+      const uint32_t e = Q.e[wi][slot];
+      const int ci = Q.c[wi][slot];
+      uint64_t mu = N.in_mult ? __ldg(N.in_mult + e) : 1ull;
+#pragma unroll
+      for (int j = 0; j < NS - 1; ++j) {
+        const uint32_t* cnt = j >= ci ? N.sub[j + 1].cnt : N.sub[j].cnt;
+        const bool plast = j >= ci ? N.sub[j + 1].last : N.sub[j].last;
+        const uint32_t* ldup = j >= ci ? N.sub[j + 1].ldup : N.sub[j].ldup;
+        if (plast && *ldup) mu *= __ldg(cnt + Q.q[j][wi][slot]);
+      }
+      uint64_t pre = fj::kTupleHashSeed;
+      long long bmin = LLONG_MAX;
+#pragma unroll
+      for (int v = 0; v < W; ++v)
+        if (v < nhead - 1) {
+          const int32_t hvv = __ldg(N.in_var[v] + e);
+          pre = fj::tuple_hash_step(pre, (int64_t)hvv);
+          if (v == min_var) bmin = hvv;
+        }
+      const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x);
+      acc_sum += mu * fj::checksum_word(h);
+      acc_lo += mu;
+      if (acc_lo < mu) ++acc_hi;
+      if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x : bmin);
+    }
+  };
+  // probe candidate x of a binding in its probed regions; survivors enqueue
+  auto probe_one = [&](bool live, int32_t x, const GjBind<NS>& B) {
+    uint32_t qv[NS - 1];
+#pragma unroll
+    for (int j = 0; j < NS - 1; ++j) {
+      qv[j] = kEmpty;
+      if (!live) continue;
+      const Slot* tb = j >= B.ci ? N.sub[j + 1].table : N.sub[j].table;
+      ++probes;
+      const uint32_t kw = (uint32_t)x;
+      uint64_t b = region_bucket(B.p[j], B.len[j], kw);
+      bool more;
+      uint32_t q = bucket_match(ld_bucket(tb, b), kw, more);
+      while (more) {
+        if (++b == (uint64_t)B.p[j] + B.len[j]) b = B.p[j];
+        q = bucket_match(ld_bucket(tb, b), kw, more);
+      }
+      if (q == kEmpty) {
+        ++misses;
+        live = false;
+      }
+      qv[j] = q;
+    }
+    if (live) {
+      const uint32_t slot = atomicAdd(&Q.tail[wi], 1u) & (HitQueue<NS>::QC - 1);
+      Q.x[wi][slot] = x;
+      Q.e[wi][slot] = B.eb;
+      Q.c[wi][slot] = (uint8_t)B.ci;
+#pragma unroll
+      for (int j = 0; j < NS - 1; ++j) Q.q[j][wi][slot] = qv[j];
+    }
+  };
+
+  constexpr uint64_t CH = 64 * RR;
+  const uint64_t nchunks = (c1 - c0 + CH - 1) / CH;
+  uint64_t tk = 0, tk_end = 0;
+  auto next_chunk = [&]() -> uint64_t {
+    if (tk == tk_end) {
+      unsigned long long t0 = 0;
+      if (lane == 0) t0 = atomicAdd(&ctr->ticket, (unsigned long long)FJG_GJ_TICKET);
+      tk = __shfl_sync(0xffffffffu, t0, 0);
+      tk_end = tk + FJG_GJ_TICKET;
+    }
+    return tk++;
+  };
+  for (uint64_t ch = next_chunk(); ch < nchunks; ch = next_chunk()) {
+    const uint64_t s0 = c0 + ch * CH, s1 = min(s0 + CH, c1);
+    uint64_t e = __ldg(owner + ch);
+    GjBind<NS> B;
+    gj_load_bind<NS>(N, scan, perm, e, B);
+#pragma unroll 1
+    for (int rr = 0; rr < RR; ++rr) {
+      const uint64_t base = s0 + 64ull * rr;
+      if (base >= s1) break;
+      while (B.end <= base) gj_load_bind<NS>(N, scan, perm, ++e, B);  // warp-uniform
+      if (base + 64 <= min(B.end, s1)) {
+        const int32_t* __restrict__ cs = (B.ci == 0 ? N.sub[0].src[0] : (B.ci == 1 ? N.sub[1].src[0]
+                                                                                   : N.sub[NS - 1].src[0])) +
+                                         B.cb + (base - B.prev);
+        const int32_t xa = __ldg(cs + lane), xb = __ldg(cs + 32 + lane);
+        body += 2;
+        if (NS == 2) {  // both buckets in flight before either is matched
+          const Slot* tb = B.ci == 0 ? N.sub[1].table : N.sub[0].table;
+          uint64_t ba = region_bucket(B.p[0], B.len[0], (uint32_t)xa);
+          uint64_t bb = region_bucket(B.p[0], B.len[0], (uint32_t)xb);
+          const Bucket8 ha = ld_bucket(tb, ba), hb = ld_bucket(tb, bb);
+          probes += 2;
+          bool ma, mb;
+          uint32_t qa = bucket_match(ha, (uint32_t)xa, ma), qb = bucket_match(hb, (uint32_t)xb, mb);
+          const uint64_t bhi = (uint64_t)B.p[0] + B.len[0];
+          while (ma) {
+            if (++ba == bhi) ba = B.p[0];
+            qa = bucket_match(ld_bucket(tb, ba), (uint32_t)xa, ma);
+          }
+          while (mb) {
+            if (++bb == bhi) bb = B.p[0];
+            qb = bucket_match(ld_bucket(tb, bb), (uint32_t)xb, mb);
+          }
+          misses += (qa == kEmpty) + (qb == kEmpty);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const uint32_t q = t ? qb : qa;
+            if (q != kEmpty) {
+              const uint32_t slot = atomicAdd(&Q.tail[wi], 1u) & (HitQueue<NS>::QC - 1);
+              Q.x[wi][slot] = t ? xb : xa;
+              Q.e[wi][slot] = B.eb;
+              Q.c[wi][slot] = (uint8_t)B.ci;
+              Q.q[0][wi][slot] = q;
+            }
+          }
+        } else {
+          probe_one(true, xa, B);
+          probe_one(true, xb, B);
+        }
+      } else {
+        // the double step crosses binding ends (or the chunk end): per lane
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const uint64_t i = base + 32 * t + lane;
+          const bool live = i < s1;
+          GjBind<NS> L = B;
+          if (live && i >= L.end) {
+            uint64_t el = e + 1;
+            while (__ldg(scan + el) <= i) ++el;
+            gj_load_bind<NS>(N, scan, perm, el, L);
+          }
+          const int32_t* cs = L.ci == 0 ? N.sub[0].src[0] : (L.ci == 1 ? N.sub[1].src[0] : N.sub[NS - 1].src[0]);
+          const int32_t x = live ? __ldg(cs + L.cb + (i - L.prev)) : 0;
+          body += live ? 1 : 0;
+          probe_one(live, x, L);
+        }
+      }
+      // warp-convergent: fold full batches of 32 (at most 64 + 31 pending)
+      __syncwarp();
+      const uint32_t tail = *(volatile uint32_t*)&Q.tail[wi];
+      while (tail - head >= 32) {
+        fold(head, 32);
+        head += 32;
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  fold(head, *(volatile uint32_t*)&Q.tail[wi] - head);
+  probes = warp_sum(probes);
+  misses = warp_sum(misses);
+  body = warp_sum(body);
+  uint64_t lo2 = acc_lo, hi2 = acc_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo2, o);
+    const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi2, o);
+    const uint64_t sm = lo2 + l2;
+    hi2 += h2 + (sm < lo2 ? 1 : 0);
+    lo2 = sm;
+  }
+  acc_sum = warp_sum(acc_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_min = min(acc_min, __shfl_xor_sync(0xffffffffu, acc_min, o));
+  if (lane == 0) {
+    if (probes) {
+      atomicAdd((unsigned long long*)&ctr->probes, (unsigned long long)probes);
+      atomicAdd((unsigned long long*)&ctr->node_probes[N.k], (unsigned long long)probes);
+    }
+    if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
+    if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
+    if (lo2) {
+      const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo2);
+      if (old + lo2 < old) ++hi2;
+    }
+    if (hi2) atomicAdd((unsigned long long*)&ctr->count_hi, (unsigned long long)hi2);
+    if (acc_sum) atomicAdd((unsigned long long*)&ctr->checksum, (unsigned long long)acc_sum);
+    if (acc_min != LLONG_MAX) atomicMin(&ctr->minv, acc_min);
+  }
+}
+
 #ifndef FJG_GJ_R
 #define FJG_GJ_R 2
 #endif
