@@ -619,21 +619,66 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
           probe_one(true, xb, B);
         }
       } else {
-        // the double step crosses binding ends (or the chunk end): per lane
+        // the double step crosses binding ends (or the chunk end). Lane j holds
+        // the end of binding e + j; when the window's bindings are among those
+        // 32 and none is empty, each lane finds its two candidates' bindings by
+        // popcounts over the window's end positions and fetches their state
+        // with shuffles from the lane that loaded it.
+        const unsigned FULL = 0xffffffffu;
+        const uint64_t wend = min(base + 64, s1);
+        const uint64_t ej = e + lane;
+        const uint64_t endj = ej < F ? __ldg(scan + ej) : ~0ull;
+        const uint64_t rel = endj - base;  // >= 1: binding e ends after base
+        const bool inwin = endj < wend;
+        const unsigned lo_bits = __reduce_or_sync(FULL, inwin && rel < 32 ? 1u << rel : 0u);
+        const unsigned hi_bits = __reduce_or_sync(FULL, inwin && rel >= 32 ? 1u << (rel - 32) : 0u);
+        const int nin = __popc(__ballot_sync(FULL, inwin));
+        const bool fits = __shfl_sync(FULL, endj, 31) >= wend && __popc(lo_bits) + __popc(hi_bits) == nin;
+        if (fits) {
+          // lanes 0..nin load the state of bindings e..e+nin
+          GjBind<NS> S = B;
+          if (lane > 0 && lane <= nin) gj_load_bind<NS>(N, scan, perm, ej, S);
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const uint64_t i = base + 32 * t + lane;
-          const bool live = i < s1;
-          GjBind<NS> L = B;
-          if (live && i >= L.end) {
-            uint64_t el = e + 1;
-            while (__ldg(scan + el) <= i) ++el;
-            gj_load_bind<NS>(N, scan, perm, el, L);
+          for (int t = 0; t < 2; ++t) {
+            const uint32_t pos = 32 * t + lane;  // candidate base + pos
+            const uint64_t i = base + pos;
+            const bool live = i < s1;
+            const unsigned below = pos >= 31 ? 0xffffffffu : ((2u << pos) - 1u);
+            const int seg = t == 0 ? __popc(lo_bits & below)
+                                   : __popc(lo_bits) + __popc(hi_bits & (lane >= 31 ? 0xffffffffu : ((2u << lane) - 1u)));
+            GjBind<NS> L;
+            L.prev = __shfl_sync(FULL, S.prev, seg);
+            L.eb = __shfl_sync(FULL, S.eb, seg);
+            L.ci = __shfl_sync(FULL, S.ci, seg);
+            L.cb = __shfl_sync(FULL, S.cb, seg);
+#pragma unroll
+            for (int j = 0; j < NS - 1; ++j) {
+              L.p[j] = __shfl_sync(FULL, S.p[j], seg);
+              L.len[j] = __shfl_sync(FULL, S.len[j], seg);
+            }
+            const int32_t* cs =
+                L.ci == 0 ? N.sub[0].src[0] : (L.ci == 1 ? N.sub[1].src[0] : N.sub[NS - 1].src[0]);
+            const int32_t x = live ? __ldg(cs + L.cb + (i - L.prev)) : 0;
+            body += live ? 1 : 0;
+            probe_one(live, x, L);
           }
-          const int32_t* cs = L.ci == 0 ? N.sub[0].src[0] : (L.ci == 1 ? N.sub[1].src[0] : N.sub[NS - 1].src[0]);
-          const int32_t x = live ? __ldg(cs + L.cb + (i - L.prev)) : 0;
-          body += live ? 1 : 0;
-          probe_one(live, x, L);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const uint64_t i = base + 32 * t + lane;
+            const bool live = i < s1;
+            GjBind<NS> L = B;
+            if (live && i >= L.end) {
+              uint64_t el = e + 1;
+              while (__ldg(scan + el) <= i) ++el;
+              gj_load_bind<NS>(N, scan, perm, el, L);
+            }
+            const int32_t* cs =
+                L.ci == 0 ? N.sub[0].src[0] : (L.ci == 1 ? N.sub[1].src[0] : N.sub[NS - 1].src[0]);
+            const int32_t x = live ? __ldg(cs + L.cb + (i - L.prev)) : 0;
+            body += live ? 1 : 0;
+            probe_one(live, x, L);
+          }
         }
       }
       // warp-convergent: fold full batches of 32 (at most 64 + 31 pending)
