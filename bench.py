@@ -291,18 +291,22 @@ def _first_var_atoms(ow):
     return fv, [i for i, a in enumerate(ow.query) if fv in a["vars"]]
 
 
-def _restricted_columns(ow, cols, parts, P):
-    import numpy as np
+_PART_CACHE = {}
+
+
+def _restricted_columns(ow, cols, T, P):
+    """The atoms holding the first variable, restricted to partitions 0..T-1 of P
+    (partition ids cached per (column, P): the C5 columns have 512M rows)."""
     fv, atoms = _first_var_atoms(ow)
     out = list(cols)
-    cache = {}
     for i in atoms:
         c = ow.query[i]["vars"].index(fv)
-        key = (id(cols[i][0]), c)
-        if key not in cache:
-            keep = np.isin(_np_partition_of(cols[i][c], P), np.asarray(parts, dtype=np.uint64))
-            cache[key] = [x[keep] for x in cols[i]]
-        out[i] = cache[key]
+        key = (id(cols[i][c]), P)
+        if key not in _PART_CACHE:
+            _PART_CACHE.clear()
+            _PART_CACHE[key] = _np_partition_of(cols[i][c], P)
+        keep = _PART_CACHE[key] < T
+        out[i] = [x[keep] for x in cols[i]]
     return out
 
 
@@ -321,7 +325,7 @@ def cpu_sample(ow, T, P, cols=None):
     cols = cols if cols is not None else ow.atom_columns()
     head = ow.head()
     mv = head.index(ow.min_var) if ow.min_var else -1
-    rc = _restricted_columns(ow, cols, list(range(T)), P) if P > 1 else cols
+    rc = _restricted_columns(ow, cols, T, P) if P > T else cols
     t0 = time.perf_counter()
     r = oracle.execute(ow.query, ow.plan, rc, part=0, nparts=P, nthreads=T, min_var=mv,
                        output_mode=ow.output_mode)
@@ -394,9 +398,12 @@ def run_reference(args):
     # of that size exceed the budget, run as many as fit (at least one)
     warm = args.warmup if s0["seconds"] * (steps + args.warmup) <= budget else 0
     steps = steps if s0["seconds"] * (steps + warm) <= budget else max(1, int(budget // max(s0["seconds"], 1e-9)))
-    for _ in range(warm):
-        cpu_sample(ow, T, s0["P"], cols)
-    runs = [cpu_sample(ow, T, s0["P"], cols) for _ in range(steps)]
+    if steps == 1 and warm == 0 and s0["seconds"] > budget / 2:
+        runs = [s0]  # the calibration sample already is one full-size step (same P, same threads)
+    else:
+        for _ in range(warm):
+            cpu_sample(ow, T, s0["P"], cols)
+        runs = [cpu_sample(ow, T, s0["P"], cols) for _ in range(steps)]
     v = statistics.median(r["value"] for r in runs)
     last = runs[-1]
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
