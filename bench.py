@@ -337,12 +337,15 @@ def cpu_sample(ow, T, P, cols=None):
 
 
 def cpu_leg(ow, T, target_s, cols=None):
-    """Adaptive bounded sample on T threads: P starts at 4096*T first-variable
+    """Adaptive bounded sample on T threads: P starts at 4096 first-variable
     partitions and shrinks 4x while a sample takes < target_s/5, so the final
     sample is ~target_s unless one thread's fixed trie build alone is longer
     (C5: ~150 s to build the 512M-row E2 trie on one core)."""
     cols = cols if cols is not None else ow.atom_columns()
-    P = 4096 * T
+    # every thread starts with 1/4096 of the query: when a sample is dominated by
+    # one thread's fixed trie build, T threads then do T times the work in the
+    # same time (P = 4096 for every T), as they would on the whole query
+    P = max(4096, T)
     s = cpu_sample(ow, T, P, cols)
     while P > T and s["seconds"] < target_s / 5:
         P = max(T, P // 4)
@@ -364,7 +367,7 @@ def cpu_baseline(ow, target_s, threads=0, cols=None):
     capped = ""
     if info["mem_available_bytes"]:
         per = _thread_bytes(ow, cols, 1.0 / max(T, 1))
-        tmax = max(1, int(0.6 * info["mem_available_bytes"] // per))
+        tmax = max(1, int(0.75 * info["mem_available_bytes"] // per))
         if tmax < T:
             T, capped = tmax, f" (capped from {os.cpu_count()} by host memory: ~{per / 2**30:.1f} GiB of tries per thread)"
     allc = cpu_leg(ow, T, target_s, cols) if T > 1 else one
@@ -389,7 +392,7 @@ def run_reference(args):
     T = args.cpu_threads or max(1, min(os.cpu_count() or 1, 64))
     info = host_info()
     if info["mem_available_bytes"]:
-        T = max(1, min(T, int(0.6 * info["mem_available_bytes"] // _thread_bytes(ow, cols, 1.0 / T))))
+        T = max(1, min(T, int(0.75 * info["mem_available_bytes"] // _thread_bytes(ow, cols, 1.0 / T))))
     steps = max(args.steps, 1)
     budget = 300.0  # seconds for the whole arm
     target = max(2.0, min(60.0, budget / (steps + args.warmup + 2)))
