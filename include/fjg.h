@@ -191,6 +191,41 @@ int fjg_relation_partition(const fjg_relation* in, int col, int nparts, fjg_rela
 int fjg_relation_partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_dev_cols,
                                 uint64_t* counts);
 
+/* ---- GHT / COLT handle (Fig 5 new/iter/get; SPEC.md:286-339
+ * force / iter_batch / estimated_key_count) ----
+ * A device COLT over one relation with a caller-given GHT schema: level l keys
+ * on the columns level_cols[off_l .. off_l + level_ncols[l]); columns no level
+ * names form a final vector level (rows). A subtrie of level l is named by its
+ * position range (p, len) in the level's ordering; the root is (0, rows). State
+ * persists across calls and queries: force is lazy and idempotent, so a host
+ * can own tries and reuse them. Creation does no device work (GHT new = BaseScan). */
+typedef struct fjg_colt fjg_colt;
+int fjg_colt_create(fjg_engine* eng, const fjg_relation* rel, const int* level_cols, const int* level_ncols,
+                    int nlevels, fjg_colt** out);
+/* number of levels (the map levels plus the vector level if any column is left) */
+int fjg_colt_levels(const fjg_colt* colt);
+/* force the n given subtries of map level `level` (level 0:
+ * the root; p/len ignored). Already forced subtries are left as they are. */
+int fjg_colt_force(fjg_colt* colt, int level, const uint32_t* p, const uint32_t* len, uint64_t n);
+/* get (Fig 12: force, then lookup), batched: for key i (arity = the level's
+ * key columns, row-major int32) in subtrie (p[i], len[i]) of map level
+ * `level`: found[i], and the child subtrie (child_p[i], child_len[i]) of level
+ * + 1. Host arrays. */
+int fjg_colt_get(fjg_colt* colt, int level, const uint32_t* p, const uint32_t* len, const int32_t* keys, uint64_t n,
+                 uint32_t* child_p, uint32_t* child_len, uint8_t* found);
+/* iter (Fig 12 on a map: force, then its keys): the distinct keys of subtrie
+ * (p, len) of map level `level` in the level's clustered order, with their
+ * child subtries; *nkeys receives the count (FJG_E_RESOURCE if > cap). */
+int fjg_colt_iter(fjg_colt* colt, int level, uint32_t p, uint32_t len, int32_t* keys_out, uint32_t* child_p,
+                  uint32_t* child_len, uint64_t cap, uint64_t* nkeys);
+/* iter on a vector / rows of any subtrie: column `col` of the len rows of
+ * subtrie (p, len) at `level`, in the subtrie's order (no forcing). */
+int fjg_colt_rows(fjg_colt* colt, int level, uint32_t p, uint32_t len, int col, int32_t* out);
+/* estimated_key_count: a forced map -> its keys; otherwise
+ * (unforced map, vector, BaseScan root) -> its length. Never forces. */
+int fjg_colt_estimated_key_count(fjg_colt* colt, int level, uint32_t p, uint32_t len, uint64_t* out);
+void fjg_colt_destroy(fjg_colt* colt);
+
 /* ---- multi-GPU execution (north_star (c)) ----
  * The reference is single-threaded with reentrant, disjoint contexts
  * (SPEC.md:354, :447); these calls run one such context per GPU and combine

@@ -124,6 +124,14 @@ def _load():
         "fjg_execute_multi": (I, [P, C.POINTER(ExecOptions), C.POINTER(Result), C.POINTER(MultiInfo)]),
         "fjg_sharded_destroy": (None, [P]),
         "fjg_exchange_layout": (I, [P, I, I, I, P, P, P]),
+        "fjg_colt_create": (I, [P, P, P, P, I, C.POINTER(P)]),
+        "fjg_colt_levels": (I, [P]),
+        "fjg_colt_force": (I, [P, I, P, P, U64]),
+        "fjg_colt_get": (I, [P, I, P, P, P, U64, P, P, P]),
+        "fjg_colt_iter": (I, [P, I, C.c_uint32, C.c_uint32, P, P, P, U64, C.POINTER(U64)]),
+        "fjg_colt_rows": (I, [P, I, C.c_uint32, C.c_uint32, I, P]),
+        "fjg_colt_estimated_key_count": (I, [P, I, C.c_uint32, C.c_uint32, C.POINTER(U64)]),
+        "fjg_colt_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -143,7 +151,8 @@ EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_o
             "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_output_relation", "fjg_query_destroy",
             "fjg_device_tuple_hash", "fjg_host_tuple_hash", "fjg_parse_csv", "fjg_comm_unique_id", "fjg_comm_create",
             "fjg_comm_size", "fjg_comm_rank", "fjg_comm_destroy", "fjg_sharded_create", "fjg_execute_multi",
-            "fjg_sharded_destroy", "fjg_exchange_layout"]
+            "fjg_sharded_destroy", "fjg_exchange_layout", "fjg_colt_create", "fjg_colt_levels", "fjg_colt_force",
+            "fjg_colt_get", "fjg_colt_iter", "fjg_colt_rows", "fjg_colt_estimated_key_count", "fjg_colt_destroy"]
 
 
 def check(rc):

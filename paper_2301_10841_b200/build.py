@@ -47,7 +47,7 @@ def _srcs(*names):
 def build_product(force=False):
     kdir = os.path.join(CSRC, "kernels")
     deps = _srcs("engine.cu", "engine.cuh", "capi.cpp", "fj_plan.cpp", "fj_plan.hpp", "fj_json.hpp",
-                 "fj_hash.hpp", "fj_errors.hpp", "multi.cuh") + [os.path.join(ROOT, "include", "fjg.h")] + \
+                 "fj_hash.hpp", "fj_errors.hpp", "multi.cuh", "colt_api.cuh") + [os.path.join(ROOT, "include", "fjg.h")] + \
         [os.path.join(kdir, f) for f in sorted(os.listdir(kdir)) if f.endswith(".cuh")]
     if force or _stale(LIBFJG, deps):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",

@@ -2107,3 +2107,4 @@ int fjg_device_tuple_hash(fjg_engine* eng, const int64_t* host_vals, int arity, 
 }  // extern "C"
 
 #include "multi.cuh"
+#include "colt_api.cuh"

@@ -118,6 +118,11 @@ class Engine:
     def query(self, query, plan, atom_relations):
         return Query(self, query, plan, atom_relations)
 
+    def colt(self, relation, levels):
+        """A GHT / COLT handle over `relation` (fjg_colt_create): `levels` = key
+        column lists per level, e.g. [[0], [1]]."""
+        return Colt(self, relation, levels)
+
     def device_tuple_hash(self, tuples):
         t = np.ascontiguousarray(np.asarray(tuples, dtype=np.int64))
         if t.ndim == 1:
@@ -275,6 +280,76 @@ class Query:
         if self._h and self.engine._h:
             lib.fjg_query_destroy(self._h)
         self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Colt:
+    """Device GHT with the COLT interface of Fig 5 / Fig 12 (PAPER.md:544-557,
+    SPEC.md:286-339): force / get / iter / rows / estimated_key_count over
+    subtries named (p, len); state persists across calls."""
+
+    def __init__(self, engine, relation, levels):
+        flat = [int(c) for lv in levels for c in lv]
+        cols = (C.c_int * max(len(flat), 1))(*flat)
+        ncols = (C.c_int * len(levels))(*[len(lv) for lv in levels])
+        h = C.c_void_p()
+        check(lib.fjg_colt_create(engine._h, relation._h, cols, ncols, len(levels), C.byref(h)))
+        self._h, self.engine, self.relation = h, engine, relation
+        self.key_arity = [len(lv) for lv in levels]
+        self.nlevels = lib.fjg_colt_levels(h)
+        engine._children.add(self)
+
+    def force(self, level, subtries):
+        p = np.ascontiguousarray([s[0] for s in subtries], dtype=np.uint32)
+        n = np.ascontiguousarray([s[1] for s in subtries], dtype=np.uint32)
+        check(lib.fjg_colt_force(self._h, level, p.ctypes.data, n.ctypes.data, len(p)))
+
+    def get(self, level, subtries, keys):
+        """keys: one tuple per subtrie; returns [(child_p, child_len) or None]."""
+        n = len(keys)
+        ar = self.key_arity[level]
+        p = np.ascontiguousarray([s[0] for s in subtries], dtype=np.uint32)
+        ln = np.ascontiguousarray([s[1] for s in subtries], dtype=np.uint32)
+        k = np.ascontiguousarray(np.asarray(keys, dtype=np.int32).reshape(n, ar))
+        cp = np.zeros(max(n, 1), dtype=np.uint32)
+        cl = np.zeros(max(n, 1), dtype=np.uint32)
+        f = np.zeros(max(n, 1), dtype=np.uint8)
+        check(lib.fjg_colt_get(self._h, level, p.ctypes.data, ln.ctypes.data, k.ctypes.data, n, cp.ctypes.data,
+                               cl.ctypes.data, f.ctypes.data))
+        return [(int(cp[i]), int(cl[i])) if f[i] else None for i in range(n)]
+
+    def iter(self, level, subtrie=(0, 0)):
+        """Distinct keys of a map subtrie with their child subtries: [(key tuple, (p, len))]."""
+        ar = self.key_arity[level]
+        cap = max(int(subtrie[1]) if level else self.relation.rows, 1)
+        keys = np.zeros(cap * ar, dtype=np.int32)
+        cp = np.zeros(cap, dtype=np.uint32)
+        cl = np.zeros(cap, dtype=np.uint32)
+        n = C.c_uint64()
+        check(lib.fjg_colt_iter(self._h, level, int(subtrie[0]), int(subtrie[1]), keys.ctypes.data, cp.ctypes.data,
+                                cl.ctypes.data, cap, C.byref(n)))
+        k = n.value
+        return [(tuple(int(x) for x in keys[i * ar:(i + 1) * ar]), (int(cp[i]), int(cl[i]))) for i in range(k)]
+
+    def rows(self, level, subtrie, col):
+        out = np.zeros(max(int(subtrie[1]), 1), dtype=np.int32)
+        check(lib.fjg_colt_rows(self._h, level, int(subtrie[0]), int(subtrie[1]), col, out.ctypes.data))
+        return out[:int(subtrie[1])]
+
+    def estimated_key_count(self, level, subtrie=(0, 0)):
+        out = C.c_uint64()
+        check(lib.fjg_colt_estimated_key_count(self._h, level, int(subtrie[0]), int(subtrie[1]), C.byref(out)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.fjg_colt_destroy(self._h)
+            self._h = None
 
     def __del__(self):
         try:

@@ -23,7 +23,15 @@ w = configs.CONFIGS[name]()
 plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
 fv, views = D.atom_views(w.query, w.atom_rel, plan)
 full = {b: [torch.from_numpy(c).cuda() for c in cols] for b, cols in w.filtered().items()}
-ops = D.DeviceOps(eng)
+
+
+def partition(cols, col, G):
+    """The product partition kernel (fjg_relation_partition_into) into torch buffers."""
+    rel = eng.relation_from_torch(cols)
+    grouped = [torch.empty_like(c) for c in cols]
+    counts = rel.partition_into(col, G, [g.data_ptr() for g in grouped])
+    rel.close()
+    return grouped, counts
 
 
 BIG = name.startswith("scale")
@@ -51,7 +59,7 @@ for G in Gs:
     for (b, col) in set(views):
         if col is None:
             continue
-        grouped, counts = ops.partition(full[b], col, G)
+        grouped, counts = partition(full[b], col, G)
         offs = [sum(counts[:r]) for r in range(G)]
         parts[(b, col)] = [[g[offs[r]: offs[r] + counts[r]].clone() for g in grouped] for r in range(G)]
     total, cs, per = 0, 0, []
