@@ -304,6 +304,10 @@ class Colt:
         self.nlevels = lib.fjg_colt_levels(h)
         engine._children.add(self)
 
+    def _arity(self, level):
+        # out-of-range levels are reported by the library (ValidationError)
+        return self.key_arity[level] if 0 <= level < len(self.key_arity) else 1
+
     def force(self, level, subtries):
         p = np.ascontiguousarray([s[0] for s in subtries], dtype=np.uint32)
         n = np.ascontiguousarray([s[1] for s in subtries], dtype=np.uint32)
@@ -312,7 +316,7 @@ class Colt:
     def get(self, level, subtries, keys):
         """keys: one tuple per subtrie; returns [(child_p, child_len) or None]."""
         n = len(keys)
-        ar = self.key_arity[level]
+        ar = self._arity(level)
         p = np.ascontiguousarray([s[0] for s in subtries], dtype=np.uint32)
         ln = np.ascontiguousarray([s[1] for s in subtries], dtype=np.uint32)
         k = np.ascontiguousarray(np.asarray(keys, dtype=np.int32).reshape(n, ar))
@@ -325,7 +329,7 @@ class Colt:
 
     def iter(self, level, subtrie=(0, 0)):
         """Distinct keys of a map subtrie with their child subtries: [(key tuple, (p, len))]."""
-        ar = self.key_arity[level]
+        ar = self._arity(level)
         cap = max(int(subtrie[1]) if level else self.relation.rows, 1)
         keys = np.zeros(cap * ar, dtype=np.int32)
         cp = np.zeros(cap, dtype=np.uint32)
