@@ -1359,7 +1359,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
         LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
       if (mode == EXPAND_ENUM)
-        LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1,
+        LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, q->min_var,
                                                q->out_tuples, q->out_cap, q->d_ctr));
       else if (mode == EXPAND_MEMO)
         LAUNCH(eng, launch_expand<EXPAND_MEMO>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, -1, nullptr, 0,
@@ -1990,23 +1990,28 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     q->backend = o.backend;
     const uint32_t l0 = eng->launches, s0 = eng->syncs;
     const bool memo = o.output_mode == FJG_OUT_FACTORIZED_COUNT && q->chain_start >= 1;
-    execute_once(q, memo ? EXPAND_MEMO : EXPAND_COUNT);
     if (o.output_mode == FJG_OUT_ENUMERATE) {
-      const uint64_t rows = q->h_ctr->count_lo;
-      if (q->h_ctr->count_hi || rows > (1ull << 34) / std::max<uint64_t>(q->head.size(), 1))
-        throw fj::ResourceError("enumerated output too large to materialise");
-      const uint64_t need = std::max<uint64_t>(rows, 1) * q->head.size() * 4;
-      if (q->out_cap < rows || !q->out_tuples) {
-        q->out_tuples = (int32_t*)q->alloc(need);
+      // one pass writes the tuples and folds count / checksum / MIN; the buffer
+      // keeps its capacity across executions, and a pass that outgrows it is
+      // rerun once with the exact size (SPEC.md:449 collector sink)
+      const size_t nh = std::max<size_t>(q->head.size(), 1);
+      auto ensure_out = [&](uint64_t rows) {
+        if (rows > (1ull << 34) / nh) throw fj::ResourceError("enumerated output too large to materialise");
+        if (q->out_cap >= rows && q->out_tuples) return;
+        q->out_tuples = (int32_t*)q->alloc(std::max<uint64_t>(rows, 1) * nh * 4);
         q->out_cap = rows;
-      }
-      DevCounters keep = *q->h_ctr;
+      };
+      if (!q->out_tuples) ensure_out(std::min<uint64_t>(std::max<uint64_t>(2 * q->max_n, 1024), 1ull << 26));
       execute_once(q, EXPAND_ENUM);
+      if (q->h_ctr->count_hi) throw fj::ResourceError("enumerated output too large to materialise");
+      if (q->h_ctr->out_rows > q->out_cap) {
+        ensure_out(q->h_ctr->out_rows);
+        execute_once(q, EXPAND_ENUM);
+      }
       q->out_rows = q->h_ctr->out_rows;
-      const DevCounters enum_ctr = *q->h_ctr;
-      *q->h_ctr = keep;
-      q->h_ctr->out_rows = enum_ctr.out_rows;
-      if (q->out_rows != rows) throw fj::EngineError("enumerate pass disagrees with count pass");
+      if (q->out_rows != q->h_ctr->count_lo) throw fj::EngineError("enumerated rows disagree with the count");
+    } else {
+      execute_once(q, memo ? EXPAND_MEMO : EXPAND_COUNT);
     }
     const DevCounters& H = *q->h_ctr;
     fjg_result r{};

@@ -1417,7 +1417,7 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
       for (int t = 0; t < MAXK; ++t)
         if (t < S.nv) put(val, S.var[t], __ldg(S.src[t] + tp[j] + off));
     }
-    if (MODE == EXPAND_COUNT) {
+    {  // count / checksum / MIN (also when enumerating: one pass yields both)
       uint64_t h = fj::kTupleHashSeed;
 #pragma unroll
       for (int v = 0; v < W; ++v)
@@ -1426,7 +1426,8 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
       acc_lo += mult;
       if (acc_lo < mult) ++acc_hi;
       if (min_var >= 0) acc_min = min(acc_min, (long long)sel(val, min_var));
-    } else {
+    }
+    if (MODE == EXPAND_ENUM) {
       const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
       for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
 #pragma unroll
@@ -1506,7 +1507,7 @@ __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, 
         if (j > 0 && inputs[j]) atomicAdd((unsigned long long*)&ctr->tail_inputs[T.node[j]], (unsigned long long)inputs[j]);
         if (body[j]) atomicAdd((unsigned long long*)&ctr->body[T.node[j]], (unsigned long long)body[j]);
       }
-    if (MODE == EXPAND_COUNT) {
+    if (MODE == EXPAND_COUNT || MODE == EXPAND_ENUM) {
       if (lo) {
         const unsigned long long old = atomicAdd((unsigned long long*)&ctr->count_lo, (unsigned long long)lo);
         if (old + lo < old) ++hi;

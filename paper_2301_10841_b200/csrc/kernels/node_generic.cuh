@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
       }
       __syncthreads();
     } else if (alive) {
-      if (MODE == EXPAND_COUNT) {
+      if (MODE == EXPAND_COUNT || MODE == EXPAND_ENUM) {  // enumerating folds the count / checksum too
         uint64_t h = fj::kTupleHashSeed;
 #pragma unroll
         for (int v = 0; v < W; ++v)
@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
         const unsigned __int128 c = mv * mult + (((unsigned __int128)acc_hi << 64) | acc_lo);
         acc_lo = (uint64_t)c;
         acc_hi = (uint64_t)(c >> 64);
-      } else {
+      }
+      if (MODE == EXPAND_ENUM) {
         const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
         for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
 #pragma unroll
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(TILE, FJG_EXPAND_MINBLOCKS) k_expand(const __g
     if (misses) atomicAdd((unsigned long long*)&ctr->misses, (unsigned long long)misses);
     if (body) atomicAdd((unsigned long long*)&ctr->body[N.k], (unsigned long long)body);
   }
-  if (MODE == EXPAND_COUNT || MODE == EXPAND_MEMO) {
+  if (MODE == EXPAND_COUNT || MODE == EXPAND_MEMO || MODE == EXPAND_ENUM) {
     // 128-bit count: carry out of the low word
     uint64_t lo = acc_lo, hi = acc_hi;
 #pragma unroll

@@ -615,3 +615,24 @@ def test_gj_last_node_probe_region_order():
         for _ in range(2):
             assert got[i] == [ref["count"], ref["checksum"]]
             i += 1
+
+
+def test_enumerate_single_pass_and_regrow(engine):
+    """Enumerate is one pass that folds count / checksum too; an output larger
+    than the buffer's capacity (2 x the largest relation at first) is rerun
+    once at the exact size, and the capacity is kept for the next execution."""
+    n = 700
+    R = [np.arange(n, dtype=np.int32), np.zeros(n, np.int32)]
+    S = [np.zeros(n, np.int32), np.arange(n, dtype=np.int32) + 5]
+    q = [{"rel": "R", "vars": ["a", "b"]}, {"rel": "S", "vars": ["b", "c"]}]
+    plan = P.compile_plan(q, "free")
+    ref = oracle.execute(q, plan, [R, S], output_mode="enumerate")
+    assert ref["count"] == n * n
+    rels = [engine.relation(R), engine.relation(S)]
+    qq = engine.query({"query": q}, plan, rels)
+    for _ in range(2):  # first: regrow and rerun; second: the kept capacity fits
+        rows, r = qq.enumerate()
+        assert r.count == len(rows) == n * n and r.checksum == ref["checksum"]
+        assert bag_equal(rows, ref["tuples"])
+    c = qq.execute()
+    assert (c.count, c.checksum) == (r.count, r.checksum)
