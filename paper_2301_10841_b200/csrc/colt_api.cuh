@@ -273,7 +273,8 @@ int fjg_colt_iter(fjg_colt* c, int level, uint32_t p, uint32_t len, int32_t* key
     const DevLevel& L = colt_trie(c).lev[level];
     uint32_t* d = (uint32_t*)eng->pool->alloc((2 * len + 1) * 4);
     CK(cudaMemsetAsync(d + 2 * len, 0, 4, eng->stream));
-    LAUNCH(eng, k_colt_keys<<<grid_for(4 * region), 256, 0, eng->stream>>>(L.table, 4ull * p, 4ull * (p + region),
+    LAUNCH(eng, k_colt_keys<<<grid_for(4ull * FJG_RS * region), 256, 0, eng->stream>>>(L.table, 4ull * FJG_RS * p,
+                                                                                          4ull * FJG_RS * (p + region),
                                                                             L.cnt, d, d + len, d + 2 * len));
     uint32_t k = 0;
     CK(cudaMemcpyAsync(&k, d + 2 * len, 4, cudaMemcpyDeviceToHost, eng->stream));

@@ -282,6 +282,7 @@ struct fjg_query {
   std::vector<uint64_t> memo_n;
   std::map<int, uint32_t*> gid;         // per chain trie: group index + 1 of each level-0 position
   std::vector<int> memo_resolve_of;     // pass -> pass whose resolved child / coef arrays it reuses
+  std::map<int, uint32_t*> memo_dense;  // per sorted chain root: dense key -> group map (size 2^key_bits)
   KNode memo_top{};                     // node k*-1 aggregating mult * memo[child]
   int stop_node = -1;
   int gj_x[MAXN];  // per node: the GJ fast-path variable, or -1
@@ -449,7 +450,7 @@ static void prepare_query(fjg_query* q) {
       H.keycols = T.levels[l];
       H.multi = H.keycols.size() >= 2;
       H.nsub = l == 0 ? 1 : std::max<uint64_t>(n, 1);
-      H.cap = 4 * std::max<uint64_t>(n, 1);  // one 4-slot bucket per position: per-subtrie regions
+      H.cap = 4ull * FJG_RS * std::max<uint64_t>(n, 1);  // FJG_RS 4-slot buckets per position: per-subtrie regions
       L.table = (Slot*)q->alloc(H.cap * sizeof(Slot));
       L.srep = H.multi ? (uint32_t*)q->alloc(H.cap * 4) : nullptr;
       L.state = (uint32_t*)q->alloc(H.nsub * 4);
@@ -474,7 +475,9 @@ static void prepare_query(fjg_query* q) {
   q->newslot_p = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->owner_scratch = (uint32_t*)q->alloc(std::max<uint64_t>(q->max_n, 1) * 4);
   q->sort_flags = (uint8_t*)q->alloc(std::max<uint64_t>(q->max_n, 1));
-  if (q->max_n >= (1ull << 31)) throw ValidationError("relations must have fewer than 2^31 rows");
+  // slot indices (4 * FJG_RS per row) are 32-bit in the force scratch
+  if (q->max_n >= (1ull << 31) || q->max_n > (1ull << 32) / (4 * FJG_RS))
+    throw ValidationError("relations must have at most " + std::to_string((1ull << 32) / (4 * FJG_RS)) + " rows");
   // static node descriptors
   const size_t K = plan.nodes.size();
   q->nodes.assign(K, DevNode{});
@@ -831,6 +834,19 @@ static void prepare_chain(fjg_query* q) {
     if (q->memo_resolve_of[i] < 0 && M.nfresh > 0) {
       if (M.cont_x >= 0) M.child = (uint32_t*)q->alloc(std::max<uint64_t>(M.n, 1) * 4);
       if (M.has_coef) M.coef = (uint64_t*)q->alloc(std::max<uint64_t>(M.n, 1) * 8);
+      // the continuing atom's root is sorted on small non-negative keys: a dense
+      // key -> group map replaces the probe and the group-id read (one read/row)
+      if (M.cont_x == 0 && M.nfresh == 1 && M.fresh[0].nv == 1) {
+        const int ft = M.fresh[0].trie;
+        const auto& FT = q->tries[ft];
+        const uint64_t dn = 1ull << std::min(FT.key_bits, 31);
+        if (FT.levels[0].size() == 1 && FT.rel->nrows >= (1u << 21) && FT.key_bits <= 30 &&
+            dn <= 8 * std::max<uint64_t>(FT.rel->nrows, 1)) {
+          if (!q->memo_dense.count(ft)) q->memo_dense[ft] = (uint32_t*)q->alloc(dn * 4);
+          M.direct = q->memo_dense[ft];
+          M.direct_n = (uint32_t)dn;
+        }
+      }
     }
   }
   for (size_t i = 0; i + 1 < passes.size(); ++i) q->memo_passes[i].memo_next = q->memo[i + 1];
@@ -1106,6 +1122,9 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
 #ifndef FJG_GJ_SORT
 #define FJG_GJ_SORT 1
 #endif
+#ifndef FJG_GJ_SORT_BITS
+#define FJG_GJ_SORT_BITS 16  // high bits of the probed region start that order the bindings
+#endif
 // Order the F bindings entering GJ last node k by the region their probed
 // subatom is probed in (k_probe_keys + radix sort), and build the permuted
 // candidate scan. Returns the permutation (null when not worth it: the probed
@@ -1137,11 +1156,14 @@ static const uint32_t* probe_region_order(fjg_query* q, int k, const KNode& KN, 
   }
   int bits = 1;
   while (bits < 32 && (1ull << bits) < rows) ++bits;
+  // locality needs only the high bits: regions whose starts share them lie in
+  // one window of 2^(bits - FJG_GJ_SORT_BITS) positions (2 radix passes, not 4)
+  const int lo_bit = std::max(0, bits - FJG_GJ_SORT_BITS);
   const unsigned g = grid_for(F, 256, eng->num_sms * 16);
   LAUNCH(eng, k_probe_keys<2><<<g, 256, 0, eng->stream>>>(KN, F, q->sort_keys, q->sort_vals));
   size_t bytes = q->sort_tmp_bytes;
   CK(cub::DeviceRadixSort::SortPairs(q->sort_tmp, bytes, q->sort_keys, q->sort_keys2, q->sort_vals, q->perm,
-                                     (int64_t)F, 0, bits, eng->stream));
+                                     (int64_t)F, lo_bit, bits, eng->stream));
   ++eng->launches;
   LAUNCH(eng, k_gather_m<<<g, 256, 0, eng->stream>>>(N.m, q->perm, F, q->m_perm));
   bytes = q->sort_tmp_bytes;
@@ -1573,11 +1595,40 @@ static void run_memo_passes(fjg_query* q) {
   }
   q->mark(eng->stream, -1);
   const unsigned grid = grid_for(std::max<uint64_t>(q->max_n, 1), 256, eng->num_sms * 16);
+  // one initialisation pass per chain trie: every memo array over its groups,
+  // and its dense key map when a pass resolves through it
+  for (auto& [t, gid] : q->gid) {
+    MemoInit I{};
+    I.n = q->tries[t].rel->nrows;
+    I.gid = gid;
+    I.cnt = q->tries[t].dev.lev[0].cnt;
+    if (q->memo_dense.count(t)) {
+      const uint64_t dn = 1ull << std::min(q->tries[t].key_bits, 31);
+      I.dense = q->memo_dense[t];
+      I.dense_n = (uint32_t)dn;
+      I.key = q->tries[t].dev.lev[0].cval[q->tries[t].dev.lev[0].keycol[0]];
+      CK(cudaMemsetAsync(I.dense, 0xff, dn * 4, eng->stream));
+    }
+    for (size_t i = 0; i < q->memo_passes.size(); ++i) {
+      const MemoPass& M = q->memo_passes[i];
+      if (M.gid != gid || !M.n) continue;
+      if (I.nout == kMemoInitMax) {
+        LAUNCH(eng, k_memo_init<<<grid, 256, 0, eng->stream>>>(I));
+        I.nout = 0;
+        I.dense = nullptr;
+      }
+      I.out[I.nout] = M.memo_out;
+      I.group_size[I.nout] = M.nfresh == 0 ? 1 : 0;
+      ++I.nout;
+    }
+    if (I.n && (I.nout || I.dense)) {
+      LAUNCH(eng, k_memo_init<<<grid, 256, 0, eng->stream>>>(I));
+      q->memo_rows[2] += I.n;
+    }
+  }
   for (int i = (int)q->memo_passes.size() - 1; i >= 0; --i) {
     const MemoPass& M = q->memo_passes[i];
     if (!M.n) continue;
-    LAUNCH(eng, k_memo_init<<<grid, 256, 0, eng->stream>>>(M));
-    q->memo_rows[2] += M.n;
     if (M.nfresh == 0) continue;  // every row counts 1: the group sizes, written by k_memo_init
     if (q->memo_resolve_of[i] < 0) {
       LAUNCH(eng, k_memo_resolve<<<grid, 256, 0, eng->stream>>>(M));
@@ -1604,7 +1655,7 @@ static void eager_build(fjg_query* q) {
     // an empty relation has no subtries below its root: its deeper tables were
     // never cleared by a force, so k_eager_list must not read them
     if (T.rel->nrows == 0) continue;
-    const uint64_t nslots = 4 * std::max<uint64_t>(T.rel->nrows, 1);
+    const uint64_t nslots = 4ull * FJG_RS * std::max<uint64_t>(T.rel->nrows, 1);
     for (int l = 1; l < T.map_levels; ++l) {
       uint32_t* cntp = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(q->d_ctr) +
                                                    offsetof(DevCounters, list_count)) +

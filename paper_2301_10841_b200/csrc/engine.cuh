@@ -183,11 +183,29 @@ struct MemoPass {
   KSub fresh[MAXS];
   const uint32_t* gid_next;    // gid of the continuing atom's trie
   uint32_t* child;             // per row: gid of the continuing atom's child, or kMemoMiss
+  const uint32_t* direct;      // dense key -> gid map of the continuing atom's sorted root (or null)
+  uint32_t direct_n;           // its size (keys are 0 .. direct_n - 1)
   uint64_t* coef;              // per row: product of leaf lengths (has_coef), 0 on a miss
   const unsigned long long* memo_next;
   unsigned long long* memo_out;
 };
 constexpr uint32_t kMemoMiss = 0xffffffffu;
+
+// Group initialisation of every memo array over one trie's level-0 groups
+// (one pass over cnt / gid instead of one per chain node) and, for a sorted
+// root whose keys are small non-negative ints, its dense key -> group map.
+constexpr int kMemoInitMax = 8;
+struct MemoInit {
+  uint64_t n;
+  const uint32_t* gid;
+  const uint32_t* cnt;
+  const int32_t* key;          // clustered level-0 key column (for `dense`), or null
+  uint32_t* dense;             // key -> group index, or null
+  uint32_t dense_n;
+  int nout;
+  unsigned long long* out[kMemoInitMax];
+  int group_size[kMemoInitMax];  // 1: write the group size (pass without fresh atoms), 0: zero
+};
 
 struct DevCounters {
   uint64_t count_lo, count_hi, checksum;

@@ -75,11 +75,13 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     uint32_t p, len, pos;
     force_locate(R, i, p, len, pos);
-    uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * pos;
-    t[0] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    t[1] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * FJG_RS * pos;  // this position's buckets
+#pragma unroll
+    for (int u = 0; u < 2 * FJG_RS; ++u) t[u] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     L.cnt[pos] = 0;
-    if (L.srep) reinterpret_cast<uint4*>(L.srep)[pos] = make_uint4(0u, 0u, 0u, 0u);
+    if (L.srep)
+#pragma unroll
+      for (int u = 0; u < FJG_RS; ++u) reinterpret_cast<uint4*>(L.srep)[(uint64_t)FJG_RS * pos + u] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -119,7 +121,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
       const uint32_t kw = key_word_r(nk, vals);
       // the winner's CAS already counts it (rank 0); repeated keys add to the count
       const unsigned long long mine = ((unsigned long long)(kPendBit | 1u) << 32) | kw;
-      const uint64_t lo = 4ull * p, hi = 4ull * ((uint64_t)p + len);
+      const uint64_t lo = 4ull * region_lo(p), hi = 4ull * region_hi(p, len);
       h = 4ull * region_bucket(p, len, kw);
       bool first = R.single;  // roots: wide regions, the home slot is usually free
       while (true) {
@@ -357,9 +359,9 @@ __global__ void k_root_clear(const DevTrie* __restrict__ tries, int trie, uint32
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     L.cnt[i] = 0;
     if (i < G) {
-      uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * i;
-      t[0] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-      t[1] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * FJG_RS * i;
+#pragma unroll
+      for (int u = 0; u < 2 * FJG_RS; ++u) t[u] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr->root_region[trie] = G;
@@ -377,7 +379,7 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
     const uint32_t c = (g + 1 < G ? starts[g + 1] : n) - q;
     const uint32_t kw = skeys[q];
     const uint32_t RG = max(G, 1u);  // region: one bucket per distinct key
-    const uint64_t lo = 0, hi = 4ull * RG;
+    const uint64_t lo = 0, hi = 4ull * region_hi(0u, RG);
     uint64_t h = 4ull * region_bucket(0u, RG, kw);
     const unsigned long long mine = ((unsigned long long)q << 32) | kw;
     while (true) {
@@ -416,7 +418,7 @@ __global__ void k_eager_list(const Slot* __restrict__ table, uint64_t nslots, co
                              const uint32_t* __restrict__ root_region) {
   uint32_t* __restrict__ list_p = child.list_p;
   uint32_t* __restrict__ list_len = child.list_len;
-  if (root_region) nslots = 4ull * *root_region;  // a root's live slots
+  if (root_region) nslots = 4ull * FJG_RS * *root_region;  // a root's live slots
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t q = table[s].q;
     if (q == kEmpty) continue;

@@ -16,15 +16,23 @@ __global__ void k_start_flags(const uint32_t* __restrict__ cnt, uint64_t n, uint
     out[i] = cnt[i] ? 1u : 0u;
 }
 
-// memo_out[g] = 0, or the group size when the pass has no fresh atom (every
-// row of the group contributes 1)
-__global__ void k_memo_init(const __grid_constant__ MemoPass M) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M.n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = __ldg(M.cnt + i);
+// every memo array over one trie's groups: 0, or the group size for a pass
+// without fresh atoms (every row counts 1); plus the dense key -> group map
+__global__ void k_memo_init(const __grid_constant__ MemoInit I) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = __ldg(I.cnt + i);
     if (!c) continue;
-    const uint64_t g = __ldg(M.gid + i) - 1u;
-    M.memo_out[2 * g] = M.nfresh == 0 ? (unsigned long long)c : 0ull;
-    M.memo_out[2 * g + 1] = 0ull;
+    const uint64_t g = __ldg(I.gid + i) - 1u;
+#pragma unroll
+    for (int k = 0; k < kMemoInitMax; ++k)
+      if (k < I.nout) {
+        I.out[k][2 * g] = I.group_size[k] ? (unsigned long long)c : 0ull;
+        I.out[k][2 * g + 1] = 0ull;
+      }
+    if (I.dense) {
+      const uint32_t key = (uint32_t)__ldg(I.key + i);
+      if (key < I.dense_n) I.dense[key] = (uint32_t)g;
+    }
   }
 }
 
@@ -36,6 +44,11 @@ __global__ void __launch_bounds__(256) k_memo_resolve(const __grid_constant__ Me
     int32_t t[MAXK];
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) t[k] = k < M.cnv ? __ldg(M.cvals[k] + pos) : 0;
+    if (M.direct) {  // single continuing fresh atom over a dense sorted root: one read
+      const uint32_t key = (uint32_t)t[M.cpos[0][0]];
+      M.child[pos] = key < M.direct_n ? __ldg(M.direct + key) : kMemoMiss;
+      continue;
+    }
     uint32_t child = kMemoMiss;
     uint64_t coef = 1;
     for (int x = 0; x < M.nfresh; ++x) {

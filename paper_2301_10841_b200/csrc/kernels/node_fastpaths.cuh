@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(TILE) k_last_gj(const __grid_constant__ KNode 
       ++probes;
       const uint32_t kw = (uint32_t)x;
       uint64_t b = region_bucket(sp[s], sl[s], kw);
-      const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+      const uint64_t blo = region_lo(sp[s]), bhi = region_hi(sp[s], sl[s]);
       const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
       uint32_t q = kEmpty;
       while (true) {
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(TILE, NS == 2 ? FJG_GJ_BF_MINB : FJG_GJ_BF_MIN
             uint32_t q = bucket_match(h[r], kw, more);
             if (more) {
               uint64_t b = b0[r];
-              const uint64_t blo = p, bhi = (uint64_t)p + len;
+              const uint64_t blo = region_lo(p), bhi = region_hi(p, len);
               do {
                 if (++b == bhi) b = blo;
                 q = bucket_match(ld_bucket(tb, b), kw, more);
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
       bool more;
       uint32_t q = bucket_match(ld_bucket(tb, b), kw, more);
       while (more) {
-        if (++b == (uint64_t)B.p[j] + B.len[j]) b = B.p[j];
+        if (++b == region_hi(B.p[j], B.len[j])) b = region_lo(B.p[j]);
         q = bucket_match(ld_bucket(tb, b), kw, more);
       }
       if (q == kEmpty) {
@@ -593,13 +593,13 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
           probes += 2;
           bool ma, mb;
           uint32_t qa = bucket_match(ha, (uint32_t)xa, ma), qb = bucket_match(hb, (uint32_t)xb, mb);
-          const uint64_t bhi = (uint64_t)B.p[0] + B.len[0];
+          const uint64_t bhi = region_hi(B.p[0], B.len[0]);
           while (ma) {
-            if (++ba == bhi) ba = B.p[0];
+            if (++ba == bhi) ba = region_lo(B.p[0]);
             qa = bucket_match(ld_bucket(tb, ba), (uint32_t)xa, ma);
           }
           while (mb) {
-            if (++bb == bhi) bb = B.p[0];
+            if (++bb == bhi) bb = region_lo(B.p[0]);
             qb = bucket_match(ld_bucket(tb, bb), (uint32_t)xb, mb);
           }
           misses += (qa == kEmpty) + (qb == kEmpty);
@@ -807,7 +807,7 @@ __device__ __forceinline__ bool gj_write_cand(const KNode& N, uint64_t c0, uint6
     ++probes;
     const uint32_t kw = (uint32_t)x;
     uint64_t b = region_bucket(sp[s], sl[s], kw);
-    const uint64_t blo = sp[s], bhi = (uint64_t)sp[s] + sl[s];
+    const uint64_t blo = region_lo(sp[s]), bhi = region_hi(sp[s], sl[s]);
     bool more;
     uint32_t q = bucket_match(ld_bucket(P.table, b), kw, more);
     while (more) {
@@ -1018,7 +1018,7 @@ __global__ void __launch_bounds__(TILE) k_write_stream(const __grid_constant__ K
         ++probes;
         const uint32_t kw = (uint32_t)key;
         uint64_t b = region_bucket(pp, pl, kw);
-        const uint64_t blo = pp, bhi = (uint64_t)pp + pl;
+        const uint64_t blo = region_lo(pp), bhi = region_hi(pp, pl);
         const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);
         uint32_t q = kEmpty;
         while (true) {
@@ -1133,7 +1133,7 @@ __device__ __forceinline__ uint32_t probe_region_one(const Slot* table, uint32_t
   bool more;
   uint32_t q = bucket_match(ld_bucket(table, b), kw, more);
   while (more) {
-    if (++b == (uint64_t)p + len) b = p;
+    if (++b == region_hi(p, len)) b = region_lo(p);
     q = bucket_match(ld_bucket(table, b), kw, more);
   }
   return q;
@@ -1329,7 +1329,7 @@ __global__ void __launch_bounds__(TILE, FJG_STREAM_MINB) k_stream_one(const __gr
         if (more) {
           uint64_t b = b0[r];
           do {
-            if (++b == (uint64_t)pp[0] + pl[0]) b = pp[0];
+            if (++b == region_hi(pp[0], pl[0])) b = region_lo(pp[0]);
             q = bucket_match(ld_bucket(P0.table, b), kw[r], more);
           } while (more);
         }
