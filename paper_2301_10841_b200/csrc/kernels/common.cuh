@@ -36,6 +36,25 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 #ifndef FJG_RS
 #define FJG_RS 1
 #endif
+// FJG_CHECK=1 (scripts/build_variant.py ... -DFJG_CHECK=1): device-side
+// invariant checks at the probe, force and output sites; a violation traps
+// (the launch fails with an illegal-instruction error naming the kernel).
+// compute-sanitizer is not available on this pool (profiles/r02_checked_build.md).
+#ifndef FJG_CHECK
+#define FJG_CHECK 0
+#endif
+#if FJG_CHECK
+#define FJG_ASSERT(c)                                                                 \
+  do {                                                                                \
+    if (!(c)) {                                                                       \
+      printf("FJG_CHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                      \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define FJG_ASSERT(c) ((void)0)
+#endif
 __device__ __forceinline__ uint64_t region_lo(uint32_t p) { return (uint64_t)p * FJG_RS; }
 __device__ __forceinline__ uint64_t region_hi(uint32_t p, uint32_t len) { return ((uint64_t)p + len) * FJG_RS; }
 __device__ __forceinline__ uint64_t region_bucket(uint32_t p, uint32_t len, uint32_t kw) {
@@ -65,6 +84,7 @@ __device__ __forceinline__ bool colt_get(const KSub& P, uint32_t p, uint32_t len
   const int nk = P.nv;
   const uint32_t kw = key_word_r(nk, key);
   len = probe_region(P, len);
+  FJG_ASSERT(len > 0 && (uint64_t)p + len <= (P.in_p ? (uint64_t)P.root_n : (uint64_t)P.root_n + 1));
   uint64_t b = region_bucket(p, len, kw);
   const uint64_t blo = region_lo(p), bhi = region_hi(p, len);
   const uint4* __restrict__ tb = reinterpret_cast<const uint4*>(P.table);

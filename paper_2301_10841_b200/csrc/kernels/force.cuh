@@ -123,6 +123,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
       const unsigned long long mine = ((unsigned long long)(kPendBit | 1u) << 32) | kw;
       const uint64_t lo = 4ull * region_lo(p), hi = 4ull * region_hi(p, len);
       h = 4ull * region_bucket(p, len, kw);
+      FJG_ASSERT(lo <= h && h < hi && pos >= p && pos < (uint64_t)p + len);
       bool first = R.single;  // roots: wide regions, the home slot is usually free
       while (true) {
         unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.table + h);

@@ -461,6 +461,10 @@ __device__ __forceinline__ void gj_load_bind(const KNode& N, const uint64_t* __r
 #pragma unroll
   for (int s = 1; s < NS; ++s)
     if (s == B.ci) B.cb = sp[s];
+  FJG_ASSERT(B.prev <= B.end && B.ci >= 0 && B.ci < NS);
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    FJG_ASSERT(sp[s] == kSingleton || (uint64_t)sp[s] + sl[s] <= (uint64_t)N.sub[s].root_n + (N.sub[s].in_p ? 0 : 1));
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
     B.p[j] = j >= B.ci ? sp[j + 1] : sp[j];

@@ -18,10 +18,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def build_caller(out_dir):
     exe = os.path.join(out_dir, "capi_multi_main")
-    libdir = os.path.dirname(_capi.LIB_PATH)
+    lib = os.path.abspath(_capi.LIB_PATH)  # the library this process loaded (FJG_LIB honoured)
     subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
-                    os.path.join(ROOT, "tests", "capi_multi_main.cpp"), "-L", libdir, "-l:libfjg.so",
-                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+                    os.path.join(ROOT, "tests", "capi_multi_main.cpp"), lib,
+                    f"-Wl,-rpath,{os.path.dirname(lib)}", "-o", exe], check=True)
     return exe
 
 
