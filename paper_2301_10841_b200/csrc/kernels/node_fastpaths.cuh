@@ -431,7 +431,11 @@ __global__ void k_gather_m(const uint64_t* __restrict__ m, const uint32_t* __res
 // binding by the whole warp (uniform addresses, broadcast loads).
 template <int NS>
 struct GjBind {
-  uint64_t prev, end;   // candidate range [prev, end) of the binding
+  // candidate range [prev, end) of the binding, relative to the launch's c0 in
+  // 32 bits (a launch spans <= 2^31 candidates): end clamped to the launch end,
+  // prev wraps below 0 for a binding that began in an earlier launch (cover
+  // offsets i - prev are computed mod 2^32 and stay exact)
+  uint32_t prev, end;
   uint32_t eb;          // binding index (after the probe-region permutation)
   int ci;               // chosen cover
   uint32_t cb;          // cover subtrie start
@@ -440,9 +444,11 @@ struct GjBind {
 
 template <int NS>
 __device__ __forceinline__ void gj_load_bind(const KNode& N, const uint64_t* __restrict__ scan,
-                                             const uint32_t* __restrict__ perm, uint64_t e, GjBind<NS>& B) {
-  B.end = __ldg(scan + e);
-  B.prev = e ? __ldg(scan + e - 1) : 0ull;
+                                             const uint32_t* __restrict__ perm, uint32_t e, uint64_t c0,
+                                             uint32_t lmax, GjBind<NS>& B) {
+  const uint64_t end = __ldg(scan + e);
+  B.end = (uint32_t)min(end - c0, (uint64_t)lmax);
+  B.prev = (uint32_t)((e ? __ldg(scan + e - 1) : 0ull) - c0);
   B.eb = perm ? __ldg(perm + e) : (uint32_t)e;
   B.ci = N.chosen[B.eb];
   uint32_t sp[NS], sl[NS];
@@ -461,7 +467,7 @@ __device__ __forceinline__ void gj_load_bind(const KNode& N, const uint64_t* __r
 #pragma unroll
   for (int s = 1; s < NS; ++s)
     if (s == B.ci) B.cb = sp[s];
-  FJG_ASSERT(B.prev <= B.end && B.ci >= 0 && B.ci < NS);
+  FJG_ASSERT(end >= c0 && B.ci >= 0 && B.ci < NS);
 #pragma unroll
   for (int s = 0; s < NS; ++s)
     FJG_ASSERT(sp[s] == kSingleton || (uint64_t)sp[s] + sl[s] <= (uint64_t)N.sub[s].root_n + (N.sub[s].in_p ? 0 : 1));
@@ -561,8 +567,9 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
     }
   };
 
-  constexpr uint64_t CH = 64 * RR;
-  const uint64_t nchunks = (c1 - c0 + CH - 1) / CH;
+  constexpr uint32_t CH = 64 * RR;
+  const uint32_t lmax = (uint32_t)(c1 - c0);  // candidates of this launch (<= 2^31)
+  const uint32_t nchunks = (lmax + CH - 1) / CH;
   uint64_t tk = 0, tk_end = 0;
   auto next_chunk = [&]() -> uint64_t {
     if (tk == tk_end) {
@@ -574,15 +581,16 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
     return tk++;
   };
   for (uint64_t ch = next_chunk(); ch < nchunks; ch = next_chunk()) {
-    const uint64_t s0 = c0 + ch * CH, s1 = min(s0 + CH, c1);
-    uint64_t e = __ldg(owner + ch);
+    // candidate positions below are local to the launch: c0 + local
+    const uint32_t s0 = (uint32_t)ch * CH, s1 = min(s0 + CH, lmax);
+    uint32_t e = __ldg(owner + ch);
     GjBind<NS> B;
-    gj_load_bind<NS>(N, scan, perm, e, B);
+    gj_load_bind<NS>(N, scan, perm, e, c0, lmax, B);
 #pragma unroll 1
     for (int rr = 0; rr < RR; ++rr) {
-      const uint64_t base = s0 + 64ull * rr;
+      const uint32_t base = s0 + 64u * rr;
       if (base >= s1) break;
-      while (B.end <= base) gj_load_bind<NS>(N, scan, perm, ++e, B);  // warp-uniform
+      while (B.end <= base) gj_load_bind<NS>(N, scan, perm, ++e, c0, lmax, B);  // warp-uniform
       if (base + 64 <= min(B.end, s1)) {
         const int32_t* __restrict__ cs = (B.ci == 0 ? N.sub[0].src[0] : (B.ci == 1 ? N.sub[1].src[0]
                                                                                    : N.sub[NS - 1].src[0])) +
@@ -629,10 +637,10 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
         // popcounts over the window's end positions and fetches their state
         // with shuffles from the lane that loaded it.
         const unsigned FULL = 0xffffffffu;
-        const uint64_t wend = min(base + 64, s1);
-        const uint64_t ej = e + lane;
+        const uint64_t wend = c0 + min(base + 64, s1);  // absolute, as scan
+        const uint32_t ej = e + lane;
         const uint64_t endj = ej < F ? __ldg(scan + ej) : ~0ull;
-        const uint64_t rel = endj - base;  // >= 1: binding e ends after base
+        const uint64_t rel = endj - (c0 + base);  // >= 1: binding e ends after base
         const bool inwin = endj < wend;
         const unsigned lo_bits = __reduce_or_sync(FULL, inwin && rel < 32 ? 1u << rel : 0u);
         const unsigned hi_bits = __reduce_or_sync(FULL, inwin && rel >= 32 ? 1u << (rel - 32) : 0u);
@@ -641,11 +649,11 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
         if (fits) {
           // lanes 0..nin load the state of bindings e..e+nin
           GjBind<NS> S = B;
-          if (lane > 0 && lane <= nin) gj_load_bind<NS>(N, scan, perm, ej, S);
+          if (lane > 0 && lane <= nin) gj_load_bind<NS>(N, scan, perm, ej, c0, lmax, S);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const uint32_t pos = 32 * t + lane;  // candidate base + pos
-            const uint64_t i = base + pos;
+            const uint32_t i = base + pos;
             const bool live = i < s1;
             const unsigned below = pos >= 31 ? 0xffffffffu : ((2u << pos) - 1u);
             const int seg = t == 0 ? __popc(lo_bits & below)
@@ -669,13 +677,13 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
         } else {
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            const uint64_t i = base + 32 * t + lane;
+            const uint32_t i = base + 32 * t + lane;
             const bool live = i < s1;
             GjBind<NS> L = B;
             if (live && i >= L.end) {
-              uint64_t el = e + 1;
-              while (__ldg(scan + el) <= i) ++el;
-              gj_load_bind<NS>(N, scan, perm, el, L);
+              uint32_t el = e + 1;
+              while (__ldg(scan + el) <= c0 + i) ++el;
+              gj_load_bind<NS>(N, scan, perm, el, c0, lmax, L);
             }
             const int32_t* cs =
                 L.ci == 0 ? N.sub[0].src[0] : (L.ci == 1 ? N.sub[1].src[0] : N.sub[NS - 1].src[0]);
