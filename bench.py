@@ -518,9 +518,11 @@ def run_ours(args):
         last_ms, last_bytes = memo_ms, memo_bytes(r0)
         kernel = "memoised chain passes (k_memo_init / k_memo_resolve / k_memo_gather), one phase"
     achieved = last_bytes / (last_ms / 1000.0) / 1e9 if last_ms > 0 else 0.0
+    # DRAM bytes per launch of the same kernel on the same workload, from this
+    # round's committed ncu capture (profiles/r02_traffic_<workload>.json)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
-    if os.path.exists(tp):
+    tp = os.path.join(ROOT, "profiles", f"r02_traffic_{w.name}.json")
+    if os.path.exists(tp) and world == 1 and dom == "last":
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
 
