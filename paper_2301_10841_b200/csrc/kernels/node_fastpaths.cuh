@@ -500,9 +500,22 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const uint64_t* __restrict__ scan = N.scan;
   const int nhead = N.nhead;
-  uint32_t head = 0;
-  if (lane == 0) Q.tail[wi] = 0;
-  __syncwarp();
+  // ring cursors, warp-uniform registers: entries [head, tail) are pending
+  uint32_t head = 0, tail = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // warp-aggregated enqueue (every lane calls it): one ballot, no atomics
+  auto enqueue = [&](bool hit, int32_t x, uint32_t eb, int ci, const uint32_t (&qv)[NS - 1]) {
+    const unsigned hm = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const uint32_t slot = (tail + __popc(hm & lt_mask)) & (HitQueue<NS>::QC - 1);
+      Q.x[wi][slot] = x;
+      Q.e[wi][slot] = eb;
+      Q.c[wi][slot] = (uint8_t)ci;
+#pragma unroll
+      for (int j = 0; j < NS - 1; ++j) Q.q[j][wi][slot] = qv[j];
+    }
+    tail += __popc(hm);
+  };
 
   auto fold = [&](uint32_t h0, uint32_t n) {
     if ((uint32_t)lane < n) {
@@ -557,14 +570,7 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
       }
       qv[j] = q;
     }
-    if (live) {
-      const uint32_t slot = atomicAdd(&Q.tail[wi], 1u) & (HitQueue<NS>::QC - 1);
-      Q.x[wi][slot] = x;
-      Q.e[wi][slot] = B.eb;
-      Q.c[wi][slot] = (uint8_t)B.ci;
-#pragma unroll
-      for (int j = 0; j < NS - 1; ++j) Q.q[j][wi][slot] = qv[j];
-    }
+    enqueue(live, x, B.eb, B.ci, qv);
   };
 
   constexpr uint32_t CH = 64 * RR;
@@ -615,17 +621,9 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
             qb = bucket_match(ld_bucket(tb, bb), (uint32_t)xb, mb);
           }
           misses += (qa == kEmpty) + (qb == kEmpty);
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const uint32_t q = t ? qb : qa;
-            if (q != kEmpty) {
-              const uint32_t slot = atomicAdd(&Q.tail[wi], 1u) & (HitQueue<NS>::QC - 1);
-              Q.x[wi][slot] = t ? xb : xa;
-              Q.e[wi][slot] = B.eb;
-              Q.c[wi][slot] = (uint8_t)B.ci;
-              Q.q[0][wi][slot] = q;
-            }
-          }
+          const uint32_t qva[NS - 1] = {qa}, qvb[NS - 1] = {qb};
+          enqueue(qa != kEmpty, xa, B.eb, B.ci, qva);
+          enqueue(qb != kEmpty, xb, B.eb, B.ci, qvb);
         } else {
           probe_one(true, xa, B);
           probe_one(true, xb, B);
@@ -694,17 +692,18 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
         }
       }
       // warp-convergent: fold full batches of 32 (at most 64 + 31 pending)
-      __syncwarp();
-      const uint32_t tail = *(volatile uint32_t*)&Q.tail[wi];
-      while (tail - head >= 32) {
-        fold(head, 32);
-        head += 32;
+      if (tail - head >= 32) {
+        __syncwarp();  // the ring entries other lanes wrote
+        do {
+          fold(head, 32);
+          head += 32;
+        } while (tail - head >= 32);
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   __syncwarp();
-  fold(head, *(volatile uint32_t*)&Q.tail[wi] - head);
+  fold(head, tail - head);
   probes = warp_sum(probes);
   misses = warp_sum(misses);
   body = warp_sum(body);
