@@ -1361,8 +1361,8 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (M == 0) return;
   if (is_last) {
     q->mark(eng->stream, -1);
-    const bool gj_any = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
-                        FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
+    const bool gj_any = q->gj_x[k] >= 0 && (mode == EXPAND_COUNT || (mode == EXPAND_ENUM && FJG_GJW)) &&
+                        q->gj_x[k] == (int)q->head.size() - 1 && FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
     uint64_t* gscan = N.scan;
     const uint32_t* perm = gj_any ? probe_region_order(q, k, KN, F, gscan) : nullptr;
     KNode KP = KN;
@@ -1370,8 +1370,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     for (uint64_t c0 = 0; c0 < M; c0 += kLastChunk) {
       const uint64_t c1 = std::min(M, c0 + kLastChunk);
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
-      const bool gj_fast = q->gj_x[k] >= 0 && mode == EXPAND_COUNT && q->gj_x[k] == (int)q->head.size() - 1 &&
-                           FJG_GJ_R > 1 && q->nodes[k].nsub <= 3;
+      const bool gj_fast = gj_any;
       if (gj_fast) {
         chunk_owners(q, gscan, F, c0, c1, FJG_GJW ? 64 * FJG_GJW_RR : 32 * FJG_GJ_R);
         if (FJG_GJ_TICKET)
@@ -1380,7 +1379,24 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       else
         LAUNCH(eng, k_tile_bounds<<<grid_for(ntiles + 1), 256, 0, eng->stream>>>(N.scan, F, c0, c1, q->bounds));
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
-      if (mode == EXPAND_ENUM)
+      if (mode == EXPAND_ENUM && gj_fast) {  // k_last_gj_warp writing the tuples
+        const int W8 = q->head.size() <= 4 ? 4 : 8;
+        const uint64_t nch = (c1 - c0 + 64 * FJG_GJW_RR - 1) / (64 * FJG_GJW_RR);
+        const unsigned gw = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * FJG_GJW_MINB));
+        if (N.nsub == 2 && W8 == 4)
+          LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
+        else if (N.nsub == 2)
+          LAUNCH(eng, (k_last_gj_warp<2, 8, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
+        else if (W8 == 4)
+          LAUNCH(eng, (k_last_gj_warp<3, 4, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
+        else
+          LAUNCH(eng, (k_last_gj_warp<3, 8, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
+      } else if (mode == EXPAND_ENUM)
         LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, q->min_var,
                                                q->out_tuples, q->out_cap, q->d_ctr));
       else if (mode == EXPAND_MEMO)

@@ -487,12 +487,13 @@ __device__ __forceinline__ void gj_load_bind(const KNode& N, const uint64_t* __r
 // registers and costs no per-lane bookkeeping; a step crossing binding ends
 // walks each lane to its own binding. Survivors are folded from the per-warp
 // ring exactly as in k_last_gj_bf.
-template <int NS, int W, int RR>
+template <int NS, int W, int RR, bool ENUMR = false>
 __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __grid_constant__ KNode N, uint64_t c0,
                                                                     uint64_t c1, uint64_t F,
                                                                     const uint32_t* __restrict__ owner,
                                                                     const uint32_t* __restrict__ perm, int min_var,
-                                                                    DevCounters* ctr) {
+                                                                    DevCounters* ctr, int32_t* __restrict__ out_tuples = nullptr,
+                                                                    uint64_t out_cap = 0) {
   static_assert(64 + 63 < HitQueue<NS>::QC, "k_last_gj_warp: survivor ring too small");
   __shared__ HitQueue<NS> Q;
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
@@ -518,6 +519,8 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
   };
 
   auto fold = [&](uint32_t h0, uint32_t n) {
+    int32_t row[W];  // enumerate mode: the output tuple (bound head variables, then x)
+    uint64_t rmu = 0;
     if ((uint32_t)lane < n) {
       const uint32_t slot = (h0 + lane) & (HitQueue<NS>::QC - 1);
       const int32_t x = Q.x[wi][slot];
@@ -539,12 +542,35 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
           const int32_t hvv = __ldg(N.in_var[v] + e);
           pre = fj::tuple_hash_step(pre, (int64_t)hvv);
           if (v == min_var) bmin = hvv;
+          if (ENUMR) row[v] = hvv;
         }
       const uint64_t h = fj::tuple_hash_step(pre, (int64_t)x);
       acc_sum += mu * fj::checksum_word(h);
       acc_lo += mu;
       if (acc_lo < mu) ++acc_hi;
       if (min_var >= 0) acc_min = min(acc_min, min_var == nhead - 1 ? (long long)x : bmin);
+      if (ENUMR) {
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+          if (v == nhead - 1) row[v] = x;
+        rmu = mu;
+      }
+    }
+    if (ENUMR) {  // the batch's rows: one global atomic per warp, lane offsets by scan
+      uint64_t off = rmu;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += o;
+      }
+      const uint64_t total = __shfl_sync(0xffffffffu, off, 31);
+      unsigned long long base = 0;
+      if (lane == 0 && total) base = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)total);
+      base = __shfl_sync(0xffffffffu, base, 0) + off - rmu;
+      for (uint64_t r = 0; r < rmu && base + r < out_cap; ++r)
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+          if (v < nhead) out_tuples[(base + r) * nhead + v] = row[v];
     }
   };
   // probe candidate x of a binding in its probed regions; survivors enqueue
@@ -1406,6 +1432,17 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
     if (own) body[j] += prod;
   }
   const bool narrow = prod <= 0xFFFFFFFFull;
+  // enumerate: the binding's prod * mult rows are reserved with one atomic (by
+  // the thread that owns it, or lane 0 for a warp-expanded binding)
+  unsigned long long obase = 0;
+  if (MODE == EXPAND_ENUM) {
+    if (own) {  // (a big binding's own call only counts: start = ~0, no rows)
+      if (prod && start == 0) obase = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)(prod * mult));
+    } else {
+      if (start == 0 && prod) obase = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)(prod * mult));
+      obase = __shfl_sync(0xffffffffu, obase, 0);
+    }
+  }
   for (uint64_t idx = start; idx < prod; idx += step) {
     uint64_t rest = idx;
 #pragma unroll
@@ -1439,7 +1476,7 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
       if (min_var >= 0) acc_min = min(acc_min, (long long)sel(val, min_var));
     }
     if (MODE == EXPAND_ENUM) {
-      const unsigned long long o = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)mult);
+      const unsigned long long o = obase + idx * mult;
       for (uint64_t r = 0; r < mult && o + r < out_cap; ++r)
 #pragma unroll
         for (int v = 0; v < W; ++v)

@@ -636,3 +636,16 @@ def test_enumerate_single_pass_and_regrow(engine):
         assert bag_equal(rows, ref["tuples"])
     c = qq.execute()
     assert (c.count, c.checksum) == (r.count, r.checksum)
+
+
+@pytest.mark.parametrize("name", ["triangle", "clique4"])
+def test_gj_last_node_enumerate(engine, name):
+    """Enumerate through the GJ warp kernel (k_last_gj_warp<ENUM>): the bag of
+    output tuples equals the oracle's, and the same pass folds count/checksum."""
+    w = {"triangle": lambda: configs.triangle(scale=12, m=40000, seed=6),
+         "clique4": lambda: configs.clique4(scale=11, m=30000)}[name]()
+    q, plan, rels = fjg.prepare_workload(engine, w)
+    rows, r = q.enumerate()
+    ref = oracle.execute(w.query, plan, w.atom_columns(), output_mode="enumerate")
+    assert r.count == len(rows) == ref["count"] and r.checksum == ref["checksum"]
+    assert bag_equal(rows, ref["tuples"])
