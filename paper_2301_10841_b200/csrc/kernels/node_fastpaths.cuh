@@ -1409,7 +1409,7 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
                                             uint32_t step, bool own, int min_var, int32_t* __restrict__ out_tuples,
                                             uint64_t out_cap, DevCounters* ctr, uint64_t& acc_lo, uint64_t& acc_hi,
                                             uint64_t& acc_sum, long long& acc_min, uint64_t (&inputs)[NT],
-                                            uint64_t (&body)[NT]) {
+                                            uint64_t (&body)[NT], unsigned long long obase_in = 0) {
   int32_t val[W];
 #pragma unroll
   for (int v = 0; v < W; ++v) val[v] = ((N.in_vars >> v) & 1u) ? __ldg(N.in_var[v] + e) : 0;
@@ -1436,8 +1436,8 @@ __device__ __forceinline__ void tail_expand(const KNode& N, const TailPlan& T, u
   // the thread that owns it, or lane 0 for a warp-expanded binding)
   unsigned long long obase = 0;
   if (MODE == EXPAND_ENUM) {
-    if (own) {  // (a big binding's own call only counts: start = ~0, no rows)
-      if (prod && start == 0) obase = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)(prod * mult));
+    if (own) {  // reserved by k_tail for its warp (a big binding's own call writes no rows)
+      obase = obase_in;
     } else {
       if (start == 0 && prod) obase = atomicAdd((unsigned long long*)&ctr->out_rows, (unsigned long long)(prod * mult));
       obase = __shfl_sync(0xffffffffu, obase, 0);
@@ -1506,6 +1506,7 @@ __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, 
   for (uint64_t b = (uint64_t)blockIdx.x * TILE; b < F; b += (uint64_t)gridDim.x * TILE) {
     const uint64_t e = b + threadIdx.x;
     bool big = false;
+    unsigned long long own_rows = 0;
     if (e < F) {
       uint64_t prod = 1;
 #pragma unroll
@@ -1516,10 +1517,24 @@ __global__ void __launch_bounds__(TILE) k_tail(const __grid_constant__ KNode N, 
           prod *= p == kSingleton ? 1u : l;
         }
       big = prod > 8;
-      // small products: this thread alone (and it counts the binding's inputs/body)
-      tail_expand<MODE, W, NT>(N, T, e, big ? ~0ull : 0ull, 1u, true, min_var, out_tuples, out_cap, ctr, acc_lo,
-                           acc_hi, acc_sum, acc_min, inputs, body);
+      own_rows = big ? 0ull : prod * (N.in_mult ? __ldg(N.in_mult + e) : 1ull);
     }
+    unsigned long long obase = 0;
+    if (MODE == EXPAND_ENUM) {  // the warp's own rows: one atomic, lane offsets by scan
+      unsigned long long off = own_rows;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += o;
+      }
+      const unsigned long long total = __shfl_sync(0xffffffffu, off, 31);
+      unsigned long long base = 0;
+      if (lane == 0 && total) base = atomicAdd((unsigned long long*)&ctr->out_rows, total);
+      obase = __shfl_sync(0xffffffffu, base, 0) + off - own_rows;
+    }
+    if (e < F)  // small products: this thread alone (and it counts the binding's inputs/body)
+      tail_expand<MODE, W, NT>(N, T, e, big ? ~0ull : 0ull, 1u, true, min_var, out_tuples, out_cap, ctr, acc_lo,
+                           acc_hi, acc_sum, acc_min, inputs, body, obase);
     unsigned bm = __ballot_sync(0xffffffffu, big);
     uint64_t none[NT], nb[NT];
     while (bm) {  // big products: the whole warp strides them
