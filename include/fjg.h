@@ -303,6 +303,13 @@ void fjg_query_destroy(fjg_query* q);
 int fjg_device_tuple_hash(fjg_engine* eng, const int64_t* host_vals, int arity, uint64_t ntuples,
                           uint64_t* host_out);
 uint64_t fjg_host_tuple_hash(const int64_t* vals, int arity);
+/* Runs one hand-written device-wide primitive of the build path on seeded
+ * data and counts the elements that differ from a host restatement:
+ * which = 0 radix sort of (u32 key, u32 value) pairs on key bits [lo, hi)
+ * (stable), 1 inclusive u64 sum (+ total), 2 inclusive u32 max-scan,
+ * 3 flagged index selection (+ count), 4 exclusive u32 sum. */
+int fjg_device_primitive_check(fjg_engine* eng, int which, uint64_t n, int lo, int hi, uint64_t seed,
+                               uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -112,6 +112,7 @@ def _load():
         "fjg_query_output_relation": (I, [P, C.POINTER(P)]),
         "fjg_query_destroy": (None, [P]),
         "fjg_device_tuple_hash": (I, [P, P, I, U64, P]),
+        "fjg_device_primitive_check": (I, [P, I, U64, I, I, U64, P]),
         "fjg_host_tuple_hash": (U64, [P, I]),
         "fjg_parse_csv": (I, [C.c_char_p, I, P, U64, C.POINTER(U64)]),
         "fjg_comm_unique_id": (I, [P]),
@@ -149,7 +150,7 @@ EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_o
             "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition",
             "fjg_relation_partition_into", "fjg_query_create",
             "fjg_execute", "fjg_query_output", "fjg_query_num_head_vars", "fjg_query_output_relation", "fjg_query_destroy",
-            "fjg_device_tuple_hash", "fjg_host_tuple_hash", "fjg_parse_csv", "fjg_comm_unique_id", "fjg_comm_create",
+            "fjg_device_tuple_hash", "fjg_device_primitive_check", "fjg_host_tuple_hash", "fjg_parse_csv", "fjg_comm_unique_id", "fjg_comm_create",
             "fjg_comm_size", "fjg_comm_rank", "fjg_comm_destroy", "fjg_sharded_create", "fjg_execute_multi",
             "fjg_sharded_destroy", "fjg_exchange_layout", "fjg_colt_create", "fjg_colt_levels", "fjg_colt_force",
             "fjg_colt_get", "fjg_colt_iter", "fjg_colt_rows", "fjg_colt_estimated_key_count", "fjg_colt_destroy"]

@@ -27,8 +27,6 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 #include <map>
 #include <memory>
 #include <set>
@@ -63,6 +61,7 @@ static void throw_cuda(cudaError_t e, const char* what, int line) {
     if (_e != cudaSuccess) throw_cuda(_e, #x, __LINE__); \
   } while (0)
 
+#include "kernels/prims.cuh"
 #include "kernels/common.cuh"
 #include "kernels/select.cuh"
 #include "kernels/force.cuh"
@@ -168,6 +167,18 @@ struct fjg_engine {
   uint32_t syncs = 0;
   int num_sms = 148;
   DevCounters* h_ctr = nullptr;  // pinned; shared by the engine's queries (execute is synchronous)
+  // device-wide primitives (kernels/prims.cuh), all on `stream`: tile ticket
+  // counter (never reset; the host keeps the running base), look-back words of
+  // the scans and of the radix passes (separate regions: epochs are compared
+  // against words of one layout only), radix histograms
+  unsigned long long* prim_ticket = nullptr;
+  uint64_t prim_tbase = 0;
+  uint32_t prim_epoch = 0;
+  void* prim_lb_scan = nullptr;
+  size_t prim_lb_scan_bytes = 0;
+  void* prim_lb_radix = nullptr;
+  size_t prim_lb_radix_bytes = 0;
+  uint32_t* prim_hist = nullptr;
 };
 
 struct fjg_relation {
@@ -204,6 +215,106 @@ static bool debug_sync() {
     CK(cudaGetLastError());                                        \
     if (debug_sync()) CK(cudaStreamSynchronize((eng)->stream));    \
   } while (0)
+
+// ---------------------------------------------------------------------------
+// device-wide primitives (kernels/prims.cuh) on the engine stream
+// ---------------------------------------------------------------------------
+static uint32_t prim_epoch(fjg_engine* eng) {
+  if (++eng->prim_epoch >= (1u << 30)) {  // 30-bit epochs wrapped: clear the look-back words
+    eng->prim_epoch = 1;
+    if (eng->prim_lb_scan) CK(cudaMemsetAsync(eng->prim_lb_scan, 0, eng->prim_lb_scan_bytes, eng->stream));
+    if (eng->prim_lb_radix) CK(cudaMemsetAsync(eng->prim_lb_radix, 0, eng->prim_lb_radix_bytes, eng->stream));
+  }
+  return eng->prim_epoch;
+}
+static void* prim_region(fjg_engine* eng, void*& p, size_t& have, size_t bytes) {
+  if (bytes > have) {
+    eng->pool->free(p);
+    p = eng->pool->alloc(bytes);
+    have = bytes;
+    CK(cudaMemsetAsync(p, 0, bytes, eng->stream));  // no stale word can carry a live epoch
+  }
+  return p;
+}
+
+// out[i] = Op(in[0..i]) (EXCL: Op(in[0..i-1])); in may alias out; *total (device,
+// optional) = Op(in[0..n)).
+template <class Op, bool EXCL, class In, class T>
+static void prim_scan(fjg_engine* eng, const In* in, T* out, uint64_t n, T* total = nullptr) {
+  if (n == 0) {
+    if (total) CK(cudaMemsetAsync(total, 0, sizeof(T), eng->stream));
+    return;
+  }
+  const uint64_t tiles = (n + prims::kScanTile - 1) / prims::kScanTile;
+  if (tiles > 0x7fffffffull) throw fj::ValidationError("scan too large");
+  auto* st = (prims::LBTile*)prim_region(eng, eng->prim_lb_scan, eng->prim_lb_scan_bytes,
+                                          tiles * sizeof(prims::LBTile));
+  const uint32_t ep = prim_epoch(eng);
+  LAUNCH(eng, (prims::k_scan_lb<In, T, Op, EXCL><<<(unsigned)tiles, prims::kScanThreads, 0, eng->stream>>>(
+                  in, out, n, st, eng->prim_ticket, eng->prim_tbase, ep, total)));
+  eng->prim_tbase += tiles;
+}
+
+// out[j] = the j-th index i (ascending) with flags[i] != 0; *count (device) = how many.
+static void prim_select_flagged(fjg_engine* eng, const uint8_t* flags, uint32_t* out, uint64_t n, uint32_t* count) {
+  if (n == 0) {
+    CK(cudaMemsetAsync(count, 0, 4, eng->stream));
+    return;
+  }
+  const uint64_t tiles = (n + prims::kSelTile - 1) / prims::kSelTile;
+  auto* st = (prims::LBTile*)prim_region(eng, eng->prim_lb_scan, eng->prim_lb_scan_bytes,
+                                          tiles * sizeof(prims::LBTile));
+  const uint32_t ep = prim_epoch(eng);
+  LAUNCH(eng, (prims::k_select_flagged<<<(unsigned)tiles, prims::kScanThreads, 0, eng->stream>>>(
+                  flags, out, n, st, eng->prim_ticket, eng->prim_tbase, ep, count)));
+  eng->prim_tbase += tiles;
+}
+
+// *out (device) = max over in[0..n) (0 when n == 0).
+static void prim_max_u32(fjg_engine* eng, const uint32_t* in, uint64_t n, uint32_t* out) {
+  CK(cudaMemsetAsync(out, 0, 4, eng->stream));
+  if (n) LAUNCH(eng, prims::k_reduce_max_u32<<<grid_for(n, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(in, n, out));
+}
+
+// Radix passes of a sort on key bits [lo, hi): 9-bit digits at most.
+static int prim_sort_passes(int lo, int hi) { return hi > lo ? (hi - lo + 8) / 9 : 0; }
+
+// Stable sort of (k0, v0)[0..n) on key bits [lo, hi) (keys must have no bit
+// set at or above hi), ping-ponging with (k1, v1). Returns which pair holds
+// the result: 0 = (k0, v0) (an even number of passes), 1 = (k1, v1).
+static int prim_sort_pairs(fjg_engine* eng, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint64_t n,
+                           int lo, int hi) {
+  const int np = prim_sort_passes(lo, hi);
+  if (n <= 1 || np == 0) return 0;
+  if (np > prims::kRadixMaxPasses) throw fj::EngineError("radix sort: too many key bits");
+  if (n >= (1ull << 32) - 16) throw fj::ValidationError("radix sort: at most 2^32-16 pairs");
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(prims::k_radix_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)prims::kRadixSmem));
+    attr = true;
+  }
+  const int db = (hi - lo + np - 1) / np;
+  CK(cudaMemsetAsync(eng->prim_hist, 0, (size_t)np * prims::kRadixBins * 4, eng->stream));
+  LAUNCH(eng, prims::k_radix_hist<<<grid_for(n / 4 + 1, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(
+                  k0, n, lo, db, np, hi, eng->prim_hist));
+  const uint64_t tiles = (n + prims::kRadixTile - 1) / prims::kRadixTile;
+  auto* st = (unsigned long long*)prim_region(eng, eng->prim_lb_radix, eng->prim_lb_radix_bytes,
+                                              tiles * prims::kRadixBins * 8);
+  uint32_t *ks = k0, *vs = v0, *kd = k1, *vd = v1;
+  for (int p = 0; p < np; ++p) {
+    const int shift = lo + p * db;
+    const int bits = std::min(db, hi - shift);
+    const uint32_t ep = prim_epoch(eng);
+    LAUNCH(eng, (prims::k_radix_pass<<<(unsigned)tiles, prims::kRadixThreads, prims::kRadixSmem, eng->stream>>>(
+                    ks, vs, kd, vd, n, shift, bits, eng->prim_hist + p * prims::kRadixBins, st, eng->prim_ticket,
+                    eng->prim_tbase, ep)));
+    eng->prim_tbase += tiles;
+    std::swap(ks, kd);
+    std::swap(vs, vd);
+  }
+  return np & 1;
+}
 
 struct PhysLevelHost {
   std::vector<int> keycols;
@@ -254,8 +365,6 @@ struct fjg_query {
   uint32_t* newslot_p = nullptr;
   uint32_t* owner_scratch = nullptr;  // force: offset index -> claimed subtrie
   uint8_t* sort_flags = nullptr;      // sorted root force: group-start flags
-  void* cub_tmp = nullptr;
-  size_t cub_tmp_bytes = 0;
   int32_t* out_tuples = nullptr;
   uint64_t out_cap = 0;
   uint64_t out_rows = 0;
@@ -297,8 +406,6 @@ struct fjg_query {
   // GJ last node in probe-region order (FJG_GJ_SORT): keys, binding permutation, permuted m / scan
   uint32_t *sort_keys = nullptr, *sort_keys2 = nullptr, *sort_vals = nullptr, *perm = nullptr;
   uint64_t *m_perm = nullptr, *scan_perm = nullptr;
-  void* sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
   uint64_t sort_cap = 0;
   int backend = FJG_BACKEND_COLT;
   // non-blocking phase timer: event pairs resolved after the final sync
@@ -551,14 +658,10 @@ static void prepare_query(fjg_query* q) {
   if (!sorted.empty()) {
     fjg_engine* eng = q->eng;
     uint32_t* dmax = (uint32_t*)eng->pool->alloc(sorted.size() * 4);
-    size_t need = 0;
-    CK(cub::DeviceReduce::Max(nullptr, need, (const uint32_t*)nullptr, dmax, (int64_t)q->max_n, eng->stream));
-    void* tmp = eng->pool->alloc(std::max<size_t>(need, 16));
     for (size_t i = 0; i < sorted.size(); ++i) {
       auto& T = q->tries[sorted[i]];
       const uint32_t* col = reinterpret_cast<const uint32_t*>(T.dev.base[T.dev.lev[0].keycol[0]]);
-      size_t bytes = need;
-      CK(cub::DeviceReduce::Max(tmp, bytes, col, dmax + i, (int64_t)T.rel->nrows, eng->stream));
+      prim_max_u32(eng, col, T.rel->nrows, dmax + i);
     }
     std::vector<uint32_t> hmax(sorted.size());
     CK(cudaMemcpyAsync(hmax.data(), dmax, sorted.size() * 4, cudaMemcpyDeviceToHost, eng->stream));
@@ -568,7 +671,6 @@ static void prepare_query(fjg_query* q) {
       while (bits < 32 && (hmax[i] >> bits)) ++bits;
       q->tries[sorted[i]].key_bits = bits;
     }
-    eng->pool->free(tmp);
     eng->pool->free(dmax);
   }
 }
@@ -891,26 +993,6 @@ static void ensure_frontiers(fjg_query* q, uint64_t cap) {
     q->chunk_owner = (uint32_t*)q->alloc((std::max<uint64_t>(cap, kLastChunk) / 32 + 2) * 4);
     q->bounds_cap = nb;
   }
-  // CUB temp storage for the largest scans
-  size_t b1 = 0, b2 = 0;
-  CK(cub::DeviceScan::InclusiveSum(nullptr, b1, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)cap));
-  CK(cub::DeviceScan::InclusiveSum(nullptr, b2, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                   (int64_t)std::max<uint64_t>(q->max_n, 1)));
-  size_t b3 = 0;
-  CK(cub::DeviceScan::InclusiveScan(nullptr, b3, (uint32_t*)nullptr, (uint32_t*)nullptr, MaxOp(),
-                                    (int64_t)std::max<uint64_t>(std::max<uint64_t>(q->max_n, 1),
-                                                                std::max<uint64_t>(cap, kLastChunk) / 32 + 2)));
-  size_t b4 = 0, b5 = 0;
-  const int64_t nm = (int64_t)std::max<uint64_t>(q->max_n, 1);
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, b4, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                     (uint32_t*)nullptr, nm));
-  CK(cub::DeviceSelect::Flagged(nullptr, b5, thrust::counting_iterator<uint32_t>(0), (uint8_t*)nullptr,
-                                (uint32_t*)nullptr, (uint32_t*)nullptr, nm));
-  size_t need = std::max(std::max(std::max(b1, b2), b3), std::max(b4, b5));
-  if (need > q->cub_tmp_bytes) {
-    q->cub_tmp = q->alloc(need);
-    q->cub_tmp_bytes = need;
-  }
   build_knodes(q);
   if (q->chain_start < 0 && q->memo_passes.empty()) prepare_chain(q);
   else if (q->chain_start >= 1) {  // frontier pointers moved: refresh the top node
@@ -960,16 +1042,17 @@ static void force_root_sorted(fjg_query* q, int t) {
       srows = reinterpret_cast<uint32_t*>(L0.cval[oc]);
     }
   }
-  LAUNCH(eng, k_root_keys<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, keys, rows, pay));
-  size_t bytes = q->cub_tmp_bytes;
+  // hand-written LSD radix sort (kernels/prims.cuh) over the key bits the column
+  // uses; the pair the keys start in is chosen so the last pass lands in
+  // (skeys, srows)
   const int kb = T.levels[0].empty() ? 1 : T.key_bits;
-  CK(cub::DeviceRadixSort::SortPairs(q->cub_tmp, bytes, keys, skeys, rows, srows, (int64_t)n, 0, kb, eng->stream));
-  ++eng->launches;
+  const bool even = n <= 1 || prim_sort_passes(0, kb) % 2 == 0;
+  uint32_t* k0 = even ? skeys : keys;
+  uint32_t* v0 = even ? srows : rows;
+  LAUNCH(eng, k_root_keys<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, k0, v0, pay));
+  prim_sort_pairs(eng, k0, v0, even ? keys : skeys, even ? rows : srows, n, 0, kb);
   LAUNCH(eng, k_root_starts<<<g, 256, 0, eng->stream>>>(skeys, n, flags));
-  bytes = q->cub_tmp_bytes;
-  CK(cub::DeviceSelect::Flagged(q->cub_tmp, bytes, thrust::counting_iterator<uint32_t>(0), flags, starts, ng,
-                                (int64_t)n, eng->stream));
-  ++eng->launches;
+  prim_select_flagged(eng, flags, starts, n, ng);
   // the root's slot region shrinks to one bucket per distinct key (load <= 0.25)
   LAUNCH(eng, k_root_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, ng, q->d_ctr));
   LAUNCH(eng, k_root_insert<<<g, 256, 0, eng->stream>>>(q->d_tries, t, n, skeys, starts, ng, q->d_ctr));
@@ -991,10 +1074,7 @@ static void chunk_owners(fjg_query* q, const uint64_t* scan, uint64_t F, uint64_
   CK(cudaMemsetAsync(q->chunk_owner, 0, n * 4, eng->stream));
   LAUNCH(eng, k_chunk_marks<<<grid_for(std::min<uint64_t>(F, (c1 - c0 + chunk - 1) / chunk + 1)), 256, 0,
                               eng->stream>>>(scan, F, c0, c1, chunk, q->chunk_owner));
-  size_t bytes = q->cub_tmp_bytes;
-  CK(cub::DeviceScan::InclusiveScan(q->cub_tmp, bytes, q->chunk_owner, q->chunk_owner, MaxOp(), (int64_t)n,
-                                    eng->stream));
-  ++eng->launches;
+  prim_scan<prims::OpMax, false>(eng, q->chunk_owner, q->chunk_owner, n);
 }
 
 // Launch a force batch (clear -> insert -> assign -> scatter, blockIdx.y =
@@ -1095,9 +1175,7 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     R.list_count = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(q->d_ctr) +
                                                      offsetof(DevCounters, list_count)) +
                    (t * MAXL + l);
-    size_t bytes = q->cub_tmp_bytes;
-    CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, L.list_len, L.list_scan, (int64_t)count, eng->stream));
-    ++eng->launches;
+    prim_scan<prims::OpSum, false>(eng, L.list_len, L.list_scan, count);
     // offsets to force: the claims' total when k_select counted it, else the level
     const uint32_t claimed = q->h_ctr->list_total[t * MAXL + l];
     upper = claimed ? std::min<uint64_t>(claimed, T.rel->nrows) : T.rel->nrows;
@@ -1105,10 +1183,7 @@ static void force_level(fjg_query* q, int t, int l, bool single, uint32_t p0, ui
     CK(cudaMemsetAsync(q->owner_scratch, 0, std::max<uint64_t>(upper, 1) * 4, eng->stream));
     LAUNCH(eng, k_force_marks<<<grid_for(count), 256, 0, eng->stream>>>(L.list_scan, R.list_count,
                                                                          q->owner_scratch));
-    bytes = q->cub_tmp_bytes;
-    CK(cub::DeviceScan::InclusiveScan(q->cub_tmp, bytes, q->owner_scratch, q->owner_scratch, MaxOp(),
-                                      (int64_t)upper, eng->stream));
-    ++eng->launches;
+    prim_scan<prims::OpMax, false>(eng, q->owner_scratch, q->owner_scratch, upper);
     R.owner = q->owner_scratch;
   }
   launch_force_batch(q, B, upper, single, T.lev[l].multi);
@@ -1147,11 +1222,6 @@ static const uint32_t* probe_region_order(fjg_query* q, int k, const KNode& KN, 
     q->perm = (uint32_t*)q->alloc(F * 4);
     q->m_perm = (uint64_t*)q->alloc(F * 8);
     q->scan_perm = (uint64_t*)q->alloc(F * 8);
-    size_t b1 = 0, b2 = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, q->sort_keys, q->sort_keys2, q->sort_vals, q->perm, (int64_t)F));
-    CK(cub::DeviceScan::InclusiveSum(nullptr, b2, q->m_perm, q->scan_perm, (int64_t)F));
-    q->sort_tmp_bytes = std::max(b1, b2);
-    q->sort_tmp = q->alloc(q->sort_tmp_bytes);
     q->sort_cap = F;
   }
   int bits = 1;
@@ -1161,16 +1231,13 @@ static const uint32_t* probe_region_order(fjg_query* q, int k, const KNode& KN, 
   const int lo_bit = std::max(0, bits - FJG_GJ_SORT_BITS);
   const unsigned g = grid_for(F, 256, eng->num_sms * 16);
   LAUNCH(eng, k_probe_keys<2><<<g, 256, 0, eng->stream>>>(KN, F, q->sort_keys, q->sort_vals));
-  size_t bytes = q->sort_tmp_bytes;
-  CK(cub::DeviceRadixSort::SortPairs(q->sort_tmp, bytes, q->sort_keys, q->sort_keys2, q->sort_vals, q->perm,
-                                     (int64_t)F, lo_bit, bits, eng->stream));
-  ++eng->launches;
-  LAUNCH(eng, k_gather_m<<<g, 256, 0, eng->stream>>>(N.m, q->perm, F, q->m_perm));
-  bytes = q->sort_tmp_bytes;
-  CK(cub::DeviceScan::InclusiveSum(q->sort_tmp, bytes, q->m_perm, q->scan_perm, (int64_t)F, eng->stream));
-  ++eng->launches;
+  const uint32_t* perm = prim_sort_pairs(eng, q->sort_keys, q->sort_vals, q->sort_keys2, q->perm, F, lo_bit, bits)
+                             ? q->perm
+                             : q->sort_vals;
+  LAUNCH(eng, k_gather_m<<<g, 256, 0, eng->stream>>>(N.m, perm, F, q->m_perm));
+  prim_scan<prims::OpSum, false>(eng, q->m_perm, q->scan_perm, F);
   scan_out = q->scan_perm;
-  return q->perm;
+  return perm;
 }
 
 static void run_node(fjg_query* q, int k, uint64_t F, int mode);
@@ -1348,11 +1415,9 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
   if (F <= kSmallScan) {
     LAUNCH(eng, k_scan_small<<<1, 1024, 0, eng->stream>>>(N.m, N.scan, (uint32_t)F, q->d_ctr));
   } else {
-    size_t bytes = q->cub_tmp_bytes;
-    CK(cub::DeviceScan::InclusiveSum(q->cub_tmp, bytes, N.m, N.scan, (int64_t)F, eng->stream));
-    ++eng->launches;
-    CK(cudaMemcpyAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, total_m), N.scan + (F - 1), 8,
-                       cudaMemcpyDeviceToDevice, eng->stream));
+    prim_scan<prims::OpSum, false>(eng, N.m, N.scan, F,
+                                   reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(q->d_ctr) +
+                                                               offsetof(DevCounters, total_m)));
   }
   sync_counters(q);
   }
@@ -1602,12 +1667,7 @@ static void run_memo_passes(fjg_query* q) {
     const uint64_t n = q->tries[t].rel->nrows;
     if (!n) continue;
     LAUNCH(eng, k_start_flags<<<grid_for(n), 256, 0, eng->stream>>>(q->tries[t].dev.lev[0].cnt, n, gid));
-    size_t bytes = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, gid, gid, (int64_t)n));
-    void* tmp = eng->pool->alloc(bytes);
-    CK(cub::DeviceScan::InclusiveSum(tmp, bytes, gid, gid, (int64_t)n, eng->stream));
-    ++eng->launches;
-    eng->pool->free(tmp);
+    prim_scan<prims::OpSum, false>(eng, gid, gid, n);
   }
   q->mark(eng->stream, -1);
   const unsigned grid = grid_for(std::max<uint64_t>(q->max_n, 1), 256, eng->num_sms * 16);
@@ -1794,6 +1854,9 @@ int fjg_engine_create(int device, fjg_engine** out) {
     CK(cudaGetDeviceProperties(&prop, device));
     e->num_sms = prop.multiProcessorCount;
     CK(cudaMallocHost(&e->h_ctr, sizeof(DevCounters)));
+    e->prim_ticket = (unsigned long long*)e->pool->alloc(8);
+    e->prim_hist = (uint32_t*)e->pool->alloc(prims::kRadixMaxPasses * prims::kRadixBins * 4);
+    CK(cudaMemsetAsync(e->prim_ticket, 0, 8, e->stream));
     *out = e;
   });
 }
@@ -1883,16 +1946,10 @@ int fjg_relation_filter(const fjg_relation* in, const fjg_predicate* preds, int 
     uint32_t total = 0;
     if (n) {
       LAUNCH(eng, k_filter_flags<<<grid_for(n), 256, 0, eng->stream>>>(P, n, flags));
-      size_t bytes = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, excl, (int64_t)n));
-      void* tmp = eng->pool->alloc(bytes);
-      CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, flags, excl, (int64_t)n, eng->stream));
-      uint32_t last[2];
-      CK(cudaMemcpyAsync(&last[0], excl + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
-      CK(cudaMemcpyAsync(&last[1], flags + n - 1, 4, cudaMemcpyDeviceToHost, eng->stream));
+      uint32_t* d_total = excl + std::max<uint64_t>(n, 1);
+      prim_scan<prims::OpSum, true>(eng, flags, excl, n, d_total);
+      CK(cudaMemcpyAsync(&total, d_total, 4, cudaMemcpyDeviceToHost, eng->stream));
       CK(cudaStreamSynchronize(eng->stream));
-      total = last[0] + last[1];
-      eng->pool->free(tmp);
     }
     fjg_relation* r = new_relation(eng, in->ncols, total);
     for (int c = 0; c < in->ncols && n; ++c)
@@ -1928,15 +1985,11 @@ static void partition_async(const fjg_relation* in, int col, int nparts, int32_t
   const uint64_t nh = (uint64_t)nparts * nblocks;
   uint32_t* hist = (uint32_t*)eng->pool->alloc((nh + 1) * 4);
   uint32_t* offs = (uint32_t*)eng->pool->alloc((nh + 1) * 4);
-  size_t bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, offs, (int64_t)(nh + 1)));
-  void* tmp = eng->pool->alloc(bytes);
   const size_t smem = (size_t)nparts * 4 * (PART_WARPS + 1);
   CK(cudaMemsetAsync(hist + nh, 0, 4, eng->stream));
   LAUNCH(eng, k_part_count<<<nblocks, 256, (size_t)nparts * 4, eng->stream>>>(in->cols[col], n, nparts, nblocks,
                                                                               hist));
-  CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, hist, offs, (int64_t)(nh + 1), eng->stream));
-  ++eng->launches;
+  prim_scan<prims::OpSum, true>(eng, hist, offs, nh + 1);
   DevPartCols pc{};
   pc.ncols = in->ncols;
   for (int c = 0; c < in->ncols; ++c) {
@@ -1948,7 +2001,6 @@ static void partition_async(const fjg_relation* in, int col, int nparts, int32_t
   // stream-ordered pool: later allocations on this stream run after these kernels
   eng->pool->free(hist);
   eng->pool->free(offs);
-  eng->pool->free(tmp);
 }
 
 static void partition_into(const fjg_relation* in, int col, int nparts, int32_t* const* out_cols, uint64_t* counts) {
@@ -2173,6 +2225,112 @@ int fjg_device_tuple_hash(fjg_engine* eng, const int64_t* host_vals, int arity, 
     CK(cudaStreamSynchronize(eng->stream));
     eng->pool->free(dv);
     eng->pool->free(dout);
+  });
+}
+
+// Test hook: run one device-wide primitive (kernels/prims.cuh) on seeded
+// host-generated data and count the elements that differ from a host
+// restatement (std::stable_sort / sequential scans).
+int fjg_device_primitive_check(fjg_engine* eng, int which, uint64_t n, int lo, int hi, uint64_t seed,
+                               uint64_t* mismatches) {
+  return guard([&] {
+    ScopedDevice sd(eng->device);
+    if (which < 0 || which > 4) throw fj::ValidationError("primitive must be 0..4");
+    if (lo < 0 || hi > 32 || lo > hi) throw fj::ValidationError("bit range must satisfy 0 <= lo <= hi <= 32");
+    uint64_t x = seed * 0x9e3779b97f4a7c15ull + 1;
+    auto next = [&]() {
+      x += 0x9e3779b97f4a7c15ull;
+      uint64_t z = x;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      return z ^ (z >> 31);
+    };
+    const size_t nb = std::max<uint64_t>(n, 1);
+    uint64_t bad = 0;
+    if (which == 0) {  // radix sort of (key, index) pairs on bits [lo, hi), skewed keys
+      std::vector<uint32_t> k(n), v(n);
+      const uint64_t km = hi == 32 ? 0xffffffffull : ((1ull << hi) - 1);
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t r = next();
+        k[i] = (uint32_t)(((r & 3) == 0 ? (r >> 8) % 7 : (r >> 8)) & km);  // a quarter of the keys on 7 values
+        v[i] = (uint32_t)i;
+      }
+      uint32_t* d = (uint32_t*)eng->pool->alloc(nb * 16);
+      CK(cudaMemcpyAsync(d, k.data(), n * 4, cudaMemcpyHostToDevice, eng->stream));
+      CK(cudaMemcpyAsync(d + nb, v.data(), n * 4, cudaMemcpyHostToDevice, eng->stream));
+      const int r = prim_sort_pairs(eng, d, d + nb, d + 2 * nb, d + 3 * nb, n, lo, hi);
+      std::vector<uint32_t> gk(n), gv(n);
+      CK(cudaMemcpyAsync(gk.data(), d + 2 * nb * r, n * 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaMemcpyAsync(gv.data(), d + nb + 2 * nb * r, n * 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      eng->pool->free(d);
+      const uint64_t dm = (hi - lo == 32) ? 0xffffffffull : (((1ull << (hi - lo)) - 1) << lo);
+      std::vector<uint32_t> idx(n);
+      for (uint64_t i = 0; i < n; ++i) idx[i] = (uint32_t)i;
+      std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return (k[a] & dm) < (k[b] & dm); });
+      for (uint64_t i = 0; i < n; ++i) bad += (gk[i] != k[idx[i]] || gv[i] != v[idx[i]]) ? 1 : 0;
+    } else if (which == 1) {  // inclusive sum of u64 (large values), total
+      std::vector<uint64_t> a(n), g(n);
+      for (uint64_t i = 0; i < n; ++i) a[i] = next() >> 20;
+      uint64_t* d = (uint64_t*)eng->pool->alloc(nb * 8 + 8);
+      CK(cudaMemcpyAsync(d, a.data(), n * 8, cudaMemcpyHostToDevice, eng->stream));
+      prim_scan<prims::OpSum, false>(eng, d, d, n, d + nb);
+      uint64_t tot = 0;
+      CK(cudaMemcpyAsync(g.data(), d, n * 8, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaMemcpyAsync(&tot, d + nb, 8, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      eng->pool->free(d);
+      uint64_t run = 0;
+      for (uint64_t i = 0; i < n; ++i) {
+        run += a[i];
+        bad += g[i] != run ? 1 : 0;
+      }
+      bad += tot != run ? 1 : 0;
+    } else if (which == 2 || which == 4) {  // inclusive max-scan / exclusive sum of u32
+      std::vector<uint32_t> a(n), g(n);
+      for (uint64_t i = 0; i < n; ++i) a[i] = which == 2 ? ((next() & 7) == 0 ? (uint32_t)i : 0u) : (uint32_t)(next() & 15);
+      uint32_t* d = (uint32_t*)eng->pool->alloc(nb * 8 + 8);
+      CK(cudaMemcpyAsync(d, a.data(), n * 4, cudaMemcpyHostToDevice, eng->stream));
+      if (which == 2)
+        prim_scan<prims::OpMax, false>(eng, d, d + nb, n);
+      else
+        prim_scan<prims::OpSum, true>(eng, d, d + nb, n);
+      CK(cudaMemcpyAsync(g.data(), d + nb, n * 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      eng->pool->free(d);
+      uint32_t run = 0;
+      for (uint64_t i = 0; i < n; ++i) {
+        if (which == 4) {
+          bad += g[i] != run ? 1 : 0;
+          run += a[i];
+        } else {
+          run = std::max(run, a[i]);
+          bad += g[i] != run ? 1 : 0;
+        }
+      }
+    } else {  // flagged selection of indices
+      std::vector<uint8_t> f(n);
+      for (uint64_t i = 0; i < n; ++i) f[i] = (next() % 5) == 0 ? (uint8_t)(1 + (i & 7)) : 0;
+      uint8_t* df = (uint8_t*)eng->pool->alloc(nb);
+      uint32_t* d = (uint32_t*)eng->pool->alloc(nb * 4 + 4);
+      CK(cudaMemcpyAsync(df, f.data(), n, cudaMemcpyHostToDevice, eng->stream));
+      prim_select_flagged(eng, df, d, n, d + nb);
+      std::vector<uint32_t> g(n);
+      uint32_t cnt = 0;
+      CK(cudaMemcpyAsync(&cnt, d + nb, 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      if (cnt <= n) CK(cudaMemcpy(g.data(), d, (size_t)cnt * 4, cudaMemcpyDeviceToHost));
+      eng->pool->free(df);
+      eng->pool->free(d);
+      uint64_t j = 0;
+      for (uint64_t i = 0; i < n; ++i)
+        if (f[i]) {
+          bad += (j >= cnt || g[j] != i) ? 1 : 0;
+          ++j;
+        }
+      bad += j != cnt ? 1 : 0;
+    }
+    *mismatches = bad;
   });
 }
 

@@ -172,9 +172,8 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
   }
   // new keys and the repeated-key flag: one atomic per block (k_force_assign
   // finds the new slots as the rank-0 offsets, so no slot list is appended)
-  typedef cub::BlockReduce<uint32_t, 256> BR;
-  __shared__ typename BR::TempStorage rtmp;
-  const uint32_t bw = BR(rtmp).Sum(wins);
+  __shared__ uint32_t rtmp[8];
+  const uint32_t bw = prims::block_sum<256>(wins, rtmp);
   if (threadIdx.x == 0 && bw) atomicAdd(&ctr->fnew[y], bw);
   if (__syncthreads_or(sawdup) && threadIdx.x == 0) {
     ctr->fdup[y] = 1u;
@@ -195,8 +194,7 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, const __grid_c
   tmp_rank += R.slot_off;
   const DevLevel& L = tries[R.trie].lev[R.lev];
   const uint32_t total = force_total(R);
-  typedef cub::BlockScan<uint32_t, 256> BS;
-  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t tmp[8];
   __shared__ uint32_t s_base;
   const uint32_t stride = gridDim.x * blockDim.x;
   const uint32_t iters = (total + stride - 1) / stride;
@@ -217,7 +215,7 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, const __grid_c
     uint32_t q = 0;
     if (SINGLE) {
       uint32_t excl, blk_total;
-      BS(tmp).ExclusiveSum(c, excl, blk_total);
+      excl = prims::block_excl_scan<256>(c, blk_total, tmp, prims::OpSum(), 0u);
       const uint32_t nb = __syncthreads_count(ok);
       if (threadIdx.x == 0 && nb) {
         s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);

@@ -172,7 +172,4 @@ __global__ void __launch_bounds__(256) k_memo_total(const uint32_t* __restrict__
   }
 }
 
-struct MaxOp {
-  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
-};
 

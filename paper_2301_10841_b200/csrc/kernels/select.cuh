@@ -163,18 +163,17 @@ __global__ void k_select_ns(const __grid_constant__ KNode N, const DevTrie* __re
 
 // Inclusive scan of a small frontier's candidate counts in one block (F <=
 // kSmallScan), total written to DevCounters::total_m: one launch instead of
-// CUB's two plus a device-to-device copy.
+// the look-back scan's tile machinery.
 constexpr uint64_t kSmallScan = 1024ull * 32;
 __global__ void __launch_bounds__(1024) k_scan_small(const uint64_t* __restrict__ m, uint64_t* __restrict__ scan,
                                                      uint32_t F, DevCounters* ctr) {
-  typedef cub::BlockScan<uint64_t, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint64_t tmp[32];
   const uint32_t per = (F + 1023) / 1024;
   const uint32_t b = threadIdx.x * per, e = min(F, b + per);
   uint64_t local = 0;
   for (uint32_t i = b; i < e; ++i) local += m[i];
   uint64_t excl, total;
-  BS(tmp).ExclusiveSum(local, excl, total);
+  excl = prims::block_excl_scan<1024>(local, total, tmp, prims::OpSum(), (uint64_t)0);
   for (uint32_t i = b; i < e; ++i) {
     excl += m[i];
     scan[i] = excl;
