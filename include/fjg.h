@@ -167,6 +167,13 @@ int fjg_engine_sync(fjg_engine* eng);
 /* Copies host columns to the device (cudaMemcpyAsync per column). */
 int fjg_relation_create(fjg_engine* eng, const int32_t* const* host_cols, int ncols, uint64_t nrows,
                         fjg_relation** out);
+/* fj::Value is an int64 (value.hpp:31): int64 host columns are staged to the
+ * device in chunks and narrowed there to the engine's int32 columns (128-bit
+ * loads). FJG_E_VALIDATION, naming the column and the first row, if a value
+ * does not fit int32 (wide domains must be dictionary-encoded by the caller;
+ * joins only need equality, MIN and the checksum need the values). */
+int fjg_relation_create_i64(fjg_engine* eng, const int64_t* const* host_cols, int ncols, uint64_t nrows,
+                            fjg_relation** out);
 /* Wraps (copy=0: zero-copy alias, caller keeps the memory alive) or copies
  * (copy=1) device columns. */
 int fjg_relation_from_device(fjg_engine* eng, const int32_t* const* dev_cols, int ncols, uint64_t nrows,

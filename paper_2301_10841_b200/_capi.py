@@ -96,6 +96,7 @@ def _load():
         "fjg_engine_sync": (I, [P]),
         "fjg_engine_stream": (P, [P]),
         "fjg_relation_create": (I, [P, C.POINTER(P), I, U64, C.POINTER(P)]),
+        "fjg_relation_create_i64": (I, [P, C.POINTER(P), I, U64, C.POINTER(P)]),
         "fjg_relation_from_device": (I, [P, C.POINTER(P), I, U64, I, C.POINTER(P)]),
         "fjg_relation_filter": (I, [P, C.POINTER(Predicate), I, C.POINTER(P)]),
         "fjg_relation_rows": (U64, [P]),
@@ -145,7 +146,8 @@ lib = _load()
 
 # every symbol include/fjg.h declares (checked by tests/test_capi.py)
 EXPORTED = ["fjg_last_error", "fjg_abi_version", "fjg_compile_plan", "fjg_plan_op", "fjg_engine_create",
-            "fjg_engine_destroy", "fjg_engine_sync", "fjg_engine_stream", "fjg_relation_create", "fjg_relation_from_device",
+            "fjg_engine_destroy", "fjg_engine_sync", "fjg_engine_stream", "fjg_relation_create", "fjg_relation_create_i64",
+            "fjg_relation_from_device",
             "fjg_relation_filter", "fjg_relation_rows", "fjg_relation_cols", "fjg_relation_device_col",
             "fjg_relation_download", "fjg_relation_destroy", "fjg_relation_partition",
             "fjg_relation_partition_into", "fjg_query_create",

@@ -56,7 +56,7 @@ extern "C" {
 
 const char* fjg_last_error(void) { return fjg::g_last_error.c_str(); }
 
-int fjg_abi_version(void) { return 4; }  // 3: fjg_result.first_node_ms; 4: fjg_comm / fjg_execute_multi
+int fjg_abi_version(void) { return 5; }  // 3: fjg_result.first_node_ms; 4: fjg_comm / fjg_execute_multi; 5: fjg_relation_create_i64
 
 int fjg_compile_plan(const char* query_json, int mode, int factor_fixpoint, char* out, size_t cap, size_t* needed) {
   return guard([&] {

@@ -1903,6 +1903,54 @@ int fjg_relation_create(fjg_engine* eng, const int32_t* const* host_cols, int nc
   });
 }
 
+// fj::Value carries int64 (value.hpp:31); the engine's columns are int32. An
+// int64 column is staged through the device in chunks and narrowed there
+// (k_narrow_i64); a value outside int32 is a ValidationError naming its
+// column and row (wide domains are dictionary-encoded by the caller).
+int fjg_relation_create_i64(fjg_engine* eng, const int64_t* const* host_cols, int ncols, uint64_t nrows,
+                            fjg_relation** out) {
+  return guard([&] {
+    ScopedDevice sd(eng->device);
+    fjg_relation* r = new_relation(eng, ncols, nrows);
+    if (nrows == 0) {
+      *out = r;
+      return;
+    }
+    constexpr uint64_t kChunk = 1ull << 24;  // 128 MB of int64 per staged chunk
+    const uint64_t chunk = std::min<uint64_t>(nrows, kChunk);
+    long long* stage = (long long*)eng->pool->alloc(chunk * 8);
+    unsigned long long* d_bad = (unsigned long long*)eng->pool->alloc((size_t)ncols * 8);
+    std::vector<unsigned long long> h_bad(ncols, ~0ull);
+    try {
+      CK(cudaMemsetAsync(d_bad, 0xFF, (size_t)ncols * 8, eng->stream));
+      for (int c = 0; c < ncols; ++c)
+        for (uint64_t r0 = 0; r0 < nrows; r0 += chunk) {
+          const uint64_t m = std::min<uint64_t>(chunk, nrows - r0);
+          CK(cudaMemcpyAsync(stage, host_cols[c] + r0, m * 8, cudaMemcpyHostToDevice, eng->stream));
+          LAUNCH(eng, k_narrow_i64<<<grid_for(m / 4 + 1, 256, eng->num_sms * 8), 256, 0, eng->stream>>>(
+                          stage, m, r0, r->cols[c] + r0, d_bad + c));
+        }
+      CK(cudaMemcpyAsync(h_bad.data(), d_bad, (size_t)ncols * 8, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      ++eng->syncs;
+    } catch (...) {
+      eng->pool->free(stage);
+      eng->pool->free(d_bad);
+      fjg_relation_destroy(r);
+      throw;
+    }
+    eng->pool->free(stage);
+    eng->pool->free(d_bad);
+    for (int c = 0; c < ncols; ++c)
+      if (h_bad[c] != ~0ull) {
+        fjg_relation_destroy(r);
+        throw fj::ValidationError("int64 value outside the int32 range at column " + std::to_string(c) + ", row " +
+                                  std::to_string(h_bad[c]) + " (dictionary-encode wide domains before loading)");
+      }
+    *out = r;
+  });
+}
+
 int fjg_relation_from_device(fjg_engine* eng, const int32_t* const* dev_cols, int ncols, uint64_t nrows, int copy,
                              fjg_relation** out) {
   return guard([&] {

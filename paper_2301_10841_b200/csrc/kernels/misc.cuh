@@ -47,6 +47,38 @@ __global__ void k_compact_col(const int32_t* in, const uint32_t* flags, const ui
     if (flags[i]) out[excl[i]] = in[i];
 }
 
+// int64 column ingestion (fj::Value is int64, value.hpp:31): narrows a staged
+// chunk of int64 values to the engine's int32 column, four values per thread
+// (two 128-bit loads, one 128-bit store). A value outside int32 records the
+// lowest offending row in *bad_row (UINT64_MAX = none); its slot is left 0.
+__global__ void k_narrow_i64(const long long* __restrict__ in, uint64_t n, uint64_t row0, int32_t* __restrict__ out,
+                             unsigned long long* bad_row) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nq = n >> 2;
+  unsigned long long bad = ~0ull;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(in) + 2 * q);
+    const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(in) + 2 * q + 1);
+    const long long v[4] = {a.x, a.y, b.x, b.y};
+    int4 o;
+    int32_t* op = &o.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool fits = v[j] == (long long)(int32_t)v[j];
+      op[j] = fits ? (int32_t)v[j] : 0;
+      if (!fits) bad = min(bad, (unsigned long long)(row0 + 4 * q + j));
+    }
+    reinterpret_cast<int4*>(out)[q] = o;
+  }
+  for (uint64_t i = (nq << 2) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long v = in[i];
+    const bool fits = v == (long long)(int32_t)v;
+    out[i] = fits ? (int32_t)v : 0;
+    if (!fits) bad = min(bad, (unsigned long long)(row0 + i));
+  }
+  if (bad != ~0ull) atomicMin(bad_row, bad);
+}
+
 // Stable hash partition (multi-GPU sharding on the first plan variable):
 // counting sort by destination. Block b owns rows [b*kPartChunk, ...); hist is
 // destination-major (d * nblocks + b) so its exclusive scan gives every

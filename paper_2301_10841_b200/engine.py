@@ -94,6 +94,18 @@ class Engine:
         check(lib.fjg_relation_create(self._h, ptrs, len(arrs), n, C.byref(h)))
         return Relation(self, h, keepalive=None)
 
+    def relation_i64(self, cols):
+        """load int64 host columns (fj::Value, value.hpp:31), narrowed on the device
+        (fjg_relation_create_i64); ValidationError if a value does not fit int32."""
+        arrs = [np.ascontiguousarray(c, dtype=np.int64) for c in cols]
+        n = len(arrs[0]) if arrs else 0
+        if any(len(a) != n for a in arrs):
+            raise _capi.ValidationError("all columns must have identical length (SPEC.md:35)")
+        ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        h = C.c_void_p()
+        check(lib.fjg_relation_create_i64(self._h, ptrs, len(arrs), n, C.byref(h)))
+        return Relation(self, h, keepalive=None)
+
     def relation_host_ptrs(self, ptrs, nrows):
         """fjg_relation_create from raw host column pointers (e.g. pinned buffers)."""
         arr = (C.c_void_p * len(ptrs))(*ptrs)

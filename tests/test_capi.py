@@ -36,7 +36,7 @@ def test_struct_sizes_match_header():
 
 
 def test_error_codes():
-    assert _capi.lib.fjg_abi_version() == 4
+    assert _capi.lib.fjg_abi_version() == 5
     with pytest.raises(_capi.ParseError):
         P.compile_plan("{not json", "free")
     with pytest.raises(_capi.ValidationError):

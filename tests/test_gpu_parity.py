@@ -185,6 +185,30 @@ def test_filter_and_partition_kernels(engine):
             off += counts[d]
 
 
+def test_int64_columns_narrowed_on_device(engine):
+    """fjg_relation_create_i64 (fj::Value is int64, value.hpp:31): int64 host columns give the same relation,
+    and the same query result, as their int32 copies; a value outside int32 is a ValidationError naming it."""
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 3, 4, 5, 1000, 100003):
+        c0 = rng.integers(-2**31, 2**31, n, dtype=np.int64)
+        c1 = rng.integers(-5, 5, n, dtype=np.int64)
+        got = engine.relation_i64([c0, c1]).download()
+        assert (got[0] == c0.astype(np.int32)).all() and (got[1] == c1.astype(np.int32)).all()
+    w = configs.triangle(scale=10, m=8000, seed=2)
+    plan = P.compile_plan({"query": w.query, "binary_plan": w.binary_plan}, w.mode)
+    cols = w.atom_columns()
+    ref = oracle.execute(w.query, plan, cols)
+    rel = engine.relation_i64([np.asarray(c, dtype=np.int64) for c in cols[0]])
+    r = engine.query({"query": w.query}, plan, [rel] * 3).execute()
+    assert (r.count, r.checksum) == (ref["count"], ref["checksum"])
+    bad = np.arange(10, dtype=np.int64)
+    for v, row in ((2**31, 6), (-2**31 - 1, 9), (2**40, 0)):
+        b = bad.copy()
+        b[row] = v
+        with pytest.raises(fjg.ValidationError, match=f"column 1, row {row}"):
+            engine.relation_i64([bad, b])
+
+
 def test_counters(engine):
     """ExecStats: probes/misses/body entries agree with the oracle where forcing order is pinned (chain)."""
     w = configs.chain(n=20000, domain=30000)
