@@ -504,7 +504,7 @@ def run_ours(args):
     last_ms = statistics.mean(r.last_node_ms / max(r.last_node_launches, 1) for r in results)
     last_bytes = last_node_bytes(plan, w.query, r0) / max(r0.last_node_launches, 1)
     first_ms = statistics.mean(r.first_node_ms for r in results)
-    kernel = "fused last node (k_last_gj_bf for GJ-shaped nodes, k_tail for a Cartesian tail, else k_expand<COUNT>)"
+    kernel = "fused last node (k_last_gj_warp for GJ-shaped nodes, k_tail for a Cartesian tail, else k_expand<COUNT>)"
     memo_ms = statistics.mean(r.memo_ms for r in results)
     cands = [(statistics.mean(r.last_node_ms for r in results), "last")]
     if world == 1:

@@ -1014,6 +1014,9 @@ static void sync_counters(fjg_query* q) {
 #ifndef FJG_SORTED_ROOT
 #define FJG_SORTED_ROOT 1
 #endif
+#ifndef FJG_SORTED_ROOT_MIN_LOG
+#define FJG_SORTED_ROOT_MIN_LOG 21  // roots of >= 2^21 rows are forced by sorting, smaller ones by CAS inserts
+#endif
 // Sort-based root force (arity <= 1 keys): see kernels/force.cuh.
 static void force_root_sorted(fjg_query* q, int t) {
   fjg_engine* eng = q->eng;
@@ -1086,11 +1089,16 @@ static void launch_force_batch(fjg_query* q, const ForceBatch& B, uint64_t upper
   const dim3 g(grid_for(upper, 256, std::max(1, eng->num_sms * 16 / B.n)), B.n);
   const dim3 ga(grid_for(upper, 256, std::max(1, eng->num_sms * 8 / B.n)), B.n);
   // (k_force_clear also resets each member's counters and a root's cursor / key count)
-  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->d_ctr));
+  const int opt_ok = (FJG_FORCE_OPT && !single && !multi) ? 1 : 0;
+  LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->d_ctr, 0, opt_ok));
   if (multi)
-    LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+    LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr, 0));
   else
-    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
+    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr, 0));
+  if (opt_ok) {  // redo of a member whose optimistic insert met a repeated key (exits at once otherwise)
+    LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->d_ctr, 1, opt_ok));
+    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr, 1));
+  }
   if (single)
     LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));
   else
@@ -1102,7 +1110,7 @@ static void launch_force_batch(fjg_query* q, const ForceBatch& B, uint64_t upper
 
 static bool root_sorted_path(const fjg_query* q, int t) {
   const auto& T = q->tries[t];
-  return T.levels[0].size() <= 1 && T.rel->nrows >= (1u << 21) && FJG_SORTED_ROOT;
+  return T.levels[0].size() <= 1 && T.rel->nrows >= (1u << FJG_SORTED_ROOT_MIN_LOG) && FJG_SORTED_ROOT;
 }
 
 // Force the roots of tries `ts` (all unforced): sorted roots one by one, the

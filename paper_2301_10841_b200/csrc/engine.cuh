@@ -228,6 +228,7 @@ struct DevCounters {
   unsigned long long ticket;   // last-node chunk tickets (FJG_GJ_TICKET)
   uint32_t fnew[MAXT];         // per member of a force batch: new keys (slots claimed)
   uint32_t fdup[MAXT];         // per member of a force batch: a repeated key was met
+  uint32_t fopt[MAXT];         // per member of a force batch: inserted optimistically (every key expected distinct)
 };
 
 // Fused Cartesian tail (nodes k..K-1 each one stream-iterated subatom binding

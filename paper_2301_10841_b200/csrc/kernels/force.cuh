@@ -4,7 +4,20 @@
 
 // ============================================================================
 // force: clear -> insert -> assign -> scatter -> finalize  (Fig 12 `force`)
+//
+// Optimistic members (FJG_FORCE_OPT; the claimed subtries of a level >= 1 with
+// one-column keys, while no force of that level has met a repeated key): the
+// insert assumes every key of a subtrie is distinct -- the winner's CAS writes
+// the final slot {key, child start = its own position} and the same thread
+// writes the unit child count and the clustered values, so clear + insert is
+// the whole force (no scratch arrays, no second pass over the rows; a level of
+// deduplicated graph edges always ends here). A repeated key flags the member,
+// and the redo launches (clear, insert with phase 1; they exit at once
+// otherwise) run the general counting protocol over the same subtries.
 // ============================================================================
+#ifndef FJG_FORCE_OPT
+#define FJG_FORCE_OPT 1
+#endif
 // Position iteration over the union of claimed ranges. single: one subtrie
 // (p0, len0) given by value (the root BaseScan).
 struct ForceRange {
@@ -58,15 +71,20 @@ __global__ void k_force_marks(const uint32_t* __restrict__ list_scan, const uint
 // clear the slot regions (one 4-slot bucket per position) and child counts of
 // the claimed subtries
 __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
-                              DevCounters* ctr) {
+                              DevCounters* ctr, int phase, int opt_ok) {
   const int y = blockIdx.y;
   const ForceRange& R = B.R[y];
   const int lev = R.lev;
   const DevLevel& L = tries[R.trie].lev[lev];
+  // phase 1 (redo): only a member whose optimistic insert met a repeated key
+  if (phase == 1 && !(ctr->fopt[y] && ctr->fdup[y])) return;
   const uint32_t total = force_total(R);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // this member's counters (read by the later kernels only)
     ctr->fnew[y] = 0;
-    ctr->fdup[y] = 0;
+    if (phase == 0) {
+      ctr->fdup[y] = 0;
+      ctr->fopt[y] = (opt_ok && !R.single && !ctr->level_dup[R.trie * MAXL + lev]) ? 1u : 0u;
+    }
     if (R.single) {
       L.cursor[lev == 0 ? 0 : R.p0] = 0;
       L.nkeys[lev == 0 ? 0 : R.p0] = 0;
@@ -79,6 +97,10 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
 #pragma unroll
     for (int u = 0; u < 2 * FJG_RS; ++u) t[u] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     L.cnt[pos] = 0;
+    if (phase == 1 && pos == p) {  // the optimistic insert set them to the unit grouping
+      L.cursor[p] = 0;
+      L.nkeys[p] = 0;
+    }
     if (L.srep)
 #pragma unroll
       for (int u = 0; u < FJG_RS; ++u) reinterpret_cast<uint4*>(L.srep)[(uint64_t)FJG_RS * pos + u] = make_uint4(0u, 0u, 0u, 0u);
@@ -91,10 +113,13 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
 template <bool MULTI>
 __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                                uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
-                               DevCounters* ctr) {
+                               DevCounters* ctr, int phase) {
   const int y = blockIdx.y;
   const ForceRange& R = B.R[y];
   const int trie = R.trie, lev = R.lev;
+  const bool fopt = !MULTI && ctr->fopt[y] != 0;
+  if (phase == 1 && !(fopt && ctr->fdup[y])) return;
+  const bool opt = fopt && phase == 0;  // optimistic: slots receive their final value
   tmp_slot += R.slot_off;
   tmp_rank += R.slot_off;
   const DevTrie& T = tries[trie];
@@ -120,7 +145,8 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
       for (int t = 0; t < MAXK; ++t) vals[t] = t < nk ? src[t][pos] : 0;
       const uint32_t kw = key_word_r(nk, vals);
       // the winner's CAS already counts it (rank 0); repeated keys add to the count
-      const unsigned long long mine = ((unsigned long long)(kPendBit | 1u) << 32) | kw;
+      // (optimistic: the final slot, child start = this position)
+      const unsigned long long mine = ((unsigned long long)(opt ? pos : (kPendBit | 1u)) << 32) | kw;
       const uint64_t lo = 4ull * region_lo(p), hi = 4ull * region_hi(p, len);
       h = 4ull * region_bucket(p, len, kw);
       FJG_ASSERT(lo <= h && h < hi && pos >= p && pos < (uint64_t)p + len);
@@ -164,9 +190,22 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
         }
         if (++h == hi) h = lo;
       }
-      const uint32_t rank = won ? 0u : (atomicAdd(&L.table[h].q, 1u) & ~kPendBit);
-      tmp_slot[pos] = (uint32_t)h;
-      tmp_rank[pos] = rank;
+      if (opt) {
+        // unit child group of this row (force_unique_body's work, same thread)
+        L.cnt[pos] = 1;
+        if (pos == p) {
+          L.nkeys[p] = len;
+          L.cursor[p] = len;
+        }
+        for (int c = 0; c < T.ncols; ++c) {
+          int32_t* out = L.cval[c];
+          if (out) out[pos] = level_src(T, lev, c)[pos];
+        }
+      } else {
+        const uint32_t rank = won ? 0u : (atomicAdd(&L.table[h].q, 1u) & ~kPendBit);
+        tmp_slot[pos] = (uint32_t)h;
+        tmp_rank[pos] = rank;
+      }
     }
     wins += won ? 1u : 0u;
   }
@@ -281,7 +320,7 @@ __global__ void k_force_scatter(const DevTrie* __restrict__ tries, const __grid_
     }
   }
   if (!ctr->fdup[y]) {
-    force_unique_body(tries, trie, lev, R, tmp_slot);
+    if (!ctr->fopt[y]) force_unique_body(tries, trie, lev, R, tmp_slot);  // (an optimistic insert did it)
     return;
   }
   const DevTrie& T = tries[trie];

@@ -1176,6 +1176,38 @@ __device__ __forceinline__ uint32_t probe_region_one(const Slot* table, uint32_t
   return q;
 }
 
+#ifndef FJG_STREAM_BULK
+#define FJG_STREAM_BULK 0  // 1: k_stream_one stages its key column with cp.async.bulk + mbarrier (measured 5% slower on C3 node 0 than the per-lane 4-byte cp.async: one mbarrier wait per 64-key chunk; profiles/README.md)
+#endif
+constexpr int kStreamStages = 4;  // bulk-copy pipeline depth per warp
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// global -> shared bulk copy (TMA engine, SASS UBLKCP): 16-byte aligned, size a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 template <int NP, int R>
 struct StreamOneQC {
   static constexpr int QC = R <= 7 ? 256 : 512;  // per-warp ring capacity per stage (>= 32*R + 31)
@@ -1326,6 +1358,47 @@ __global__ void __launch_bounds__(TILE, FJG_STREAM_MINB) k_stream_one(const __gr
   const int32_t* __restrict__ kcol0 = S.src[SP.kc[0]] + pos0;
   const KSub& P0 = N.sub[SP.s[0]];
   uint32_t base = (uint32_t)c0 + (blockIdx.x * (TILE / 32) + wi) * 32u * R;
+#if FJG_STREAM_BULK
+  // software pipeline: the first-probe keys of the warp's next chunks stream
+  // into shared memory as bulk copies (cp.async.bulk, one 128*R-byte copy per
+  // chunk issued by lane 0, completion on a per-warp mbarrier per stage;
+  // kStreamStages - 1 chunks in flight) while this chunk probes. A chunk that
+  // is ragged (the column's end) or not 16-byte aligned is loaded by its lanes.
+  __shared__ __align__(16) uint32_t KB[kStreamStages][TILE / 32][32 * R];
+  __shared__ uint64_t MB[kStreamStages][TILE / 32];
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStreamStages; ++s) mbar_init(&MB[s][wi], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncwarp();
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(kcol0) & 15u) == 0) && ((base & 3u) == 0);
+  auto prefetch = [&](uint32_t b, int stg) {
+    if (b >= e1) return;
+    if (bulk_ok && e1 - b >= 32u * R) {
+      if (lane == 0) {
+        mbar_expect_tx(&MB[stg][wi], 32u * R * 4u);
+        bulk_g2s(&KB[stg][wi][0], kcol0 + b, 32u * R * 4u, &MB[stg][wi]);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t i = b + r * 32 + lane;
+        KB[stg][wi][r * 32 + lane] = i < e1 ? (uint32_t)__ldg(kcol0 + i) : 0u;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&MB[stg][wi]);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < kStreamStages - 1; ++s) prefetch(base + s * gstep, s);
+  for (uint32_t it = 0; base < e1; base += gstep, ++it) {
+    const int buf = it % kStreamStages;
+    __syncwarp();  // every lane has read the stage refilled below (one iteration ago)
+    prefetch(base + (kStreamStages - 1) * gstep, (it + kStreamStages - 1) % kStreamStages);
+    mbar_wait(&MB[buf][wi], (it / kStreamStages) & 1u);
+#else
   // software pipeline: the next chunk's first-probe keys stream into shared
   // memory (cp.async, double buffer) while this chunk probes; each lane copies
   // and reads only its own slots, so no warp barrier is needed.
@@ -1345,6 +1418,7 @@ __global__ void __launch_bounds__(TILE, FJG_STREAM_MINB) k_stream_one(const __gr
   for (; base < e1; base += gstep, buf ^= 1) {
     prefetch(base + gstep, buf ^ 1);
     asm volatile("cp.async.wait_group 1;\n" ::);
+#endif
     uint32_t kw[R], b0[R];
     bool live[R];
     Bucket8 h[R];
@@ -1382,7 +1456,9 @@ __global__ void __launch_bounds__(TILE, FJG_STREAM_MINB) k_stream_one(const __gr
     for (int j = 1; j < NP; ++j)
       while (qtail[j - 1] - qhead[j - 1] >= 32) stage(j, 32);
   }
+#if !FJG_STREAM_BULK
   asm volatile("cp.async.wait_group 0;\n" ::);
+#endif
   // drain the partial batches, stage by stage
 #pragma unroll
   for (int j = 1; j < NP; ++j)

@@ -84,22 +84,23 @@ __device__ __forceinline__ T block_sum(T v, T* sm) {
 }
 
 // ---------------------------------------------------------------------------
-// decoupled look-back (scans): per tile {flag, aggregate, inclusive}
+// decoupled look-back (scans): one 16-byte descriptor per tile. Each 64-bit
+// half carries the tag (epoch << 2 | status: 1 = the tile's aggregate, 2 = its
+// inclusive prefix) in its high word and one 32-bit half of the value in its
+// low word, so a descriptor is published with one 128-bit store and read with
+// one 128-bit load -- no fence, no dependent second load. A reader accepts a
+// descriptor only when both halves carry the same tag of this epoch (a half is
+// written once per status, so equal tags mean both halves belong to one write).
 // ---------------------------------------------------------------------------
-struct LBTile {
-  unsigned long long flag;  // epoch << 2 | 1 (aggregate) / 2 (inclusive prefix)
-  unsigned long long agg;
-  unsigned long long inc;
+struct __align__(16) LBTile {
+  unsigned long long a, b;
 };
 
 __device__ __forceinline__ void lb_publish(LBTile* t, bool inclusive, unsigned long long v, uint32_t epoch) {
-  volatile unsigned long long* w = reinterpret_cast<volatile unsigned long long*>(t);
-  if (inclusive)
-    w[2] = v;
-  else
-    w[1] = v;
-  __threadfence();
-  w[0] = ((unsigned long long)epoch << 2) | (inclusive ? 2ull : 1ull);
+  const unsigned long long tag = (unsigned long long)((epoch << 2) | (inclusive ? 2u : 1u)) << 32;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};\n" ::"l"(t), "l"(tag | (v & 0xffffffffull)),
+               "l"(tag | (v >> 32))
+               : "memory");
 }
 
 // Warp 0 of tile `tile` (> 0): the exclusive prefix over tiles [0, tile).
@@ -110,18 +111,17 @@ __device__ T lb_lookback(LBTile* st, uint64_t tile, uint32_t epoch, Op op, T id)
   int64_t t = (int64_t)tile - 1;
   while (true) {
     const int64_t tt = t - (int64_t)lane;
-    unsigned long long f = 2;
+    unsigned status = 2;
     T v = id;
     if (tt >= 0) {
-      volatile unsigned long long* w = reinterpret_cast<volatile unsigned long long*>(st + tt);
+      unsigned long long a, b;
       do {
-        f = w[0];
-      } while ((uint32_t)(f >> 2) != epoch);
-      __threadfence();
-      v = (T)((f & 3ull) == 2ull ? w[2] : w[1]);
-      f &= 3ull;
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(st + tt) : "memory");
+      } while ((uint32_t)(a >> 34) != epoch || (a >> 32) != (b >> 32));
+      status = (unsigned)(a >> 32) & 3u;
+      v = (T)((a & 0xffffffffull) | (b << 32));
     }
-    const unsigned pm = __ballot_sync(kFull, f == 2ull);
+    const unsigned pm = __ballot_sync(kFull, status == 2u);
     // lanes up to (and including) the nearest inclusive prefix contribute
     const int first = pm ? __ffs(pm) - 1 : 31;
     if ((int)lane > first) v = id;
@@ -134,7 +134,10 @@ __device__ T lb_lookback(LBTile* st, uint64_t tile, uint32_t epoch, Op op, T id)
 
 // Single-pass scan: out[i] = op(in[0..i]) (EXCL: op(in[0..i-1]), identity first).
 // In may alias out. `total` (optional) receives the reduction of all n.
-constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+#ifndef FJG_SCAN_ITEMS
+#define FJG_SCAN_ITEMS 8
+#endif
+constexpr int kScanThreads = 256, kScanItems = FJG_SCAN_ITEMS, kScanTile = kScanThreads * kScanItems;
 template <class In, class T, class Op, bool EXCL>
 __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const In* in, T* out, uint64_t n, LBTile* st,
                                                           unsigned long long* ticket, uint64_t tbase,
