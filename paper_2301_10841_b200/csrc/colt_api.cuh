@@ -26,7 +26,7 @@ __global__ void k_colt_claim(const DevTrie* tries, DevCounters* ctr, int t, int 
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + it * stride;
     const bool ok = i < n;
     const uint32_t pi = ok ? p[i] : 0u, li = ok ? len[i] : 0u;
-    const bool need = ok && li > 0 && *((volatile const uint32_t*)(tries[t].lev[l].state + pi)) == 0u;
+    const bool need = ok && li > 0 && *((volatile const uint32_t*)&tries[t].lev[l].sn[pi].state) == 0u;
     claim_subtrie(tries, ctr, S, pi, li, need);
   }
 }
@@ -120,8 +120,7 @@ KSub colt_ksub(fjg_colt* c, int level) {
   for (int t = 0; t < L.nk; ++t) S.kcmp[t] = L.cval[L.keycol[t]];
   S.cnt = L.cnt;
   S.table = L.table;
-  S.state = L.state;
-  S.nkeys = L.nkeys;
+  S.sn = L.sn;
   // a non-null in_p marks a non-root subtrie (probe_region uses its length)
   S.in_p = level == 0 ? nullptr : L.cnt;
   S.root_n = (uint32_t)c->rows;
@@ -346,11 +345,10 @@ int fjg_colt_estimated_key_count(fjg_colt* c, int level, uint32_t p, uint32_t le
     if (level >= c->map_levels) return;
     const DevLevel& L = colt_trie(c).lev[level];
     const uint32_t at = level == 0 ? 0u : p;
-    uint32_t st = 0, nk = 0;
-    CK(cudaMemcpyAsync(&st, L.state + at, 4, cudaMemcpyDeviceToHost, eng->stream));
-    CK(cudaMemcpyAsync(&nk, L.nkeys + at, 4, cudaMemcpyDeviceToHost, eng->stream));
+    SubState sn{};
+    CK(cudaMemcpyAsync(&sn, L.sn + at, sizeof(sn), cudaMemcpyDeviceToHost, eng->stream));
     CK(cudaStreamSynchronize(eng->stream));
-    if (st == 2u) *out = nk;  // a forced map: its number of keys (never forces)
+    if (sn.state == 2u) *out = sn.nkeys;  // a forced map: its number of keys (never forces)
   });
 }
 

@@ -560,8 +560,7 @@ static void prepare_query(fjg_query* q) {
       H.cap = 4ull * FJG_RS * std::max<uint64_t>(n, 1);  // FJG_RS 4-slot buckets per position: per-subtrie regions
       L.table = (Slot*)q->alloc(H.cap * sizeof(Slot));
       L.srep = H.multi ? (uint32_t*)q->alloc(H.cap * 4) : nullptr;
-      L.state = (uint32_t*)q->alloc(H.nsub * 4);
-      L.nkeys = (uint32_t*)q->alloc(H.nsub * 4);
+      L.sn = (SubState*)q->alloc(H.nsub * sizeof(SubState));
       L.cursor = (uint32_t*)q->alloc(H.nsub * 4);
       L.cnt = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
       std::set<int> cols;
@@ -780,8 +779,7 @@ static void build_knodes(fjg_query* q) {
       }
       S.cnt = L.cnt;
       S.table = L.table;
-      S.state = L.state;
-      S.nkeys = L.nkeys;
+      S.sn = L.sn;
       const bool open = (N.in_atoms >> D.atom) & 1u;
       S.in_p = open ? N.in.p[D.atom] : nullptr;
       S.in_len = open ? N.in.len[D.atom] : nullptr;
@@ -1629,9 +1627,9 @@ static void reset_query(fjg_query* q) {
       auto& H = T.lev[l];
       DevLevel& L = T.dev.lev[l];
       if (H.dirty) {
-        P.ptr[P.nz] = L.state;
-        P.n[P.nz] = (uint32_t)H.nsub;
-        maxn = std::max<uint32_t>(maxn, (uint32_t)H.nsub);
+        P.ptr[P.nz] = reinterpret_cast<uint32_t*>(L.sn);  // (state, key count) records: both words cleared
+        P.n[P.nz] = (uint32_t)(2 * H.nsub);
+        maxn = std::max<uint32_t>(maxn, (uint32_t)(2 * H.nsub));
         ++P.nz;
         H.dirty = false;
       }

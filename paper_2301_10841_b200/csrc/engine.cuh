@@ -21,8 +21,8 @@
 // Per level l (l >= 0), with n = relation rows:
 //   table   open-addressing hash map (parent p, key) -> child (q, cnt);
 //           16-byte slots, linear probing, capacity pow2 >= 2n (load <= 0.5)
-//   state   per subtrie id: 0 unforced, 1 claimed for forcing, 2 forced
-//   nkeys   per subtrie id: distinct keys once forced (estimated_key_count)
+//   sn      per subtrie id: {state: 0 unforced, 1 claimed for forcing, 2 forced;
+//           nkeys: distinct keys once forced (estimated_key_count)}
 //   cursor  per subtrie id: child-range allocation cursor (force only)
 //   cnt     per position of domain l: child length at a child start, else 0
 //   cval[c] per position of domain l: column c (every column used at levels >= l)
@@ -60,11 +60,18 @@ struct __align__(8) Slot {
 };
 constexpr uint32_t kPendBit = 0x80000000u;  // positions are < 2^31
 
+// Per subtrie id: its state (0 unforced, 1 claimed for forcing, 2 forced) and,
+// once forced, its number of distinct keys (estimated_key_count). One 8-byte
+// record, so k_select's random read of a subtrie costs one sector, not two.
+struct __align__(8) SubState {
+  uint32_t state;
+  uint32_t nkeys;
+};
+
 struct DevLevel {
   Slot* table;       // 4n slots
   uint32_t* srep;    // arity >= 2 only, per slot: representative position + 1 during insertion
-  uint32_t* state;
-  uint32_t* nkeys;
+  SubState* sn;  // per subtrie id: {state, key count}
   uint32_t* cursor;
   uint32_t* cnt;
   int32_t* cval[MAXC];
@@ -129,8 +136,7 @@ struct KSub {
   const int32_t* kcmp[MAXK];  // probe key compare for arity >= 2: cval of depth at the child start
   const uint32_t* cnt;        // cnt of depth (keys-mode iteration)
   const Slot* table;          // slots of depth
-  const uint32_t* state;      // state of depth (estimated_key_count, claims)
-  const uint32_t* nkeys;
+  const SubState* sn;         // {state, key count} of depth's subtries (estimated_key_count, claims)
   const uint32_t* in_p;       // frontier subtrie column of this atom (null: root)
   const uint32_t* in_len;
   uint32_t root_n;

@@ -134,12 +134,21 @@ __device__ __forceinline__ void subtrie_of(const KSub& S, uint64_t e, uint32_t& 
   }
 }
 
+// {state, key count} of a subtrie in one 8-byte load (not cached in L1: claims
+// and forces of earlier kernels of this stream must be seen)
+__device__ __forceinline__ uint2 ld_substate(const SubState* p) {
+  uint2 v;
+  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
 // estimated_key_count: forced map -> #keys, vector -> its
 // length, BaseScan -> cardinality. Never forces.
 __device__ __forceinline__ uint64_t estimate(const KSub& S, uint32_t p, uint32_t len) {
   if (p == kSingleton) return 1;
   const uint32_t id = S.depth == 0 ? 0u : p;
-  if (*((volatile const uint32_t*)(S.state + id)) == 2u) return S.nkeys[id];
+  const uint2 sn = ld_substate(S.sn + id);  // state and key count: one 8-byte load
+  if (sn.x == 2u) return sn.y;
   return len;
 }
 

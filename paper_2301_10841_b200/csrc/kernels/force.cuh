@@ -87,7 +87,7 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
     }
     if (R.single) {
       L.cursor[lev == 0 ? 0 : R.p0] = 0;
-      L.nkeys[lev == 0 ? 0 : R.p0] = 0;
+      L.sn[lev == 0 ? 0 : R.p0].nkeys = 0;
     }
   }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -99,7 +99,7 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
     L.cnt[pos] = 0;
     if (phase == 1 && pos == p) {  // the optimistic insert set them to the unit grouping
       L.cursor[p] = 0;
-      L.nkeys[p] = 0;
+      L.sn[p].nkeys = 0;
     }
     if (L.srep)
 #pragma unroll
@@ -110,8 +110,11 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
 // Insert every offset of the claimed subtries: claim a slot for its key (CAS
 // on the 8-byte slot), then count it (the pending slot's q word is the group
 // counter; the returned value is the offset's rank inside its child group).
+#ifndef FJG_FORCE_MINB
+#define FJG_FORCE_MINB 5
+#endif
 template <bool MULTI>
-__global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
+__global__ void __launch_bounds__(256, FJG_FORCE_MINB) k_force_insert(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                                uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
                                DevCounters* ctr, int phase) {
   const int y = blockIdx.y;
@@ -194,7 +197,7 @@ __global__ void k_force_insert(const DevTrie* __restrict__ tries, const __grid_c
         // unit child group of this row (force_unique_body's work, same thread)
         L.cnt[pos] = 1;
         if (pos == p) {
-          L.nkeys[p] = len;
+          L.sn[p].nkeys = len;
           L.cursor[p] = len;
         }
         for (int c = 0; c < T.ncols; ++c) {
@@ -258,7 +261,7 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, const __grid_c
       const uint32_t nb = __syncthreads_count(ok);
       if (threadIdx.x == 0 && nb) {
         s_base = p0 + atomicAdd(&L.cursor[p0], blk_total);
-        atomicAdd(&L.nkeys[p0], nb);
+        atomicAdd(&L.sn[p0].nkeys, nb);
       }
       __syncthreads();
       q = s_base + excl;
@@ -280,7 +283,7 @@ __global__ void k_force_assign(const DevTrie* __restrict__ tries, const __grid_c
       uint32_t base = 0;
       if (lane == leader) {
         base = atomicAdd(&L.cursor[p], tot);
-        atomicAdd(&L.nkeys[p], (uint32_t)__popc(grp));
+        atomicAdd(&L.sn[p].nkeys, (uint32_t)__popc(grp));
       }
       base = __shfl_sync(grp, base, leader);
       q = p + base + pre;
@@ -312,11 +315,11 @@ __global__ void k_force_scatter(const DevTrie* __restrict__ tries, const __grid_
     if (blockIdx.x == 0 && threadIdx.x == 0)  // members of a batch finalize concurrently
       atomicAdd((unsigned long long*)&ctr->keys_inserted, (unsigned long long)ctr->fnew[y]);
     if (R.single) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) L.state[lev == 0 ? 0 : R.p0] = 2u;
+      if (blockIdx.x == 0 && threadIdx.x == 0) L.sn[lev == 0 ? 0 : R.p0].state = 2u;
     } else {
       const uint32_t c = *R.list_count;
       for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
-        L.state[R.list_p[i]] = 2u;
+        L.sn[R.list_p[i]].state = 2u;
     }
   }
   if (!ctr->fdup[y]) {
@@ -353,7 +356,7 @@ __device__ void force_unique_body(const DevTrie* __restrict__ tries, int trie, i
     L.table[tmp_slot[pos]].q = pos;
     L.cnt[pos] = 1;
     if (pos == p) {
-      L.nkeys[lev == 0 ? 0 : p] = len;
+      L.sn[lev == 0 ? 0 : p].nkeys = len;
       L.cursor[lev == 0 ? 0 : p] = len;
     }
     for (int c = 0; c < T.ncols; ++c) {
@@ -430,8 +433,8 @@ __global__ void k_root_insert(const DevTrie* __restrict__ tries, int trie, uint3
   }
   if (__any_sync(0xffffffffu, sawdup) && (threadIdx.x & 31) == 0) ctr->level_dup[trie * MAXL] = 1u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    L.nkeys[0] = G;
-    L.state[0] = 2u;
+    L.sn[0].nkeys = G;
+    L.sn[0].state = 2u;
     ctr->newslots = G;
     atomicAdd((unsigned long long*)&ctr->keys_inserted, (unsigned long long)G);
   }
@@ -461,7 +464,7 @@ __global__ void k_eager_list(const Slot* __restrict__ table, uint64_t nslots, co
     const uint32_t q = table[s].q;
     if (q == kEmpty) continue;
     child.cursor[q] = 0;
-    child.nkeys[q] = 0;
+    child.sn[q].nkeys = 0;
     const uint32_t i = atomicAdd(list_count, 1u);
     list_p[i] = q;
     list_len[i] = cnt[q];

@@ -25,10 +25,10 @@ __device__ __forceinline__ void claim_subtrie(const DevTrie* tries, DevCounters*
   }
   const DevLevel& L = tries[S.trie].lev[S.depth];
   bool won = false;
-  if (lead && atomicCAS(L.state + p, 0u, 1u) == 0u) {
+  if (lead && atomicCAS(&L.sn[p].state, 0u, 1u) == 0u) {
     won = true;
     L.cursor[p] = 0;
-    L.nkeys[p] = 0;
+    L.sn[p].nkeys = 0;
   }
   const unsigned wm = __ballot_sync(act, won);
   if (!wm) return;
@@ -86,7 +86,7 @@ __global__ void k_select(const __grid_constant__ KNode N, const DevTrie* __restr
       if (ok) {
         subtrie_of(S, e, p, l);
         need = (p != kSingleton) && (s != best || !S.stream);
-        if (need) need = *((volatile const uint32_t*)(S.state + (S.depth == 0 ? 0u : p))) == 0u;
+        if (need) need = *((volatile const uint32_t*)&S.sn[S.depth == 0 ? 0u : p].state) == 0u;
       }
       claim_subtrie(tries, ctr, S, p, l, need);
     }
@@ -94,69 +94,87 @@ __global__ void k_select(const __grid_constant__ KNode N, const DevTrie* __restr
 }
 
 
+#ifndef FJG_SELECT_ILP
+#define FJG_SELECT_ILP 1  // bindings per thread and trip (2 measured equal on C5: the kernel is bound by random DRAM sectors, not by latency)
+#endif
 // k_select for nodes of at most NS subatoms: each subatom's subtrie and state
 // word are read once per binding and reused by the cover choice and the claims
 // (the generic kernel re-reads them for the claims).
 template <int NS>
 __global__ void k_select_ns(const __grid_constant__ KNode N, const DevTrie* __restrict__ tries, uint64_t F,
                             int dynamic, DevCounters* ctr) {
+  // U bindings per thread and trip: their subtrie ranges, then their {state,
+  // key count} records are loaded back to back, the claims run after
+  constexpr int U = FJG_SELECT_ILP;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t iters = (F + stride - 1) / stride;
+  const uint64_t iters = (F + U * stride - 1) / (U * stride);
   for (uint64_t it = 0; it < iters; ++it) {
-    const uint64_t e = start + it * stride;
-    const bool ok = e < F;
-    uint32_t p[NS], l[NS], st[NS];
+    uint64_t e[U];
+    bool ok[U];
+    uint32_t p[U][NS], l[U][NS], st[U][NS], nk[U][NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      p[s] = l[s] = 0;
-      st[s] = 1;
-      if (ok && s < N.nsub) {
-        const KSub& S = N.sub[s];
-        subtrie_of(S, e, p[s], l[s]);
-        if (p[s] != kSingleton) st[s] = *((volatile const uint32_t*)(S.state + (S.depth == 0 ? 0u : p[s])));
+    for (int u = 0; u < U; ++u) {
+      e[u] = start + (it * U + u) * stride;
+      ok[u] = e[u] < F;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        p[u][s] = l[u][s] = nk[u][s] = 0;
+        st[u][s] = 1;
+        if (ok[u] && s < N.nsub) subtrie_of(N.sub[s], e[u], p[u][s], l[u][s]);
       }
     }
-    int best = N.cov[0];
-    if (ok) {
-      auto est = [&](int s) -> uint64_t {
-        uint64_t v = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (ok[u] && s < N.nsub && p[u][s] != kSingleton) {
+          const KSub& S = N.sub[s];
+          const uint2 sn = ld_substate(S.sn + (S.depth == 0 ? 0u : p[u][s]));  // state + key count: one load
+          st[u][s] = sn.x;
+          nk[u][s] = sn.y;
+        }
+    const bool est_all = dynamic && N.ncov > 1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int best = N.cov[0];
+      if (ok[u]) {
+        auto est = [&](int s) -> uint64_t {
+          uint64_t v = 0;
+#pragma unroll
+          for (int t = 0; t < NS; ++t)
+            if (t == s) v = p[u][t] == kSingleton ? 1ull : (st[u][t] == 2u ? (uint64_t)nk[u][t] : l[u][t]);
+          return v;
+        };
+        if (est_all) {
+          uint64_t best_est = est(best);
+          for (int ci = 1; ci < N.ncov; ++ci) {
+            const int s = N.cov[ci];
+            const uint64_t v = est(s);
+            if (v < best_est) {  // ties keep the lowest position
+              best_est = v;
+              best = s;
+            }
+          }
+        }
+        uint32_t bp = 0, bl = 0;
 #pragma unroll
         for (int t = 0; t < NS; ++t)
-          if (t == s) {
-            const KSub& S = N.sub[t];
-            v = p[t] == kSingleton ? 1ull : (st[t] == 2u ? (uint64_t)S.nkeys[S.depth == 0 ? 0u : p[t]] : l[t]);
+          if (t == best) {
+            bp = p[u][t];
+            bl = l[u][t];
           }
-        return v;
-      };
-      if (dynamic && N.ncov > 1) {
-        uint64_t best_est = est(best);
-        for (int ci = 1; ci < N.ncov; ++ci) {
-          const int s = N.cov[ci];
-          const uint64_t v = est(s);
-          if (v < best_est) {  // ties keep the lowest position
-            best_est = v;
-            best = s;
-          }
-        }
+        N.chosen[e[u]] = (uint8_t)best;
+        N.m[e[u]] = (bp == kSingleton) ? 1ull : (uint64_t)bl;
       }
-      uint32_t bp = 0, bl = 0;
+      // claims: the keys-iterated cover and every probed subatom must be forced
 #pragma unroll
-      for (int t = 0; t < NS; ++t)
-        if (t == best) {
-          bp = p[t];
-          bl = l[t];
-        }
-      N.chosen[e] = (uint8_t)best;
-      N.m[e] = (bp == kSingleton) ? 1ull : (uint64_t)bl;
-    }
-    // claims: the keys-iterated cover and every probed subatom must be forced
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s >= N.nsub) break;
-      const KSub& S = N.sub[s];
-      const bool need = ok && p[s] != kSingleton && (s != best || !S.stream) && st[s] == 0u;
-      claim_subtrie(tries, ctr, S, p[s], l[s], need);
+      for (int s = 0; s < NS; ++s) {
+        if (s >= N.nsub) break;
+        const KSub& S = N.sub[s];
+        const bool need = ok[u] && p[u][s] != kSingleton && (s != best || !S.stream) && st[u][s] == 0u;
+        claim_subtrie(tries, ctr, S, p[u][s], l[u][s], need);
+      }
     }
   }
 }
