@@ -1090,12 +1090,18 @@ static void launch_force_batch(fjg_query* q, const ForceBatch& B, uint64_t upper
   const int opt_ok = (FJG_FORCE_OPT && !single && !multi) ? 1 : 0;
   LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->d_ctr, 0, opt_ok));
   if (multi)
-    LAUNCH(eng, k_force_insert<true><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr, 0));
+    LAUNCH(eng, (k_force_insert<true, false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank,
+                                                                         q->d_ctr, 0)));
+  else if (opt_ok)
+    LAUNCH(eng, (k_force_insert<false, true><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank,
+                                                                         q->d_ctr, 0)));
   else
-    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr, 0));
+    LAUNCH(eng, (k_force_insert<false, false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank,
+                                                                          q->d_ctr, 0)));
   if (opt_ok) {  // redo of a member whose optimistic insert met a repeated key (exits at once otherwise)
     LAUNCH(eng, k_force_clear<<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->d_ctr, 1, opt_ok));
-    LAUNCH(eng, k_force_insert<false><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr, 1));
+    LAUNCH(eng, (k_force_insert<false, true><<<g, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank,
+                                                                         q->d_ctr, 1)));
   }
   if (single)
     LAUNCH(eng, k_force_assign<true><<<ga, 256, 0, eng->stream>>>(q->d_tries, B, q->tmp_slot, q->tmp_rank, q->d_ctr));

@@ -18,6 +18,9 @@
 #ifndef FJG_FORCE_OPT
 #define FJG_FORCE_OPT 1
 #endif
+#ifndef FJG_CLEAR_STREAM
+#define FJG_CLEAR_STREAM 1
+#endif
 // Position iteration over the union of claimed ranges. single: one subtrie
 // (p0, len0) given by value (the root BaseScan).
 struct ForceRange {
@@ -83,7 +86,9 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
     ctr->fnew[y] = 0;
     if (phase == 0) {
       ctr->fdup[y] = 0;
-      ctr->fopt[y] = (opt_ok && !R.single && !ctr->level_dup[R.trie * MAXL + lev]) ? 1u : 0u;
+      int ncl = 0;  // clustered columns of this level (the optimistic insert copies at most two)
+      for (int c = 0; c < tries[R.trie].ncols; ++c) ncl += L.cval[c] ? 1 : 0;
+      ctr->fopt[y] = (opt_ok && !R.single && ncl <= 2 && !ctr->level_dup[R.trie * MAXL + lev]) ? 1u : 0u;
     }
     if (R.single) {
       L.cursor[lev == 0 ? 0 : R.p0] = 0;
@@ -94,9 +99,17 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
     uint32_t p, len, pos;
     force_locate(R, i, p, len, pos);
     uint4* t = reinterpret_cast<uint4*>(L.table) + 2ull * FJG_RS * pos;  // this position's buckets
+#if FJG_CLEAR_STREAM
+    // streaming (evict-first) stores: the cleared lines must not stay resident in
+    // L2, where they crowd out the lines the insert's CAS traffic reuses
+#pragma unroll
+    for (int u = 0; u < 2 * FJG_RS; ++u) __stcs(t + u, make_uint4(kEmpty, kEmpty, kEmpty, kEmpty));
+    __stcs(L.cnt + pos, 0u);
+#else
 #pragma unroll
     for (int u = 0; u < 2 * FJG_RS; ++u) t[u] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     L.cnt[pos] = 0;
+#endif
     if (phase == 1 && pos == p) {  // the optimistic insert set them to the unit grouping
       L.cursor[p] = 0;
       L.sn[p].nkeys = 0;
@@ -111,16 +124,20 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
 // on the 8-byte slot), then count it (the pending slot's q word is the group
 // counter; the returned value is the offset's rank inside its child group).
 #ifndef FJG_FORCE_MINB
-#define FJG_FORCE_MINB 5
+#define FJG_FORCE_MINB 4
 #endif
-template <bool MULTI>
-__global__ void __launch_bounds__(256, FJG_FORCE_MINB) k_force_insert(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
+// OPTK: the kernel of a batch that may hold optimistic members (level >= 1,
+// one-column keys); roots and multi-column keys run the plain instantiation
+// (48 registers, 5 blocks per SM, no per-trip reconvergence: on a root's wide
+// region the lanes that run ahead hide latency, C1 chain 0.47 vs 0.50 ms).
+template <bool MULTI, bool OPTK>
+__global__ void __launch_bounds__(256, OPTK ? FJG_FORCE_MINB : 5) k_force_insert(const DevTrie* __restrict__ tries, const __grid_constant__ ForceBatch B,
                                uint32_t* __restrict__ tmp_slot, uint32_t* __restrict__ tmp_rank,
                                DevCounters* ctr, int phase) {
   const int y = blockIdx.y;
   const ForceRange& R = B.R[y];
   const int trie = R.trie, lev = R.lev;
-  const bool fopt = !MULTI && ctr->fopt[y] != 0;
+  const bool fopt = OPTK && !MULTI && ctr->fopt[y] != 0;
   if (phase == 1 && !(fopt && ctr->fdup[y])) return;
   const bool opt = fopt && phase == 0;  // optimistic: slots receive their final value
   tmp_slot += R.slot_off;
@@ -135,13 +152,28 @@ __global__ void __launch_bounds__(256, FJG_FORCE_MINB) k_force_insert(const DevT
   bool sawdup = false;  // a repeated key: flagged once per block at the end (one hot address)
   uint32_t wins = 0;     // slots this thread claimed (new keys), summed once per block at the end
   // block-uniform trip count (the end-of-kernel block reduction needs every thread)
+  // optimistic members copy their (at most two: k_force_clear checks) clustered
+  // columns in place; the pointers are loaded once
+  const int32_t *osrc0 = nullptr, *osrc1 = nullptr;
+  int32_t *odst0 = nullptr, *odst1 = nullptr;
+  if (opt)
+    for (int c = 0; c < T.ncols; ++c)
+      if (L.cval[c]) {
+        if (!odst0) {
+          osrc0 = level_src(T, lev, c);
+          odst0 = L.cval[c];
+        } else {
+          osrc1 = level_src(T, lev, c);
+          odst1 = L.cval[c];
+        }
+      }
   for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < total; b0 += gridDim.x * blockDim.x) {
     const uint32_t i = b0 + threadIdx.x;
+    const bool live = i < total;
     bool won = false;
     uint64_t h = 0;
-    uint32_t p = 0;
-    if (i < total) {
-      uint32_t len, pos;
+    uint32_t p = 0, len = 0, pos = 0;
+    if (live) {
       force_locate(R, i, p, len, pos);
       int32_t vals[MAXK];
 #pragma unroll
@@ -193,6 +225,15 @@ __global__ void __launch_bounds__(256, FJG_FORCE_MINB) k_force_insert(const DevT
         }
         if (++h == hi) h = lo;
       }
+    }
+    // Reconverge the warp (every lane reaches this: the trip count is block
+    // uniform). Lanes leave the probe loop at different times; left alone, the
+    // early ones run ahead into the stores and the next trip, the warp splits
+    // into fragments of ~13 lanes and every coalesced load and store of a trip
+    // is issued once per fragment (ncu source view: 2x the instructions, L2
+    // sectors and DRAM bytes of the converged kernel).
+    if (OPTK) __syncwarp();
+    if (live) {
       if (opt) {
         // unit child group of this row (force_unique_body's work, same thread)
         L.cnt[pos] = 1;
@@ -200,10 +241,8 @@ __global__ void __launch_bounds__(256, FJG_FORCE_MINB) k_force_insert(const DevT
           L.sn[p].nkeys = len;
           L.cursor[p] = len;
         }
-        for (int c = 0; c < T.ncols; ++c) {
-          int32_t* out = L.cval[c];
-          if (out) out[pos] = level_src(T, lev, c)[pos];
-        }
+        if (odst0) odst0[pos] = osrc0[pos];
+        if (odst1) odst1[pos] = osrc1[pos];
       } else {
         const uint32_t rank = won ? 0u : (atomicAdd(&L.table[h].q, 1u) & ~kPendBit);
         tmp_slot[pos] = (uint32_t)h;
@@ -211,6 +250,7 @@ __global__ void __launch_bounds__(256, FJG_FORCE_MINB) k_force_insert(const DevT
       }
     }
     wins += won ? 1u : 0u;
+    if (OPTK) __syncwarp();
   }
   // new keys and the repeated-key flag: one atomic per block (k_force_assign
   // finds the new slots as the rank-0 offsets, so no slot list is appended)
