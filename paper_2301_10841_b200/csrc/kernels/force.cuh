@@ -126,6 +126,9 @@ __global__ void k_force_clear(const DevTrie* __restrict__ tries, const __grid_co
 #ifndef FJG_FORCE_MINB
 #define FJG_FORCE_MINB 4
 #endif
+#ifndef FJG_FORCE_SYNC_ALL
+#define FJG_FORCE_SYNC_ALL 0  // 1: roots reconverge every trip too
+#endif
 // OPTK: the kernel of a batch that may hold optimistic members (level >= 1,
 // one-column keys); roots and multi-column keys run the plain instantiation
 // (48 registers, 5 blocks per SM, no per-trip reconvergence: on a root's wide
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(256, OPTK ? FJG_FORCE_MINB : 5) k_force_insert
     // into fragments of ~13 lanes and every coalesced load and store of a trip
     // is issued once per fragment (ncu source view: 2x the instructions, L2
     // sectors and DRAM bytes of the converged kernel).
-    if (OPTK) __syncwarp();
+    if (OPTK || FJG_FORCE_SYNC_ALL) __syncwarp();
     if (live) {
       if (opt) {
         // unit child group of this row (force_unique_body's work, same thread)
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(256, OPTK ? FJG_FORCE_MINB : 5) k_force_insert
       }
     }
     wins += won ? 1u : 0u;
-    if (OPTK) __syncwarp();
+    if (OPTK || FJG_FORCE_SYNC_ALL) __syncwarp();
   }
   // new keys and the repeated-key flag: one atomic per block (k_force_assign
   // finds the new slots as the rank-0 offsets, so no slot list is appended)
