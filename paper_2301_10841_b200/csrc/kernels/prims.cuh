@@ -257,7 +257,13 @@ __global__ void k_reduce_max_u32(const uint32_t* __restrict__ in, uint64_t n, ui
 // ---------------------------------------------------------------------------
 // radix sort of (u32 key, u32 value) pairs
 // ---------------------------------------------------------------------------
-constexpr int kRadixThreads = 512, kRadixItems = 16, kRadixTile = kRadixThreads * kRadixItems;
+#ifndef FJG_RADIX_ITEMS
+#define FJG_RADIX_ITEMS 16
+#endif
+#ifndef FJG_RADIX_MINB
+#define FJG_RADIX_MINB 2
+#endif
+constexpr int kRadixThreads = 512, kRadixItems = FJG_RADIX_ITEMS, kRadixTile = kRadixThreads * kRadixItems;
 constexpr int kRadixBins = 512, kRadixMaxPasses = 4, kRadixWarps = kRadixThreads / 32;
 constexpr size_t kRadixSmem = (size_t)kRadixTile * 8 + (size_t)kRadixWarps * kRadixBins * 2 + kRadixBins * 8 + 64;
 
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* __restrict__
 
 // One pass: digit = (key >> shift) & (2^dbits - 1), dbits <= 9; stable.
 // Look-back word per (tile, digit): epoch << 34 | flag << 32 | count.
-__global__ void __launch_bounds__(kRadixThreads, 2) k_radix_pass(const uint32_t* __restrict__ kin,
+__global__ void __launch_bounds__(kRadixThreads, FJG_RADIX_MINB) k_radix_pass(const uint32_t* __restrict__ kin,
                                                                  const uint32_t* __restrict__ vin,
                                                                  uint32_t* __restrict__ kout,
                                                                  uint32_t* __restrict__ vout, uint64_t n, int shift,
