@@ -478,6 +478,18 @@ __device__ __forceinline__ void gj_load_bind(const KNode& N, const uint64_t* __r
   }
 }
 
+// Three-subatom GJ nodes: candidates alive after the first probe wait in a
+// per-warp ring and the second probe runs on full batches of 32 (C4: 27% of
+// the candidates survive the first probe, so probing the second subatom in
+// place ran every step at a quarter of its lanes).
+template <int NS>
+struct GjStage1 {
+  static constexpr int NW = TILE / 32, QC = NS == 3 ? FJG_GJ_QC : 1;
+  int32_t x[NW][QC];
+  uint32_t e[NW][QC], q0[NW][QC], p1[NW][QC], len1[NW][QC];
+  uint8_t c[NW][QC];
+};
+
 // GJ-shaped last node, warp-uniform bindings: a warp walks chunks of 64 * RR
 // consecutive candidates (tickets from a device counter, as k_last_gj_bf) in
 // double steps of 64 (lane l takes candidates base + l and base + 32 + l, so
@@ -496,6 +508,8 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
                                                                     uint64_t out_cap = 0) {
   static_assert(64 + 63 < HitQueue<NS>::QC, "k_last_gj_warp: survivor ring too small");
   __shared__ HitQueue<NS> Q;
+  __shared__ GjStage1<NS> S1;
+  uint32_t h1 = 0, t1 = 0;  // stage-1 ring cursors (NS == 3), warp-uniform
   uint64_t acc_lo = 0, acc_hi = 0, acc_sum = 0, probes = 0, misses = 0, body = 0;
   long long acc_min = LLONG_MAX;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -574,7 +588,68 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
     }
   };
   // probe candidate x of a binding in its probed regions; survivors enqueue
+  // second probe of 32 (or the last n) stage-1 entries, one per lane
+  auto stage2 = [&](uint32_t n) {
+    if (NS != 3) return;
+    const bool live = (uint32_t)lane < n;
+    const uint32_t slot = (h1 + lane) & (GjStage1<NS>::QC - 1);
+    int32_t x = 0;
+    uint32_t eb = 0, q0 = 0, q1 = kEmpty;
+    int ci = 0;
+    if (live) {
+      x = S1.x[wi][slot];
+      eb = S1.e[wi][slot];
+      q0 = S1.q0[wi][slot];
+      ci = S1.c[wi][slot];
+      const uint32_t p1 = S1.p1[wi][slot], len1 = S1.len1[wi][slot];
+      const Slot* tb = 1 >= ci ? N.sub[NS - 1].table : N.sub[1].table;
+      ++probes;
+      const uint32_t kw = (uint32_t)x;
+      uint64_t b = region_bucket(p1, len1, kw);
+      bool more;
+      q1 = bucket_match(ld_bucket(tb, b), kw, more);
+      while (more) {
+        if (++b == region_hi(p1, len1)) b = region_lo(p1);
+        q1 = bucket_match(ld_bucket(tb, b), kw, more);
+      }
+      if (q1 == kEmpty) ++misses;
+    }
+    h1 += n;
+    uint32_t qv[NS - 1];
+    qv[0] = q0;
+    if (NS == 3) qv[NS - 2] = q1;
+    enqueue(live && q1 != kEmpty, x, eb, ci, qv);
+  };
   auto probe_one = [&](bool live, int32_t x, const GjBind<NS>& B) {
+    if (NS == 3) {  // first probe here, survivors queue for stage2
+      uint32_t q = kEmpty;
+      if (live) {
+        const Slot* tb = 0 >= B.ci ? N.sub[1].table : N.sub[0].table;
+        ++probes;
+        const uint32_t kw = (uint32_t)x;
+        uint64_t b = region_bucket(B.p[0], B.len[0], kw);
+        bool more;
+        q = bucket_match(ld_bucket(tb, b), kw, more);
+        while (more) {
+          if (++b == region_hi(B.p[0], B.len[0])) b = region_lo(B.p[0]);
+          q = bucket_match(ld_bucket(tb, b), kw, more);
+        }
+        if (q == kEmpty) ++misses;
+      }
+      const bool hit = live && q != kEmpty;
+      const unsigned hm = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const uint32_t slot = (t1 + __popc(hm & lt_mask)) & (GjStage1<NS>::QC - 1);
+        S1.x[wi][slot] = x;
+        S1.e[wi][slot] = B.eb;
+        S1.q0[wi][slot] = q;
+        S1.c[wi][slot] = (uint8_t)B.ci;
+        S1.p1[wi][slot] = B.p[NS - 2];
+        S1.len1[wi][slot] = B.len[NS - 2];
+      }
+      t1 += __popc(hm);
+      return;
+    }
     uint32_t qv[NS - 1];
 #pragma unroll
     for (int j = 0; j < NS - 1; ++j) {
@@ -717,6 +792,20 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
           }
         }
       }
+      if (NS == 3) {  // second probes on full batches (at most 64 + 31 stage-1 entries pending)
+        while (t1 - h1 >= 32) {
+          __syncwarp();  // the stage-1 entries other lanes wrote
+          stage2(32);
+          if (tail - head >= 32) {
+            __syncwarp();
+            do {
+              fold(head, 32);
+              head += 32;
+            } while (tail - head >= 32);
+          }
+        }
+        __syncwarp();
+      }
       // warp-convergent: fold full batches of 32 (at most 64 + 31 pending)
       if (tail - head >= 32) {
         __syncwarp();  // the ring entries other lanes wrote
@@ -729,6 +818,17 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
     }
   }
   __syncwarp();
+  if (NS == 3) {
+    while (t1 != h1) {
+      stage2(min(32u, t1 - h1));
+      __syncwarp();
+      if (tail - head >= 32) {
+        fold(head, 32);
+        head += 32;
+        __syncwarp();
+      }
+    }
+  }
   fold(head, tail - head);
   probes = warp_sum(probes);
   misses = warp_sum(misses);
