@@ -209,6 +209,31 @@ def test_int64_columns_narrowed_on_device(engine):
             engine.relation_i64([bad, b])
 
 
+def test_optimistic_force_redo_on_repeated_keys(engine):
+    """Level >= 1 forces insert optimistically (every key of a subtrie distinct) and redo a member with the
+    counting protocol when a repeated key shows up: a multigraph triangle whose early subtries are duplicate
+    free and whose later ones repeat keys, under small batches (several force batches per execution: optimistic,
+    then redo, then the level's dup flag routes later batches to the counting protocol), executed twice."""
+    rng = np.random.default_rng(11)
+    n = 6000
+    src = rng.integers(0, 300, n).astype(np.int32)
+    dst = rng.integers(0, 300, n).astype(np.int32)
+    clean = np.unique(np.stack([src, dst], 1), axis=0)  # duplicate-free prefix ...
+    dup = clean[rng.integers(len(clean) // 2, len(clean), 2000)]  # ... then repeats of the upper half
+    e = np.concatenate([clean, dup])
+    cols = [np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1])]
+    q = [{"rel": "E1", "vars": ["a", "b"]}, {"rel": "E2", "vars": ["b", "c"]}, {"rel": "E3", "vars": ["a", "c"]}]
+    plan = P.compile_plan({"query": q, "binary_plan": configs.left_deep(["E1", "E2", "E3"])}, "generic")
+    for dyn in (True, False):
+        for bs in (0, 997, 64):
+            r, ref = check(engine, q, plan, [cols] * 3, shared=[0, 0, 0], dynamic_cover=dyn, batch_size=bs)
+            assert r.count > 0
+    rel = engine.relation(cols)
+    qq = engine.query({"query": q}, plan, [rel] * 3)
+    a, b = qq.execute(batch_size=500), qq.execute(batch_size=500)
+    assert (a.count, a.checksum) == (b.count, b.checksum)
+
+
 def test_counters(engine):
     """ExecStats: probes/misses/body entries agree with the oracle where forcing order is pinned (chain)."""
     w = configs.chain(n=20000, domain=30000)
