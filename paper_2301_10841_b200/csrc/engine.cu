@@ -332,6 +332,7 @@ struct PhysTrieHost {
   bool root_forced = false;
   int map_levels = 0;  // levels that are maps in some sharing atom's GHT schema (SIMPLE / SLT eager builds)
   int key_bits = 32;   // bits used by the root key column (sorted roots: radix-sort end bit)
+  uint64_t root_key_bound = 1;  // buckets of the root's slot region (rows; a sorted root: its possible distinct keys)
 };
 
 struct AtomInfo {
@@ -456,6 +457,7 @@ struct fjg_query {
 // ============================================================================
 // query preparation
 // ============================================================================
+static bool root_sorted_path(const fjg_query* q, int t);  // (defined with the root force below)
 static void prepare_query(fjg_query* q) {
   using fj::EngineError;
   using fj::ValidationError;
@@ -538,6 +540,42 @@ static void prepare_query(fjg_query* q) {
     const int ml = (int)levels.size() - (last_is_cover ? 1 : 0);
     q->tries[found].map_levels = std::max(q->tries[found].map_levels, ml);
   }
+  // Roots forced by radix sort sort only the bits their key column uses (its
+  // largest value as uint32; negative keys use all 32): one reduction per such
+  // trie here, at query creation, instead of a fourth sort pass per execution.
+  // The same bound sizes the root's slot region: a sorted root keeps one bucket
+  // per distinct key, and there are at most min(rows, largest key + 1) of them
+  // (C5: 2^27 buckets = 4.3 GB instead of 17 GB for the 512M-row relation).
+  {
+    std::vector<int> sorted;
+    for (size_t t = 0; t < q->tries.size(); ++t) {
+      auto& T = q->tries[t];
+      T.root_key_bound = std::max<uint64_t>(T.rel->nrows, 1);
+      if (T.levels[0].empty() && root_sorted_path(q, (int)t)) T.root_key_bound = 1;
+      if (T.levels[0].size() == 1 && T.rel->nrows >= (1u << 21)) sorted.push_back((int)t);
+    }
+    if (!sorted.empty()) {
+      fjg_engine* eng = q->eng;
+      uint32_t* dmax = (uint32_t*)eng->pool->alloc(sorted.size() * 4);
+      for (size_t i = 0; i < sorted.size(); ++i) {
+        auto& T = q->tries[sorted[i]];
+        const uint32_t* col = reinterpret_cast<const uint32_t*>(T.rel->cols[T.levels[0][0]]);
+        prim_max_u32(eng, col, T.rel->nrows, dmax + i);
+      }
+      std::vector<uint32_t> hmax(sorted.size());
+      CK(cudaMemcpyAsync(hmax.data(), dmax, sorted.size() * 4, cudaMemcpyDeviceToHost, eng->stream));
+      CK(cudaStreamSynchronize(eng->stream));
+      for (size_t i = 0; i < sorted.size(); ++i) {
+        auto& T = q->tries[sorted[i]];
+        int bits = 1;
+        while (bits < 32 && (hmax[i] >> bits)) ++bits;
+        T.key_bits = bits;
+        if (root_sorted_path(q, sorted[i]))
+          T.root_key_bound = std::min<uint64_t>(T.root_key_bound, (uint64_t)hmax[i] + 1);
+      }
+      eng->pool->free(dmax);
+    }
+  }
   // allocate trie storage
   for (size_t t = 0; t < q->tries.size(); ++t) {
     auto& T = q->tries[t];
@@ -557,7 +595,8 @@ static void prepare_query(fjg_query* q) {
       H.keycols = T.levels[l];
       H.multi = H.keycols.size() >= 2;
       H.nsub = l == 0 ? 1 : std::max<uint64_t>(n, 1);
-      H.cap = 4ull * FJG_RS * std::max<uint64_t>(n, 1);  // FJG_RS 4-slot buckets per position: per-subtrie regions
+      // FJG_RS 4-slot buckets per position (per-subtrie regions); a sorted root: per possible distinct key
+      H.cap = 4ull * FJG_RS * (l == 0 ? T.root_key_bound : std::max<uint64_t>(n, 1));
       L.table = (Slot*)q->alloc(H.cap * sizeof(Slot));
       L.srep = H.multi ? (uint32_t*)q->alloc(H.cap * 4) : nullptr;
       L.sn = (SubState*)q->alloc(H.nsub * sizeof(SubState));
@@ -646,32 +685,6 @@ static void prepare_query(fjg_query* q) {
   std::vector<DevTrie> dt;
   for (auto& T : q->tries) dt.push_back(T.dev);
   CK(cudaMemcpyAsync(q->d_tries, dt.data(), dt.size() * sizeof(DevTrie), cudaMemcpyHostToDevice, q->eng->stream));
-  // Roots forced by radix sort sort only the bits their key column uses (its
-  // largest value as uint32; negative keys use all 32): one reduction per such
-  // trie here, at query creation, instead of a fourth sort pass per execution.
-  std::vector<int> sorted;
-  for (size_t t = 0; t < q->tries.size(); ++t) {
-    const auto& T = q->tries[t];
-    if (T.levels[0].size() == 1 && T.rel->nrows >= (1u << 21)) sorted.push_back((int)t);
-  }
-  if (!sorted.empty()) {
-    fjg_engine* eng = q->eng;
-    uint32_t* dmax = (uint32_t*)eng->pool->alloc(sorted.size() * 4);
-    for (size_t i = 0; i < sorted.size(); ++i) {
-      auto& T = q->tries[sorted[i]];
-      const uint32_t* col = reinterpret_cast<const uint32_t*>(T.dev.base[T.dev.lev[0].keycol[0]]);
-      prim_max_u32(eng, col, T.rel->nrows, dmax + i);
-    }
-    std::vector<uint32_t> hmax(sorted.size());
-    CK(cudaMemcpyAsync(hmax.data(), dmax, sorted.size() * 4, cudaMemcpyDeviceToHost, eng->stream));
-    CK(cudaStreamSynchronize(eng->stream));
-    for (size_t i = 0; i < sorted.size(); ++i) {
-      int bits = 1;
-      while (bits < 32 && (hmax[i] >> bits)) ++bits;
-      q->tries[sorted[i]].key_bits = bits;
-    }
-    eng->pool->free(dmax);
-  }
 }
 
 // Resolve each node's descriptor into the constant-bank kernel plan.
