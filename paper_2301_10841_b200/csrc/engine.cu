@@ -608,9 +608,12 @@ static void prepare_query(fjg_query* q) {
       L.nk = (int)H.keycols.size();
       for (int i = 0; i < L.nk; ++i) L.keycol[i] = H.keycols[i];
       if (l > 0) {
-        L.list_p = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
-        L.list_len = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
-        L.list_scan = (uint32_t*)q->alloc(std::max<uint64_t>(n, 1) * 4);
+        // claim lists: one entry per subtrie of this level at most; level 1's
+        // subtries are the root's child groups (a sorted root: its key bound)
+        const uint64_t nl = l == 1 ? std::min<uint64_t>(std::max<uint64_t>(n, 1), T.root_key_bound) : std::max<uint64_t>(n, 1);
+        L.list_p = (uint32_t*)q->alloc(nl * 4);
+        L.list_len = (uint32_t*)q->alloc(nl * 4);
+        L.list_scan = (uint32_t*)q->alloc(nl * 4);
       }
     }
   }
