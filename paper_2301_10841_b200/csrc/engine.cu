@@ -1465,7 +1465,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
       const bool gj_fast = gj_any;
       if (gj_fast) {
-        chunk_owners(q, gscan, F, c0, c1, FJG_GJW ? 64 * FJG_GJW_RR : 32 * FJG_GJ_R);
+        chunk_owners(q, gscan, F, c0, c1, FJG_GJW ? 64 * (N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR) : 32 * FJG_GJ_R);
         if (FJG_GJ_TICKET)
           CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, ticket), 0, 8, eng->stream));
       }
@@ -1474,7 +1474,8 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
       if (mode == EXPAND_ENUM && gj_fast) {  // k_last_gj_warp writing the tuples
         const int W8 = q->head.size() <= 4 ? 4 : 8;
-        const uint64_t nch = (c1 - c0 + 64 * FJG_GJW_RR - 1) / (64 * FJG_GJW_RR);
+        const uint64_t rr = N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR;
+        const uint64_t nch = (c1 - c0 + 64 * rr - 1) / (64 * rr);
         const unsigned gw = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * FJG_GJW_MINB));
         if (N.nsub == 2 && W8 == 4)
@@ -1484,10 +1485,10 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
           LAUNCH(eng, (k_last_gj_warp<2, 8, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
                           KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
         else if (W8 == 4)
-          LAUNCH(eng, (k_last_gj_warp<3, 4, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
+          LAUNCH(eng, (k_last_gj_warp<3, 4, FJG_GJW_RR3, true><<<gw, TILE, 0, eng->stream>>>(
                           KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
         else
-          LAUNCH(eng, (k_last_gj_warp<3, 8, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
+          LAUNCH(eng, (k_last_gj_warp<3, 8, FJG_GJW_RR3, true><<<gw, TILE, 0, eng->stream>>>(
                           KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
       } else if (mode == EXPAND_ENUM)
         LAUNCH(eng, launch_expand<EXPAND_ENUM>(q->width, g, eng->stream, KN, c0, c1, F, q->bounds, q->min_var,
@@ -1497,7 +1498,8 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
                                                q->d_ctr));
       else if (gj_fast && FJG_GJW) {  // k_last_gj_warp: x is the last head variable
         const int W8 = q->head.size() <= 4 ? 4 : 8;
-        const uint64_t nch = (c1 - c0 + 64 * FJG_GJW_RR - 1) / (64 * FJG_GJW_RR);
+        const uint64_t rr = N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR;
+        const uint64_t nch = (c1 - c0 + 64 * rr - 1) / (64 * rr);
         const unsigned gw = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * FJG_GJW_MINB));
         if (N.nsub == 2 && W8 == 4)
@@ -1507,10 +1509,10 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
           LAUNCH(eng, (k_last_gj_warp<2, 8, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
                                                                                       perm, q->min_var, q->d_ctr)));
         else if (W8 == 4)
-          LAUNCH(eng, (k_last_gj_warp<3, 4, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+          LAUNCH(eng, (k_last_gj_warp<3, 4, FJG_GJW_RR3><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
                                                                                       perm, q->min_var, q->d_ctr)));
         else
-          LAUNCH(eng, (k_last_gj_warp<3, 8, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
+          LAUNCH(eng, (k_last_gj_warp<3, 8, FJG_GJW_RR3><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
                                                                                       perm, q->min_var, q->d_ctr)));
       } else if (gj_fast) {  // k_last_gj_bf: x is the last head variable
         const int W8 = q->head.size() <= 4 ? 4 : 8;

@@ -420,6 +420,9 @@ __global__ void k_gather_m(const uint64_t* __restrict__ m, const uint32_t* __res
 #ifndef FJG_GJW_RR
 #define FJG_GJW_RR 4  // 64-candidate double steps per warp chunk (chunk = 64 * RR candidates)
 #endif
+#ifndef FJG_GJW_RR3
+#define FJG_GJW_RR3 1  // three-subatom nodes (C4): one double step per chunk (last node 71.6 -> 70.2 ms; 2: 70.9, 4: 71.6, 8: 74.5)
+#endif
 #ifndef FJG_GJW_MINB
 #define FJG_GJW_MINB 5  // 48 registers: C5 last node 1017 -> 973 ms vs 6 blocks (40 registers + spills)
 #endif
