@@ -16,7 +16,7 @@
 //              lowest position), candidate count, claims of unforced subtries
 //              every probe/keys-iteration of this node needs (lazy forcing in
 //              batch, deduplicated by CAS on the subtrie state)
-//   scan       inclusive scan of candidate counts (CUB)
+//   scan       inclusive scan of candidate counts (kernels/prims.cuh: decoupled look-back)
 //   force      per (trie, level) with claims: insert -> assign -> scatter
 //   k_expand   per candidate (load-balanced over the scan): iterate the cover,
 //              probe every other subatom in node order, drop misses, compact
@@ -1477,7 +1477,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
         const uint64_t rr = N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR;
         const uint64_t nch = (c1 - c0 + 64 * rr - 1) / (64 * rr);
         const unsigned gw = (unsigned)std::max<uint64_t>(
-            1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * FJG_GJW_MINB));
+            1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * (N.nsub == 3 ? FJG_GJW_MINB3 : FJG_GJW_MINB)));
         if (N.nsub == 2 && W8 == 4)
           LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
                           KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
@@ -1501,7 +1501,7 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
         const uint64_t rr = N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR;
         const uint64_t nch = (c1 - c0 + 64 * rr - 1) / (64 * rr);
         const unsigned gw = (unsigned)std::max<uint64_t>(
-            1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * FJG_GJW_MINB));
+            1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * (N.nsub == 3 ? FJG_GJW_MINB3 : FJG_GJW_MINB)));
         if (N.nsub == 2 && W8 == 4)
           LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
                                                                                       perm, q->min_var, q->d_ctr)));

@@ -420,6 +420,12 @@ __global__ void k_gather_m(const uint64_t* __restrict__ m, const uint32_t* __res
 #ifndef FJG_GJW_RR
 #define FJG_GJW_RR 4  // 64-candidate double steps per warp chunk (chunk = 64 * RR candidates)
 #endif
+#ifndef FJG_GJW_MINB3
+#define FJG_GJW_MINB3 5
+#endif
+#ifndef FJG_GJ_TICKET3
+#define FJG_GJ_TICKET3 FJG_GJ_TICKET
+#endif
 #ifndef FJG_GJW_RR3
 #define FJG_GJW_RR3 1  // three-subatom nodes (C4): one double step per chunk (last node 71.6 -> 70.2 ms; 2: 70.9, 4: 71.6, 8: 74.5)
 #endif
@@ -503,7 +509,7 @@ struct GjStage1 {
 // walks each lane to its own binding. Survivors are folded from the per-warp
 // ring exactly as in k_last_gj_bf.
 template <int NS, int W, int RR, bool ENUMR = false>
-__global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __grid_constant__ KNode N, uint64_t c0,
+__global__ void __launch_bounds__(TILE, NS == 3 ? FJG_GJW_MINB3 : FJG_GJW_MINB) k_last_gj_warp(const __grid_constant__ KNode N, uint64_t c0,
                                                                     uint64_t c1, uint64_t F,
                                                                     const uint32_t* __restrict__ owner,
                                                                     const uint32_t* __restrict__ perm, int min_var,
@@ -684,9 +690,9 @@ __global__ void __launch_bounds__(TILE, FJG_GJW_MINB) k_last_gj_warp(const __gri
   auto next_chunk = [&]() -> uint64_t {
     if (tk == tk_end) {
       unsigned long long t0 = 0;
-      if (lane == 0) t0 = atomicAdd(&ctr->ticket, (unsigned long long)FJG_GJ_TICKET);
+      if (lane == 0) t0 = atomicAdd(&ctr->ticket, (unsigned long long)(NS == 3 ? FJG_GJ_TICKET3 : FJG_GJ_TICKET));
       tk = __shfl_sync(0xffffffffu, t0, 0);
-      tk_end = tk + FJG_GJ_TICKET;
+      tk_end = tk + (NS == 3 ? FJG_GJ_TICKET3 : FJG_GJ_TICKET);
     }
     return tk++;
   };
