@@ -1460,12 +1460,16 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
     const uint32_t* perm = gj_any ? probe_region_order(q, k, KN, F, gscan) : nullptr;
     KNode KP = KN;
     KP.scan = gscan;
+    // double steps per ticketed chunk: 4 when the bindings were ordered by probe region (tries larger than
+    // L2: C5 1025 vs 1170 ms at 1), 1 otherwise (C2 3.36 vs 3.44 ms at 4; three-subatom nodes: C4)
+    const bool rr_small = perm == nullptr;
+    const uint64_t rr_gj = N.nsub == 3 ? FJG_GJW_RR3 : (rr_small ? FJG_GJW_RR_UNSORTED : FJG_GJW_RR);
     for (uint64_t c0 = 0; c0 < M; c0 += kLastChunk) {
       const uint64_t c1 = std::min(M, c0 + kLastChunk);
       const uint64_t ntiles = (c1 - c0 + TILE - 1) / TILE;
       const bool gj_fast = gj_any;
       if (gj_fast) {
-        chunk_owners(q, gscan, F, c0, c1, FJG_GJW ? 64 * (N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR) : 32 * FJG_GJ_R);
+        chunk_owners(q, gscan, F, c0, c1, FJG_GJW ? 64 * rr_gj : 32 * FJG_GJ_R);
         if (FJG_GJ_TICKET)
           CK(cudaMemsetAsync(reinterpret_cast<char*>(q->d_ctr) + offsetof(DevCounters, ticket), 0, 8, eng->stream));
       }
@@ -1474,11 +1478,17 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
       const unsigned g = grid_for(c1 - c0, TILE, eng->num_sms * 8);
       if (mode == EXPAND_ENUM && gj_fast) {  // k_last_gj_warp writing the tuples
         const int W8 = q->head.size() <= 4 ? 4 : 8;
-        const uint64_t rr = N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR;
+        const uint64_t rr = rr_gj;
         const uint64_t nch = (c1 - c0 + 64 * rr - 1) / (64 * rr);
         const unsigned gw = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * (N.nsub == 3 ? FJG_GJW_MINB3 : FJG_GJW_MINB)));
-        if (N.nsub == 2 && W8 == 4)
+        if (N.nsub == 2 && W8 == 4 && rr_small)
+          LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR_UNSORTED, true><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
+        else if (N.nsub == 2 && rr_small)
+          LAUNCH(eng, (k_last_gj_warp<2, 8, FJG_GJW_RR_UNSORTED, true><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
+        else if (N.nsub == 2 && W8 == 4)
           LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR, true><<<gw, TILE, 0, eng->stream>>>(
                           KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr, q->out_tuples, q->out_cap)));
         else if (N.nsub == 2)
@@ -1498,11 +1508,17 @@ static void run_node(fjg_query* q, int k, uint64_t F, int mode) {
                                                q->d_ctr));
       else if (gj_fast && FJG_GJW) {  // k_last_gj_warp: x is the last head variable
         const int W8 = q->head.size() <= 4 ? 4 : 8;
-        const uint64_t rr = N.nsub == 3 ? FJG_GJW_RR3 : FJG_GJW_RR;
+        const uint64_t rr = rr_gj;
         const uint64_t nch = (c1 - c0 + 64 * rr - 1) / (64 * rr);
         const unsigned gw = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>((nch + TILE / 32 - 1) / (TILE / 32), (uint64_t)eng->num_sms * (N.nsub == 3 ? FJG_GJW_MINB3 : FJG_GJW_MINB)));
-        if (N.nsub == 2 && W8 == 4)
+        if (N.nsub == 2 && W8 == 4 && rr_small)
+          LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR_UNSORTED><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr)));
+        else if (N.nsub == 2 && rr_small)
+          LAUNCH(eng, (k_last_gj_warp<2, 8, FJG_GJW_RR_UNSORTED><<<gw, TILE, 0, eng->stream>>>(
+                          KP, c0, c1, F, q->chunk_owner, perm, q->min_var, q->d_ctr)));
+        else if (N.nsub == 2 && W8 == 4)
           LAUNCH(eng, (k_last_gj_warp<2, 4, FJG_GJW_RR><<<gw, TILE, 0, eng->stream>>>(KP, c0, c1, F, q->chunk_owner,
                                                                                       perm, q->min_var, q->d_ctr)));
         else if (N.nsub == 2)

@@ -420,6 +420,9 @@ __global__ void k_gather_m(const uint64_t* __restrict__ m, const uint32_t* __res
 #ifndef FJG_GJW_RR
 #define FJG_GJW_RR 4  // 64-candidate double steps per warp chunk (chunk = 64 * RR candidates)
 #endif
+#ifndef FJG_GJW_RR_UNSORTED
+#define FJG_GJW_RR_UNSORTED 1  // double steps per chunk when the bindings are not ordered by probe region (C2)
+#endif
 #ifndef FJG_GJW_MINB3
 #define FJG_GJW_MINB3 5
 #endif
