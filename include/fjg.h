@@ -63,8 +63,9 @@ typedef struct fjg_query fjg_query;
 
 /* ExecOptions. batch_size is the iter_batch size of
  * Fig 13: on the device it bounds the number of cover
- * candidates expanded per node launch (0 = engine default, 2^25; at most
- * 2^31, else FJG_E_VALIDATION). */
+ * candidates expanded per node launch (0 = engine default: 2^25, up to 2^27
+ * when the largest relation has more than 2^22 rows; at most 2^31, else
+ * FJG_E_VALIDATION). */
 typedef struct {
   uint64_t batch_size;
   int32_t dynamic_cover; /* §4.4 select_cover */

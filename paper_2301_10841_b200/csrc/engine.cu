@@ -2191,7 +2191,16 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     o.min_var = -1;
     if (opts) o = *opts;
     if (o.min_var >= (int)q->head.size()) throw fj::ValidationError("min_var out of range");
-    uint64_t batch = o.batch_size ? o.batch_size : (1ull << 25);
+    // engine default: 2^25 candidates per node launch, up to 2^27 for large inputs (8 x the largest relation):
+    // larger frontier batches give the probe-region ordering of the last node more bindings per region
+    // (C5 1025 -> 994 ms, C4 103.3 -> 99.7 ms at 2^27; 2^28 and up: equal) at 49 B of frontier per entry
+    // and node. Factorised-count mode keeps 2^25 (the memoised chain count's frontier is one node deep).
+    uint64_t batch = o.batch_size;
+    if (!batch) {
+      batch = 1ull << 25;
+      if (o.output_mode != FJG_OUT_FACTORIZED_COUNT)
+        while (batch < 8 * q->max_n && batch < (1ull << 27)) batch <<= 1;
+    }
     if (batch > kLastChunk) throw fj::ValidationError("batch_size must be <= " + std::to_string(kLastChunk));
     ensure_frontiers(q, batch);
     q->dynamic = o.dynamic_cover != 0;
