@@ -524,7 +524,10 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", f"r02_traffic_{w.name}.json")
     if os.path.exists(tp) and world == 1 and dom == "last":
         with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        # per launch of THIS run: the capture's DRAM bytes per execution over the run's launch count
+        traffic = (tj["dram_bytes_per_execution"] / max(r0.last_node_launches, 1)
+                   if "dram_bytes_per_execution" in tj else tj.get("dram_bytes_per_launch"))
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
