@@ -976,6 +976,18 @@ static void prepare_chain(fjg_query* q) {
   q->memo_top.memo_gid = q->memo_passes[0].gid;
 }
 
+// Bytes ensure_frontiers allocates per unit of capacity (all nodes).
+static uint64_t frontier_entry_bytes(const fjg_query* q) {
+  uint64_t b = 0;
+  const size_t K = q->nodes.size();
+  for (size_t k = 0; k < K; ++k) {
+    const DevNode& N = q->nodes[k];
+    if (k > 0) b += 1 + 8 + 8;  // chosen, m, scan
+    if (k + 1 < K) b += 4ull * __builtin_popcount(N.out_vars) + 8ull * __builtin_popcount(N.out_atoms) + 8;
+  }
+  return b;
+}
+
 // (Re)allocate per-node frontier buffers for a candidate capacity `cap`.
 static void ensure_frontiers(fjg_query* q, uint64_t cap) {
   if (q->cap >= cap && q->cap) return;
@@ -2199,7 +2211,9 @@ int fjg_execute(fjg_query* q, const fjg_exec_options* opts, fjg_result* out) {
     if (!batch) {
       batch = 1ull << 25;
       if (o.output_mode != FJG_OUT_FACTORIZED_COUNT)
-        while (batch < 8 * q->max_n && batch < (1ull << 27)) batch <<= 1;
+        // (while the frontier buffers of all nodes stay under 32 GiB: wide or deep plans keep smaller batches)
+        while (batch < 8 * q->max_n && batch < (1ull << 27) && 2 * batch * frontier_entry_bytes(q) <= (32ull << 30))
+          batch <<= 1;
     }
     if (batch > kLastChunk) throw fj::ValidationError("batch_size must be <= " + std::to_string(kLastChunk));
     ensure_frontiers(q, batch);
